@@ -426,6 +426,51 @@ def integrate(prob, state, fibers=None):
     return value, log10, sign, n_evals
 
 
+def _dd_weighted_sum(F, w):
+    """sum_a w_a F[..., a] in double-double (Dekker products, Knuth sums), vectorised."""
+    from .integrand import _two_prod
+    hi = np.zeros(F.shape[:-1])
+    lo = np.zeros(F.shape[:-1])
+    for a in range(F.shape[-1]):
+        p, e = _two_prod(np.full(hi.shape, w[a]), F[..., a])
+        s = hi + p
+        bb = s - hi
+        err = (hi - (s - bb)) + (p - bb)
+        lo = lo + err + e
+        hi = s + lo
+        lo = lo - (hi - s)
+    return hi, lo
+
+
+def integrate_exact(prob, state, fibers=None, dps=50):
+    """The §4.1 product (4/d!) W_0 M_0^{-1} ... W_{d-1} evaluated (nearly) exactly for the
+    given fp64 fiber entries: W sums in double-double, the chain in mpmath at ``dps``
+    digits.  DESIGN.md R9: this -- not the fp64 evaluation, whose error grows like
+    cond(M_i) * eps -- is what the CUDA path's double-double contraction is compared with.
+    Returns (value, log10|value|, sign)."""
+    import mpmath
+    d = prob.d
+    fibers = tt_fibers(prob, state) if fibers is None else fibers
+    with mpmath.workdps(dps):
+        v = None
+        for m in range(d):
+            hi, lo = _dd_weighted_sum(fibers[m], prob.w[m])
+            W = mpmath.matrix(hi.shape[0], hi.shape[1])
+            for a in range(hi.shape[0]):
+                for b in range(hi.shape[1]):
+                    W[a, b] = mpmath.mpf(float(hi[a, b])) + mpmath.mpf(float(lo[a, b]))
+            v = W[0, :] if v is None else v * W
+            if m < d - 1:
+                M = mpmath.matrix(intersection(prob, state, m).tolist())
+                v = mpmath.lu_solve(M.T, v.T).T
+        core = v[0]
+        if core == 0:
+            return 0.0, -math.inf, 0
+        sign = 1 if core > 0 else -1
+        val = core * 4 / mpmath.factorial(d)
+        return float(val), float(mpmath.log10(abs(val))), sign
+
+
 def run(prob, n_sweeps, state=None):
     """Init (if no state), n_sweeps full sweeps, then the quadrature."""
     st = initial_state(prob) if state is None else state

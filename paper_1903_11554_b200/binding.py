@@ -1,0 +1,224 @@
+"""Thin ctypes binding of libttcross (include/ttcross.h).
+
+Argument marshalling only: every step of the TT-cross hot path runs in the CUDA kernels of
+``libttcross.so``.  There is no CPU fallback: if the shared library is missing or a call
+fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libttcross.so")
+
+TTC_OK = 0
+TTC_FAMILY_C = 0
+TTC_FAMILY_D = 1
+TTC_DIR_LR = 0
+TTC_DIR_RL = 1
+TTC_MEM_HOST = 0
+TTC_MEM_DEVICE = 1
+
+# every symbol declared in include/ttcross.h (checked by tests/test_abi.py)
+EXPORTS = [
+    "tt_cross_init", "tt_cross_reset", "tt_cross_sweep", "tt_cross_half_sweep",
+    "tt_cross_commit", "tt_cross_exchange_buffer", "tt_integrate", "tt_integrate_local",
+    "tt_integrate_partials_buffer", "tt_integrate_finish", "tt_cross_get_state",
+    "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_set_timing", "tt_cross_destroy",
+    "tt_last_error", "tt_build_info",
+]
+
+
+class TtcConfig(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int32),
+        ("rank_cap", ctypes.c_int32), ("n_enrich", ctypes.c_int32), ("max_swaps", ctypes.c_int32),
+        ("tol", ctypes.c_double), ("delta", ctypes.c_double), ("seed", ctypes.c_uint64),
+        ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+    ]
+
+
+class TtcStats(ctypes.Structure):
+    _fields_ = [
+        ("evals", ctypes.c_int64), ("launches", ctypes.c_int64), ("sweeps", ctypes.c_int32),
+        ("half_sweeps", ctypes.c_int32), ("ms_fiber", ctypes.c_double), ("ms_cross", ctypes.c_double),
+        ("ms_quad", ctypes.c_double), ("ms_other", ctypes.c_double), ("fiber_launches", ctypes.c_int64),
+        ("cross_launches", ctypes.c_int64), ("fiber_entries", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libttcross.so (raises FileNotFoundError / OSError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "tt_cross_init": (i32, [ctypes.POINTER(P), ctypes.POINTER(TtcConfig), P, P, i32, P]),
+        "tt_cross_reset": (i32, [P]),
+        "tt_cross_sweep": (i32, [P, i32]),
+        "tt_cross_half_sweep": (i32, [P, i32]),
+        "tt_cross_commit": (i32, [P]),
+        "tt_cross_exchange_buffer": (i32, [P, ctypes.POINTER(P), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "tt_integrate": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
+        "tt_integrate_local": (i32, [P]),
+        "tt_integrate_partials_buffer": (i32, [P, ctypes.POINTER(P), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "tt_integrate_finish": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
+        "tt_cross_get_state": (i32, [P, P, P]),
+        "tt_cross_get_fiber": (i32, [P, i32, P, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "tt_cross_get_stats": (i32, [P, ctypes.POINTER(TtcStats)]),
+        "tt_cross_set_timing": (i32, [P, i32]),
+        "tt_cross_destroy": (None, [P]),
+        "tt_last_error": (ctypes.c_char_p, []),
+        "tt_build_info": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class TTCError(RuntimeError):
+    pass
+
+
+def _check(lib, rc, what):
+    if rc != TTC_OK:
+        raise TTCError(f"{what} failed (code {rc}): {lib.tt_last_error().decode()}")
+
+
+def _ptr_and_kind(arr):
+    """(pointer, mem_kind, keepalive) for a numpy array or a CUDA tensor/array."""
+    if hasattr(arr, "__cuda_array_interface__") and not isinstance(arr, np.ndarray):
+        iface = arr.__cuda_array_interface__
+        if iface["typestr"] != "<f8":
+            raise TypeError("device arrays must be float64")
+        return ctypes.c_void_p(iface["data"][0]), TTC_MEM_DEVICE, arr
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    return a.ctypes.data_as(ctypes.c_void_p), TTC_MEM_HOST, a
+
+
+class DeviceView:
+    """__cuda_array_interface__ wrapper of a library-owned device buffer (zero copy)."""
+
+    def __init__(self, ptr, nbytes, typestr):
+        self.ptr, self.nbytes, self.typestr = ptr, nbytes, typestr
+        itemsize = int(typestr[2:])
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes // itemsize,), "typestr": typestr, "data": (ptr, False), "version": 2,
+        }
+
+
+class TTCross:
+    """Handle on one TT-cross problem (C-ABI context)."""
+
+    def __init__(self, family, u, w, rank_cap, tol, n_enrich=4, max_swaps=0, delta=1e-2,
+                 seed=0, rank=0, world=1, stream=None):
+        self.lib = load()
+        self.d, self.n = int(u.shape[0]), int(u.shape[1])
+        self.cap = int(rank_cap)
+        self.cfg = TtcConfig(int(family), self.d, self.n, self.cap, int(n_enrich), int(max_swaps),
+                             float(tol), float(delta), int(seed) & ((1 << 64) - 1), int(rank), int(world))
+        pu, ku, keep_u = _ptr_and_kind(u)
+        pw, kw, keep_w = _ptr_and_kind(w)
+        if ku != kw:
+            raise TypeError("nodes and weights must both be host or both be device arrays")
+        self._h = ctypes.c_void_p()
+        sp = ctypes.c_void_p(int(stream)) if stream else ctypes.c_void_p()
+        _check(self.lib, self.lib.tt_cross_init(ctypes.byref(self._h), ctypes.byref(self.cfg), pu, pw, ku, sp),
+               "tt_cross_init")
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self.lib.tt_cross_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        _check(self.lib, self.lib.tt_cross_reset(self._h), "tt_cross_reset")
+
+    def set_timing(self, on=True):
+        _check(self.lib, self.lib.tt_cross_set_timing(self._h, 1 if on else 0), "tt_cross_set_timing")
+
+    # -- the hot path
+    def sweep(self, n_sweeps=1):
+        _check(self.lib, self.lib.tt_cross_sweep(self._h, int(n_sweeps)), "tt_cross_sweep")
+
+    def half_sweep(self, direction):
+        _check(self.lib, self.lib.tt_cross_half_sweep(self._h, int(direction)), "tt_cross_half_sweep")
+
+    def commit(self):
+        _check(self.lib, self.lib.tt_cross_commit(self._h), "tt_cross_commit")
+
+    def integrate(self):
+        v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        _check(self.lib, self.lib.tt_integrate(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
+               "tt_integrate")
+        return v.value, l10.value, sg.value
+
+    def integrate_local(self):
+        _check(self.lib, self.lib.tt_integrate_local(self._h), "tt_integrate_local")
+
+    def integrate_finish(self):
+        v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        _check(self.lib, self.lib.tt_integrate_finish(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
+               "tt_integrate_finish")
+        return v.value, l10.value, sg.value
+
+    # -- buffers for the multi-process exchange (zero-copy device views)
+    def exchange_view(self):
+        p, tot, per = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+        _check(self.lib, self.lib.tt_cross_exchange_buffer(self._h, ctypes.byref(p), ctypes.byref(tot),
+                                                           ctypes.byref(per)), "tt_cross_exchange_buffer")
+        return DeviceView(p.value, tot.value, "<i4"), per.value
+
+    def partials_view(self):
+        p, tot, per = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+        _check(self.lib, self.lib.tt_integrate_partials_buffer(self._h, ctypes.byref(p), ctypes.byref(tot),
+                                                               ctypes.byref(per)), "tt_integrate_partials_buffer")
+        return DeviceView(p.value, tot.value, "<f8"), per.value
+
+    # -- inspection
+    def state(self):
+        ranks = np.zeros(self.d - 1, dtype=np.int32)
+        piv = np.zeros((self.d - 1, self.cap, self.d), dtype=np.int32)
+        _check(self.lib, self.lib.tt_cross_get_state(self._h, ranks.ctypes.data_as(ctypes.c_void_p),
+                                                     piv.ctypes.data_as(ctypes.c_void_p)), "tt_cross_get_state")
+        return ranks, [piv[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
+
+    def fiber(self, mode):
+        rx, ry = ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib, self.lib.tt_cross_get_fiber(self._h, int(mode), None, 0, ctypes.byref(rx), ctypes.byref(ry)),
+               "tt_cross_get_fiber")
+        out = np.empty((rx.value, ry.value, self.n), dtype=np.float64)
+        _check(self.lib, self.lib.tt_cross_get_fiber(self._h, int(mode), out.ctypes.data_as(ctypes.c_void_p),
+                                                     out.size, ctypes.byref(rx), ctypes.byref(ry)),
+               "tt_cross_get_fiber")
+        return out
+
+    def stats(self):
+        s = TtcStats()
+        _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
+        return {f: getattr(s, f) for f, _ in TtcStats._fields_}
+
+
+def build_info():
+    return load().tt_build_info().decode()

@@ -1,0 +1,694 @@
+// ttc_api.cu -- host side of libttcross: context, memory, launch sequences, C-ABI
+// (include/ttcross.h).  One translation unit; compiled for sm_100a only.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/ttcross.h"
+#include "ttc_common.cuh"
+#include "ttc_cross.cuh"
+#include "ttc_kernels.cuh"
+
+using namespace ttc;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(TTC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+enum KClass { KC_FIBER = 0, KC_CROSS = 1, KC_QUAD = 2, KC_OTHER = 3 };
+
+struct EvRec {
+  cudaEvent_t a, b;
+  int cls;
+  long long entries;
+};
+
+}  // namespace
+
+struct ttc_ctx {
+  ttc_config cfg{};
+  cudaStream_t stream = nullptr;
+  DevCtx dc{};
+  int chunk = 0, kb = 0, ke = 0, n_owned = 0, slots = 0;
+  int sweeps = 0, half_sweeps = 0;
+  int pending = 0;  // a half-sweep waits for commit
+  // cross kernel launch shape
+  int G = 1, rpc = 0;
+  bool smem_mode = true;
+  size_t cross_smem = 0;
+  // buffers
+  std::vector<void*> allocs;
+  int* rec_init = nullptr;
+  long long rec_ints = 0;
+  double* partials = nullptr;  // [world][3 + 2*cap*cap] (see k_chain)
+  double* out_dev = nullptr;   // [4]
+  double* out_host = nullptr;  // pinned [8]
+  // accounting
+  long long launches = 0;
+  bool timing = false;
+  std::vector<EvRec> evs;
+  std::vector<cudaEvent_t> ev_pool;
+  double ms[4] = {0, 0, 0, 0};
+  long long fiber_launches = 0, cross_launches = 0, fiber_entries = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(ttc_ctx* c, T** p, size_t count) {
+  void* q = nullptr;
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess)
+    return fail(TTC_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  c->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return TTC_OK;
+}
+
+cudaEvent_t get_event(ttc_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// bracket a launch with events when timing is enabled
+struct Timed {
+  ttc_ctx* c;
+  int cls;
+  long long entries;
+  cudaEvent_t a = nullptr;
+  Timed(ttc_ctx* c_, int cls_, long long e_ = 0) : c(c_), cls(cls_), entries(e_) {
+    c->launches++;
+    if (c->timing) {
+      a = get_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Timed() {
+    if (c->timing) {
+      cudaEvent_t b = get_event(c);
+      cudaEventRecord(b, c->stream);
+      c->evs.push_back({a, b, cls, entries});
+    }
+  }
+};
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TTC_OK;
+}
+
+// ------------------------------------------------------------------ host initial pivots
+// Mirrors oracle/cross.py::initial_state (seed-fixed nested random pivots, R5).
+std::vector<long long> partial_fisher_yates(uint64_t seed, int tag, int d, int i, long long M, int r) {
+  std::unordered_map<long long, long long> perm;
+  std::vector<long long> out;
+  auto get = [&](long long k) {
+    auto it = perm.find(k);
+    return it == perm.end() ? k : it->second;
+  };
+  for (int s = 0; s < r; ++s) {
+    long long j = s + (long long)(splitmix64(seed, draw_ctr((uint64_t)tag, d, i, s)) % (uint64_t)(M - s));
+    long long vs = get(s), vj = get(j);
+    perm[s] = vj;
+    perm[j] = vs;
+    out.push_back(vj);
+  }
+  return out;
+}
+
+long long ipow_cap(long long n, int e, long long cap) {
+  long long v = 1;
+  for (int k = 0; k < e; ++k) {
+    v *= n;
+    if (v >= cap) return cap;
+  }
+  return v;
+}
+
+void initial_records(const ttc_config& cfg, int RS, long long nrec, std::vector<int32_t>& rec) {
+  const int d = cfg.d, n = cfg.n, cap = cfg.rank_cap;
+  rec.assign(nrec * RS, -1);
+  std::vector<int> r(d - 1);
+  for (int i = 0; i < d - 1; ++i)
+    r[i] = (int)std::min<long long>(cap, std::min(ipow_cap(n, i + 1, cap), ipow_cap(n, d - 1 - i, cap)));
+  std::vector<std::vector<std::vector<int>>> left(d - 1), right(d - 1);
+  for (int i = 0; i < d - 1; ++i) {
+    long long prev = i > 0 ? r[i - 1] : 1;
+    auto sel = partial_fisher_yates(cfg.seed, 0, d, i, prev * n, r[i]);
+    for (long long cnd : sel) {
+      long long alpha = cnd / n, a = cnd % n;
+      std::vector<int> t;
+      if (i > 0) t = left[i - 1][alpha];
+      t.push_back((int)a);
+      left[i].push_back(t);
+    }
+  }
+  for (int i = d - 2; i >= 0; --i) {
+    long long nxt = i < d - 2 ? r[i + 1] : 1;
+    auto sel = partial_fisher_yates(cfg.seed, 1, d, i, nxt * n, r[i]);
+    for (long long cnd : sel) {
+      long long beta = cnd / n, a = cnd % n;
+      std::vector<int> t{(int)a};
+      if (i < d - 2) t.insert(t.end(), right[i + 1][beta].begin(), right[i + 1][beta].end());
+      right[i].push_back(t);
+    }
+  }
+  for (int i = 0; i < d - 1; ++i) {
+    int32_t* R = rec.data() + (long long)i * RS;
+    R[0] = r[i];
+    for (int s = 0; s < r[i]; ++s) {
+      for (int q = 0; q <= i; ++q) R[1 + (long long)s * d + q] = left[i][s][q];
+      for (int q = i + 1; q < d; ++q) R[1 + (long long)s * d + q] = right[i][s][q - i - 1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launch sequences
+// frozen parts + fiber entries for jobs [jbase, jbase+njobs) of the given kind
+int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
+  DevCtx& dc = c->dc;
+  const int nc = dc.ncols_max, n = dc.n;
+  const int tup_max = std::max(nc, dc.cap);
+  {
+    Timed t(c, KC_FIBER);
+    k_frozen_sides<<<dim3((tup_max + 63) / 64, 2, njobs), 64, 0, c->stream>>>(dc, kind, jbase);
+  }
+  if (int e = check_launch("k_frozen_sides")) return e;
+  if (dc.family == TTC_FAMILY_D) {
+    {
+      Timed t(c, KC_FIBER);
+      k_frozen_q<<<dim3((n + 127) / 128, tup_max, 2 * njobs), 128, 0, c->stream>>>(dc, kind, jbase);
+    }
+    if (int e = check_launch("k_frozen_q")) return e;
+    {
+      Timed t(c, KC_FIBER);
+      k_frozen_lr<<<dim3((tup_max + 63) / 64, tup_max, njobs), 64, 0, c->stream>>>(dc, kind, jbase);
+    }
+    if (int e = check_launch("k_frozen_lr")) return e;
+  }
+  const int gx = std::min(4096, (tup_max * n + 255) / 256);
+  {
+    Timed t(c, KC_FIBER, -1);
+    c->fiber_launches++;
+    if (dc.family == TTC_FAMILY_C)
+      k_fiber<0><<<dim3(gx, tup_max, njobs), 256, 0, c->stream>>>(dc, kind, jbase);
+    else
+      k_fiber<1><<<dim3(gx, tup_max, njobs), 256, 0, c->stream>>>(dc, kind, jbase);
+  }
+  return check_launch("k_fiber");
+}
+
+int launch_cross(ttc_ctx* c, int kind) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(c->n_owned * c->G);
+  lc.blockDim = dim3(CROSS_THREADS);
+  lc.dynamicSmemBytes = c->cross_smem;
+  lc.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = c->G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e;
+  {
+    Timed t(c, KC_CROSS);
+    c->cross_launches++;
+    if (c->smem_mode)
+      e = cudaLaunchKernelEx(&lc, k_cross<true>, c->dc, kind, c->G, c->rpc);
+    else
+      e = cudaLaunchKernelEx(&lc, k_cross<false>, c->dc, kind, c->G, c->rpc);
+  }
+  if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_cross launch: ") + cudaGetErrorString(e));
+  return check_launch("k_cross");
+}
+
+int do_half_sweep(ttc_ctx* c, int dir) {
+  if (c->n_owned > 0) {
+    DevCtx& dc = c->dc;
+    {
+      Timed t(c, KC_OTHER);
+      k_enrich<<<c->n_owned, 128, 0, c->stream>>>(dc, dir, c->sweeps);
+    }
+    if (int e = check_launch("k_enrich")) return e;
+    if (int e = launch_fibers(c, dir, 0, c->n_owned)) return e;
+    if (int e = launch_cross(c, dir)) return e;
+    {
+      Timed t(c, KC_OTHER);
+      k_commit<<<dim3(dc.cap, c->n_owned), 64, 0, c->stream>>>(dc, dir);
+    }
+    if (int e = check_launch("k_commit")) return e;
+  }
+  if (c->cfg.world == 1) {
+    // nothing to exchange: all interfaces are owned
+  }
+  c->pending = 1;
+  return TTC_OK;
+}
+
+int do_commit(ttc_ctx* c) {
+  if (!c->pending) return fail(TTC_ERR_STATE, "tt_cross_commit without a pending half-sweep");
+  std::swap(c->dc.rec_cur, c->dc.rec_next);
+  c->pending = 0;
+  c->half_sweeps++;
+  if (c->half_sweeps % 2 == 0) c->sweeps++;
+  return TTC_OK;
+}
+
+int do_integrate_local(ttc_ctx* c) {
+  DevCtx dc = c->dc;
+  const int cap = dc.cap;
+  const int rank = c->cfg.rank;
+  // modes whose fibers are needed: i+1 for the owned interfaces i, and mode 0 on rank 0
+  int m_lo = c->kb + 1, m_hi = c->ke;  // inclusive range
+  if (rank == 0) m_lo = 0;
+  const int nm = (c->n_owned > 0) ? (m_hi - m_lo + 1) : (rank == 0 ? 1 : 0);
+  if (nm > 0) {
+    if (int e = launch_fibers(c, JOB_INT, m_lo, nm)) return e;
+    {
+      Timed t(c, KC_QUAD);
+      k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->stream>>>(dc, m_lo);
+    }
+    if (int e = check_launch("k_wsum")) return e;
+  }
+  CK(cudaMemsetAsync(dc.flags, 0, 4 * sizeof(int), c->stream));
+  if (c->n_owned > 0) {
+    {
+      Timed t(c, KC_QUAD);
+      k_intersection<<<dim3((cap + 63) / 64, cap, c->n_owned), 64, 0, c->stream>>>(dc, c->kb);
+    }
+    if (int e = check_launch("k_intersection")) return e;
+    {
+      Timed t(c, KC_QUAD);
+      k_solve<<<c->n_owned, 256, 2 * cap * cap * sizeof(DD), c->stream>>>(dc);
+    }
+    if (int e = check_launch("k_solve")) return e;
+  }
+  double* rec = c->partials + (long long)rank * chain_record_size(cap);
+  {
+    Timed t(c, KC_QUAD);
+    k_chain<<<1, 256, 2 * cap * cap * sizeof(DD), c->stream>>>(dc, c->kb, c->ke, rank == 0 ? 1 : 0, rec);
+  }
+  return check_launch("k_chain");
+}
+
+int do_integrate_finish(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  const int cap = c->dc.cap, d = c->dc.d;
+  {
+    Timed t(c, KC_QUAD);
+    k_finish<<<1, 256, 0, c->stream>>>(c->partials, c->cfg.world, cap, c->out_dev);
+  }
+  if (int e = check_launch("k_finish")) return e;
+  CK(cudaMemcpyAsync(c->out_host, c->out_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->out_host + 2, c->dc.flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int flag = 0;
+  std::memcpy(&flag, c->out_host + 2, sizeof(int));
+  if (flag) return fail(TTC_ERR_SINGULAR, "an intersection matrix A(I_{<=i}, I_{>i}) is singular");
+  const double core = c->out_host[0];
+  const double lg2 = c->out_host[1];
+  int sg = core > 0 ? 1 : (core < 0 ? -1 : 0);
+  double l10, val;
+  if (core == 0.0 || !std::isfinite(core)) {
+    l10 = core == 0.0 ? -INFINITY : NAN;
+    val = core;
+  } else {
+    const double lnpre = std::log(4.0) - std::lgamma((double)d + 1.0);
+    const double ln_abs = std::log(std::fabs(core)) + lg2 * std::log(2.0) + lnpre;
+    l10 = ln_abs / std::log(10.0);
+    if (ln_abs > -700.0 && ln_abs < 700.0) {
+      if (lg2 > -1000 && lg2 < 1000 && d <= 170) {
+        double pre = 4.0;
+        for (int k = 2; k <= d; ++k) pre /= (double)k;
+        val = std::ldexp(core, (int)lg2) * pre;
+      } else {
+        val = sg * std::exp(ln_abs);
+      }
+    } else {
+      val = sg * (ln_abs > 0 ? INFINITY : 0.0);
+    }
+  }
+  if (value) *value = val;
+  if (log10_abs) *log10_abs = l10;
+  if (sign) *sign = sg;
+  return TTC_OK;
+}
+
+int resolve_timing(ttc_ctx* c) {
+  if (c->evs.empty()) return TTC_OK;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->evs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->ms[r.cls] += ms;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->evs.clear();
+  return TTC_OK;
+}
+
+}  // namespace
+
+// ====================================================================================
+// C-ABI
+// ====================================================================================
+extern "C" {
+
+const char* tt_last_error(void) { return g_err.c_str(); }
+
+const char* tt_build_info(void) {
+  return "libttcross 0.1 (sm_100a, fp64, -fmad=false, cluster cross+maxvol)";
+}
+
+int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, const double* weights,
+                  int32_t mem_kind, void* stream) {
+  if (!out || !cfg || !nodes_u || !weights) return fail(TTC_ERR_ARG, "null argument");
+  *out = nullptr;
+  const ttc_config& k = *cfg;
+  if (k.family != TTC_FAMILY_C && k.family != TTC_FAMILY_D) return fail(TTC_ERR_ARG, "family must be 0 (C) or 1 (D)");
+  if (k.d < 2 || k.d > 2000) return fail(TTC_ERR_ARG, "d must be in [2, 2000]");
+  if (k.n < 2 || k.n > 4096) return fail(TTC_ERR_ARG, "n must be in [2, 4096]");
+  if (k.rank_cap < 1 || k.rank_cap > TTC_MAX_RANK) return fail(TTC_ERR_ARG, "rank_cap must be in [1, 64]");
+  if (k.n_enrich < 0 || k.n_enrich > TTC_MAX_ENRICH) return fail(TTC_ERR_ARG, "n_enrich must be in [0, 16]");
+  if (k.max_swaps < 0) return fail(TTC_ERR_ARG, "max_swaps must be >= 0");
+  if (!(k.tol >= 0.0 && k.tol < 1.0)) return fail(TTC_ERR_ARG, "tol must be in [0, 1)");
+  if (!(k.delta >= 0.0)) return fail(TTC_ERR_ARG, "delta must be >= 0");
+  if (k.world < 1 || k.rank < 0 || k.rank >= k.world) return fail(TTC_ERR_ARG, "need 0 <= rank < world");
+  if (mem_kind != TTC_MEM_HOST && mem_kind != TTC_MEM_DEVICE) return fail(TTC_ERR_ARG, "mem_kind");
+  if (mem_kind == TTC_MEM_HOST) {
+    for (long long t = 0; t < (long long)k.d * k.n; ++t)
+      if (!(nodes_u[t] > 0.0) || !std::isfinite(nodes_u[t])) return fail(TTC_ERR_ARG, "u-nodes must be finite and > 0");
+  }
+
+  ttc_ctx* c = new ttc_ctx();
+  c->cfg = k;
+  if (c->cfg.max_swaps == 0) c->cfg.max_swaps = 2 * k.rank_cap;
+  c->stream = static_cast<cudaStream_t>(stream);
+  const int d = k.d, n = k.n, cap = k.rank_cap, p = k.n_enrich;
+  DevCtx& dc = c->dc;
+  dc.family = k.family;
+  dc.d = d;
+  dc.n = n;
+  dc.cap = cap;
+  dc.p = p;
+  dc.max_swaps = c->cfg.max_swaps;
+  dc.tol = k.tol;
+  dc.delta = k.delta;
+  dc.seed = k.seed;
+  dc.world = k.world;
+  dc.rank = k.rank;
+  c->chunk = (d - 1 + k.world - 1) / k.world;
+  dc.chunk = c->chunk;
+  c->kb = std::min(d - 1, k.rank * c->chunk);
+  c->ke = std::min(d - 1, (k.rank + 1) * c->chunk);
+  c->n_owned = c->ke - c->kb;
+  dc.kb = c->kb;
+  dc.ke = c->ke;
+  dc.RS = 1 + cap * d;
+  dc.ncols_max = cap + p;
+  c->slots = d;
+  const long long nrec = (long long)k.world * c->chunk;
+  c->rec_ints = nrec * dc.RS;
+  dc.fib_stride = (long long)cap * dc.ncols_max * n;
+  const int tup = std::max(dc.ncols_max, cap);
+
+  auto bail = [&](int e) {
+    tt_cross_destroy(c);
+    return e;
+  };
+  int e = 0;
+  double *u = nullptr, *w = nullptr;
+  long long *chi = nullptr, *clo = nullptr;
+  if ((e = dalloc(c, &u, (size_t)d * n)) || (e = dalloc(c, &w, (size_t)d * n)) ||
+      (e = dalloc(c, &chi, (size_t)d * n)) || (e = dalloc(c, &clo, (size_t)d * n)))
+    return bail(e);
+  dc.u = u;
+  dc.w = w;
+  dc.chi = chi;
+  dc.clo = clo;
+  if ((e = dalloc(c, &dc.rec_cur, (size_t)c->rec_ints)) || (e = dalloc(c, &dc.rec_next, (size_t)c->rec_ints)) ||
+      (e = dalloc(c, &c->rec_init, (size_t)c->rec_ints)) ||
+      (e = dalloc(c, &dc.ext, (size_t)(d - 1) * dc.ncols_max * d)) || (e = dalloc(c, &dc.ext_cnt, (size_t)d)) ||
+      (e = dalloc(c, &dc.fib, (size_t)c->slots * dc.fib_stride)) ||
+      (e = dalloc(c, &dc.sl, (size_t)c->slots * tup)) || (e = dalloc(c, &dc.sr, (size_t)c->slots * tup)) ||
+      (e = dalloc(c, &dc.pll, (size_t)c->slots * tup)) || (e = dalloc(c, &dc.prr, (size_t)c->slots * tup)) ||
+      (e = dalloc(c, &dc.pf, (size_t)c->slots * tup * tup)) ||
+      (e = dalloc(c, &dc.sel_row, (size_t)c->slots * cap)) || (e = dalloc(c, &dc.sel_col, (size_t)c->slots * cap)) ||
+      (e = dalloc(c, &dc.sel_rank, (size_t)c->slots)) || (e = dalloc(c, &dc.sel_nsw, (size_t)c->slots)) ||
+      (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
+      (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
+      (e = dalloc(c, &dc.counters, 4)) ||
+      (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)))
+    return bail(e);
+  if (k.family == TTC_FAMILY_D) {
+    if ((e = dalloc(c, &dc.ql, (size_t)c->slots * tup * n)) || (e = dalloc(c, &dc.qr, (size_t)c->slots * tup * n)))
+      return bail(e);
+  }
+  {
+    cudaError_t ce = cudaMallocHost(&c->out_host, 8 * sizeof(double));
+    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(ce)));
+  }
+  // grid upload
+  const cudaMemcpyKind kind = mem_kind == TTC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  {
+    cudaError_t ce = cudaMemcpyAsync(u, nodes_u, sizeof(double) * d * n, kind, c->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(w, weights, sizeof(double) * d * n, kind, c->stream);
+    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("grid upload: ") + cudaGetErrorString(ce)));
+  }
+  {
+    Timed t(c, KC_OTHER);
+    k_prep_nodes<<<(d * n + 255) / 256, 256, 0, c->stream>>>(u, chi, clo, d * n);
+  }
+  if ((e = check_launch("k_prep_nodes"))) return bail(e);
+  // initial pivots (host, mirrors the oracle), uploaded once and kept for reset
+  std::vector<int32_t> rec;
+  initial_records(c->cfg, dc.RS, nrec, rec);
+  {
+    cudaError_t ce = cudaMemcpy(c->rec_init, rec.data(), sizeof(int32_t) * rec.size(), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("pivot upload: ") + cudaGetErrorString(ce)));
+  }
+  // cross kernel shape: smallest cluster whose shared memory holds the fiber matrix
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t head = ((sizeof(CrossSmem) + 127) / 128) * 128;
+    const long long nrows_max = (long long)cap * n;
+    c->smem_mode = false;
+    for (int G : {1, 2, 4, 8, 16}) {
+      long long rpc = (nrows_max + G - 1) / G;
+      size_t bytes = head + (size_t)rpc * dc.ncols_max * sizeof(double);
+      if (bytes <= (size_t)optin) {
+        c->G = G;
+        c->rpc = (int)rpc;
+        c->cross_smem = bytes;
+        c->smem_mode = true;
+        break;
+      }
+    }
+    if (!c->smem_mode) {
+      c->G = 16;
+      c->rpc = (int)((nrows_max + 15) / 16);
+      c->cross_smem = head;
+    }
+    cudaError_t ce = cudaFuncSetAttribute(k_cross<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_cross<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ce == cudaSuccess)
+      ce = cudaFuncSetAttribute(k_cross<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(c->cross_smem, head));
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_cross<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head);
+    const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
+    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
+  }
+  c->timing = false;
+  int rc = tt_cross_reset(c);
+  if (rc) return bail(rc);
+  *out = c;
+  return TTC_OK;
+}
+
+int tt_cross_reset(ttc_ctx* c) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  CK(cudaMemcpyAsync(c->dc.rec_cur, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->dc.rec_next, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->dc.counters, 0, 4 * sizeof(unsigned long long), c->stream));
+  c->sweeps = 0;
+  c->half_sweeps = 0;
+  c->pending = 0;
+  c->launches = 0;
+  if (int e = resolve_timing(c)) return e;
+  for (double& m : c->ms) m = 0.0;
+  c->fiber_launches = c->cross_launches = c->fiber_entries = 0;
+  return TTC_OK;
+}
+
+int tt_cross_half_sweep(ttc_ctx* c, int32_t direction) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (direction != TTC_DIR_LR && direction != TTC_DIR_RL) return fail(TTC_ERR_ARG, "direction");
+  if (c->pending) return fail(TTC_ERR_STATE, "previous half-sweep not committed");
+  return do_half_sweep(c, direction);
+}
+
+int tt_cross_commit(ttc_ctx* c) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  return do_commit(c);
+}
+
+int tt_cross_sweep(ttc_ctx* c, int32_t n_sweeps) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_cross_sweep needs world == 1");
+  if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  for (int s = 0; s < n_sweeps; ++s) {
+    for (int dir : {TTC_DIR_LR, TTC_DIR_RL}) {
+      if (int e = do_half_sweep(c, dir)) return e;
+      if (int e = do_commit(c)) return e;
+    }
+  }
+  return TTC_OK;
+}
+
+int tt_cross_exchange_buffer(ttc_ctx* c, void** dev_ptr, int64_t* bytes_total, int64_t* bytes_per_rank) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (dev_ptr) *dev_ptr = c->dc.rec_next;
+  if (bytes_total) *bytes_total = c->rec_ints * (int64_t)sizeof(int32_t);
+  if (bytes_per_rank) *bytes_per_rank = (int64_t)c->chunk * c->dc.RS * (int64_t)sizeof(int32_t);
+  return TTC_OK;
+}
+
+int tt_integrate(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate needs world == 1");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (int e = do_integrate_local(c)) return e;
+  return do_integrate_finish(c, value, log10_abs, sign);
+}
+
+int tt_integrate_local(ttc_ctx* c) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  return do_integrate_local(c);
+}
+
+int tt_integrate_partials_buffer(ttc_ctx* c, void** dev_ptr, int64_t* bytes_total, int64_t* bytes_per_rank) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  const int64_t rsz = chain_record_size(c->dc.cap) * (int64_t)sizeof(double);
+  if (dev_ptr) *dev_ptr = c->partials;
+  if (bytes_total) *bytes_total = rsz * c->cfg.world;
+  if (bytes_per_rank) *bytes_per_rank = rsz;
+  return TTC_OK;
+}
+
+int tt_integrate_finish(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  return do_integrate_finish(c, value, log10_abs, sign);
+}
+
+int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  const int d = c->dc.d, cap = c->dc.cap, RS = c->dc.RS;
+  std::vector<int32_t> rec(c->rec_ints);
+  CK(cudaMemcpyAsync(rec.data(), c->dc.rec_cur, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < d - 1; ++i) {
+    const int32_t* R = rec.data() + (long long)i * RS;
+    if (ranks_out) ranks_out[i] = R[0];
+    if (piv_out)
+      for (long long t = 0; t < (long long)cap * d; ++t) {
+        const long long s = t / d;
+        piv_out[(long long)i * cap * d + t] = s < R[0] ? R[1 + t] : -1;
+      }
+  }
+  return TTC_OK;
+}
+
+int tt_cross_get_fiber(ttc_ctx* c, int32_t mode, double* out, int64_t capacity, int32_t* rx, int32_t* ry) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  const int d = c->dc.d, n = c->dc.n, RS = c->dc.RS;
+  if (mode < 0 || mode >= d) return fail(TTC_ERR_ARG, "mode out of range");
+  int32_t a = 1, b = 1;
+  if (mode > 0) CK(cudaMemcpyAsync(&a, c->dc.rec_cur + (long long)(mode - 1) * RS, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if (mode < d - 1) CK(cudaMemcpyAsync(&b, c->dc.rec_cur + (long long)mode * RS, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (rx) *rx = a;
+  if (ry) *ry = b;
+  const long long cnt = (long long)a * b * n;
+  if (out) {
+    if (capacity < cnt) return fail(TTC_ERR_ARG, "fiber buffer too small");
+    CK(cudaMemcpyAsync(out, c->dc.fib + (long long)mode * c->dc.fib_stride, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return TTC_OK;
+}
+
+int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
+  if (!c || !out) return fail(TTC_ERR_ARG, "null argument");
+  unsigned long long cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, c->dc.counters, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (int e = resolve_timing(c)) return e;
+  std::memset(out, 0, sizeof(*out));
+  out->evals = (int64_t)cnt;
+  out->launches = c->launches;
+  out->sweeps = c->sweeps;
+  out->half_sweeps = c->half_sweeps;
+  out->ms_fiber = c->ms[KC_FIBER];
+  out->ms_cross = c->ms[KC_CROSS];
+  out->ms_quad = c->ms[KC_QUAD];
+  out->ms_other = c->ms[KC_OTHER];
+  out->fiber_launches = c->fiber_launches;
+  out->cross_launches = c->cross_launches;
+  out->fiber_entries = c->fiber_entries;
+  return TTC_OK;
+}
+
+int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  c->timing = enable != 0;
+  return TTC_OK;
+}
+
+void tt_cross_destroy(ttc_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& r : c->evs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->out_host) cudaFreeHost(c->out_host);
+  delete c;
+}
+
+}  // extern "C"

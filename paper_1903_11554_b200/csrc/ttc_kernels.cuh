@@ -1,0 +1,511 @@
+// ttc_kernels.cuh -- fiber evaluation, enrichment, commit and quadrature kernels.
+//
+// Fiber of mode m for a job: F[alpha][beta][a] = A(X[alpha][0:m], a, Y[beta][m+1:d])
+// (eq. (3) factors A(I_{<=k-1}, i_k, I_{>k}), lines 312-320).  The entry is
+// factorised over the frozen coordinates (DESIGN.md §5 "fiber kernel"):
+//   S = S_L[alpha] + S_R[beta] + c_m[a]                               (exact int64 limbs)
+//   P = Pf[alpha][beta] * Q_L[alpha][a] * Q_R[beta][a]                (double-double)
+//   Pf = P_LL[alpha] * P_RR[beta] * prod_{i<m<j} rho(X_i, Y_j),
+//   Q_L = prod_{j<m} rho(u_m[a], X_j),  Q_R = prod_{j>m} rho(u_m[a], Y_j).
+// Because S and P are rounded once from exactly (resp. to 2^-100) accumulated values, the
+// result equals the oracle's plain O(d^2)-per-entry evaluation bit for bit.
+#pragma once
+#include "ttc_common.cuh"
+
+namespace ttc {
+
+// ---------------------------------------------------------------------------------------
+// per-node tables: c = fl(u + fl(1/u)) split into (floor(c), frac(c)*2^52)
+// ---------------------------------------------------------------------------------------
+__global__ void k_prep_nodes(const double* __restrict__ u, long long* chi, long long* clo, int total) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  double x = u[t];
+  double c = __dadd_rn(x, __ddiv_rn(1.0, x));
+  double h = floor(c);
+  chi[t] = __double2ll_rn(h);
+  clo[t] = __double2ll_rn(__dmul_rn(__dsub_rn(c, h), 0x1p52));
+}
+
+// ---------------------------------------------------------------------------------------
+// enrichment: extended column set of interface i (existing pivots + p random superblock
+// columns, duplicates skipped) -- PAPER.md Alg. 2 line 1 ("random set of samples")
+// ---------------------------------------------------------------------------------------
+__global__ void k_enrich(DevCtx c, int dir, int sweep) {
+  const int i = c.kb + blockIdx.x;
+  const int d = c.d, n = c.n;
+  __shared__ int cand[2048 + 8];
+  __shared__ int cnt, dup;
+  int* ext = c.ext + (long long)i * c.ncols_max * d;
+  const int r = rec_rank(c.rec_cur, c.RS, i);
+  const int* P = rec_piv(c.rec_cur, c.RS, i);
+  for (int t = threadIdx.x; t < r * d; t += blockDim.x) ext[t] = P[t];
+  if (threadIdx.x == 0) cnt = r;
+  // range of coordinates that identifies a column of this interface
+  const int lo = (dir == JOB_LR) ? i + 1 : 0;
+  const int hi = (dir == JOB_LR) ? d : i + 1;
+  const uint64_t tag = 2ULL + 2ULL * (uint64_t)sweep + (uint64_t)dir;
+  __syncthreads();
+  for (int jd = 0; jd < c.p; ++jd) {
+    if (threadIdx.x == 0) {
+      long long M;
+      if (dir == JOB_LR) M = (long long)((i < d - 2) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1) * n;
+      else M = (long long)((i > 0) ? rec_rank(c.rec_cur, c.RS, i - 1) : 1) * n;
+      uint64_t v = splitmix64(c.seed, draw_ctr(tag, d, i, jd)) % (uint64_t)M;
+      int outer = (int)(v / (uint64_t)n), a = (int)(v % (uint64_t)n);
+      dup = 0;
+      if (dir == JOB_LR) {
+        for (int j = 0; j <= i; ++j) cand[j] = -1;
+        cand[i + 1] = a;
+        if (i < d - 2) {
+          const int* Pn = rec_piv(c.rec_cur, c.RS, i + 1) + (long long)outer * d;
+          for (int j = i + 2; j < d; ++j) cand[j] = Pn[j];
+        }
+      } else {
+        if (i > 0) {
+          const int* Pp = rec_piv(c.rec_cur, c.RS, i - 1) + (long long)outer * d;
+          for (int j = 0; j < i; ++j) cand[j] = Pp[j];
+        }
+        cand[i] = a;
+        for (int j = i + 1; j < d; ++j) cand[j] = -1;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int* E = ext + (long long)e * d;
+      bool eq = true;
+      for (int j = lo; j < hi; ++j)
+        if (E[j] != cand[j]) { eq = false; break; }
+      if (eq) atomicOr(&dup, 1);
+    }
+    __syncthreads();
+    if (!dup) {
+      for (int j = threadIdx.x; j < d; j += blockDim.x) ext[(long long)cnt * d + j] = cand[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !dup) cnt++;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) c.ext_cnt[i] = cnt;
+}
+
+// ---------------------------------------------------------------------------------------
+// frozen parts, per (job, side, tuple): S_L / P_LL (side 0), S_R / P_RR (side 1)
+// grid: x = tuple (<= ncols_max), y = side, z = job
+// ---------------------------------------------------------------------------------------
+__global__ void k_frozen_sides(DevCtx c, int kind, int jbase) {
+  const int j = jbase + blockIdx.z, side = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  Job jb = make_job(c, kind, j);
+  const int d = c.d, n = c.n, m = jb.m;
+  const long long so = (long long)j * c.ncols_max + t;
+  if (side == 0 && t == 0 && c.counters) atomicAdd(&c.counters[0], (unsigned long long)jb.rx * jb.ry * n);
+  if (side == 0) {
+    if (t >= jb.rx) return;
+    ESum s = esum_zero();
+    DDE p = dde_one();
+    if (jb.X) {
+      const int* T = jb.X + (long long)t * d;
+      for (int q = 0; q < m; ++q) esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
+      if (c.family == 1)
+        for (int a = 0; a < m; ++a) {
+          double ua = c.u[a * n + T[a]];
+          for (int b = a + 1; b < m; ++b) dde_mul_d(p, rho(ua, c.u[b * n + T[b]]));
+        }
+    }
+    c.sl[so] = s;
+    c.pll[so] = p;
+  } else {
+    if (t >= jb.ry) return;
+    ESum s = esum_zero();
+    DDE p = dde_one();
+    if (jb.Y) {
+      const int* T = jb.Y + (long long)t * d;
+      for (int q = m + 1; q < d; ++q) esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
+      if (c.family == 1)
+        for (int a = m + 1; a < d; ++a) {
+          double ua = c.u[a * n + T[a]];
+          for (int b = a + 1; b < d; ++b) dde_mul_d(p, rho(ua, c.u[b * n + T[b]]));
+        }
+    }
+    c.sr[so] = s;
+    c.prr[so] = p;
+  }
+}
+
+// Q_L[alpha][a] (side 0) and Q_R[beta][a] (side 1); grid: x = node a, y = tuple, z = job*2+side
+__global__ void k_frozen_q(DevCtx c, int kind, int jbase) {
+  const int j = jbase + (blockIdx.z >> 1), side = blockIdx.z & 1;
+  const int tup = blockIdx.y;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = c.d, n = c.n;
+  if (a >= n) return;
+  Job jb = make_job(c, kind, j);
+  const int m = jb.m;
+  const double um = c.u[m * n + a];
+  DDE p = dde_one();
+  const long long o = ((long long)j * c.ncols_max + tup) * n + a;
+  if (side == 0) {
+    if (tup >= jb.rx) return;
+    if (jb.X) {
+      const int* T = jb.X + (long long)tup * d;
+      for (int q = 0; q < m; ++q) dde_mul_d(p, rho(um, c.u[q * n + T[q]]));
+    }
+    c.ql[o] = p;
+  } else {
+    if (tup >= jb.ry) return;
+    if (jb.Y) {
+      const int* T = jb.Y + (long long)tup * d;
+      for (int q = m + 1; q < d; ++q) dde_mul_d(p, rho(um, c.u[q * n + T[q]]));
+    }
+    c.qr[o] = p;
+  }
+}
+
+// Pf[alpha][beta] = P_LL * P_RR * prod_{i<m<j} rho(X_i, Y_j); grid: x = beta, y = alpha, z = job
+__global__ void k_frozen_lr(DevCtx c, int kind, int jbase) {
+  const int j = jbase + blockIdx.z, al = blockIdx.y;
+  const int be = blockIdx.x * blockDim.x + threadIdx.x;
+  Job jb = make_job(c, kind, j);
+  if (al >= jb.rx || be >= jb.ry) return;
+  const int d = c.d, n = c.n, m = jb.m;
+  const long long base = (long long)j * c.ncols_max;
+  DDE p = c.pll[base + al];
+  dde_mul(p, c.prr[base + be]);
+  if (jb.X && jb.Y) {
+    const int* TX = jb.X + (long long)al * d;
+    const int* TY = jb.Y + (long long)be * d;
+    for (int a = 0; a < m; ++a) {
+      double ua = c.u[a * n + TX[a]];
+      for (int b = m + 1; b < d; ++b) dde_mul_d(p, rho(ua, c.u[b * n + TY[b]]));
+    }
+  }
+  c.pf[(base + al) * c.ncols_max + be] = p;
+}
+
+// ---------------------------------------------------------------------------------------
+// fiber entries: grid x = flat (beta*n + a) chunks, y = alpha, z = job
+// ---------------------------------------------------------------------------------------
+template <int FAMILY>
+__global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
+  const int j = jbase + blockIdx.z, al = blockIdx.y;
+  Job jb = make_job(c, kind, j);
+  if (al >= jb.rx) return;
+  const int n = c.n, m = jb.m;
+  const int total = jb.ry * n;
+  const long long base = (long long)j * c.ncols_max;
+  const ESum sl = c.sl[base + al];
+  double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+    const int be = f / n;
+    const int a = f - be * n;
+    ESum s = sl;
+    esum_add(s, c.sr[base + be]);
+    esum_add(s, c.chi[m * n + a], c.clo[m * n + a]);
+    const double S = esum_round(s);
+    const double SS = __dmul_rn(S, S);
+    double v;
+    if (FAMILY == 0) {
+      v = __drcp_rn(SS);
+    } else {
+      DDE p = c.pf[(base + al) * c.ncols_max + be];
+      dde_mul(p, c.ql[(base + al) * n + a]);
+      dde_mul(p, c.qr[(base + be) * n + a]);
+      v = __ddiv_rn(dde_round(p), SS);
+    }
+    F[f] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// commit the selected cross of every owned interface into rec_next
+// grid: x = slot, y = job ; block threads over the d coordinates
+// ---------------------------------------------------------------------------------------
+__global__ void k_commit(DevCtx c, int kind) {
+  const int j = blockIdx.y, s = blockIdx.x;
+  Job jb = make_job(c, kind, j);
+  const int i = jb.iface, d = c.d, n = c.n, m = jb.m;
+  const int rnew = c.sel_rank[j];
+  int* R = c.rec_next + (long long)i * c.RS;
+  const int* Pc = rec_piv(c.rec_cur, c.RS, i);
+  if (rnew == 0) {  // identically zero fiber: keep the interface (R8)
+    const int rold = rec_rank(c.rec_cur, c.RS, i);
+    if (s == 0 && threadIdx.x == 0) R[0] = rold;
+    for (int q = threadIdx.x; q < d; q += blockDim.x)
+      R[1 + (long long)s * d + q] = s < rold ? Pc[(long long)s * d + q] : -1;
+    return;
+  }
+  if (s == 0 && threadIdx.x == 0) R[0] = rnew;
+  if (s >= rnew) {
+    for (int q = threadIdx.x; q < d; q += blockDim.x) R[1 + (long long)s * d + q] = -1;
+    return;
+  }
+  const int row = c.sel_row[(long long)j * c.cap + s];
+  const int col = c.sel_col[(long long)j * c.cap + s];
+  const int outer = row / n, a = row - outer * n;
+  const int x = (kind == JOB_LR) ? outer : col;
+  const int y = (kind == JOB_LR) ? col : outer;
+  for (int q = threadIdx.x; q < d; q += blockDim.x) {
+    int v;
+    if (q < m) v = jb.X[(long long)x * d + q];
+    else if (q == m) v = a;
+    else v = jb.Y[(long long)y * d + q];
+    R[1 + (long long)s * d + q] = v;
+  }
+}
+
+// copy records of non-owned interfaces (world == 1: none; used so rec_next is complete)
+__global__ void k_copy_records(int* dst, const int* src, long long nints) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nints;
+       t += (long long)gridDim.x * blockDim.x)
+    dst[t] = src[t];
+}
+
+// ---------------------------------------------------------------------------------------
+// quadrature (§4.1)
+// ---------------------------------------------------------------------------------------
+// intersection matrices M_i[s][t] = A(left(PIV[i][s]), right(PIV[i][t])), direct O(d^2)
+__global__ void k_intersection(DevCtx c, int ibase) {
+  const int i = ibase + blockIdx.z;
+  const int s = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = c.d, n = c.n;
+  const int r = rec_rank(c.rec_cur, c.RS, i);
+  if (s == 0 && t == 0 && c.counters) atomicAdd(&c.counters[0], (unsigned long long)r * r);
+  if (s >= r || t >= r) return;
+  const int* Ps = rec_piv(c.rec_cur, c.RS, i) + (long long)s * d;
+  const int* Pt = rec_piv(c.rec_cur, c.RS, i) + (long long)t * d;
+  ESum S = esum_zero();
+  for (int q = 0; q < d; ++q) {
+    int node = q <= i ? Ps[q] : Pt[q];
+    esum_add(S, c.chi[q * n + node], c.clo[q * n + node]);
+  }
+  const double Sd = esum_round(S);
+  const double SS = __dmul_rn(Sd, Sd);
+  double v;
+  if (c.family == 0) {
+    v = __drcp_rn(SS);
+  } else {
+    DDE p = dde_one();
+    for (int a = 0; a < d; ++a) {
+      double ua = c.u[a * n + (a <= i ? Ps[a] : Pt[a])];
+      for (int b = a + 1; b < d; ++b) dde_mul_d(p, rho(ua, c.u[b * n + (b <= i ? Ps[b] : Pt[b])]));
+    }
+    v = __ddiv_rn(dde_round(p), SS);
+  }
+  c.M[((long long)i * c.cap + s) * c.cap + t] = v;
+}
+
+// W_m[alpha][beta] = sum_a w_{m,a} F_m[alpha][beta][a] in double-double; one warp per entry
+__global__ void k_wsum(DevCtx c, int mode_base) {
+  const int m = mode_base + blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int al = blockIdx.y;
+  const int be = blockIdx.x * (blockDim.x >> 5) + warp;
+  Job jb = make_job(c, JOB_INT, m);
+  if (al >= jb.rx || be >= jb.ry) return;
+  const int n = c.n;
+  const double* F = c.fib + (long long)m * c.fib_stride + ((long long)al * jb.ry + be) * n;
+  const double* w = c.w + (long long)m * n;
+  DD acc = dd_make(0.0);
+  for (int a = lane; a < n; a += 32) {
+    double p = w[a] * F[a];
+    acc = dd_add(acc, DD{p, fma(w[a], F[a], -p)});
+  }
+  for (int o = 16; o; o >>= 1) {
+    DD other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+    acc = dd_add(acc, other);
+  }
+  if (lane == 0) c.W[((long long)m * c.cap + al) * c.cap + be] = acc;
+}
+
+// H_i = M_i^{-1} W_{i+1}: LU with partial pivoting in double-double (shared memory),
+// one CTA per owned interface.
+__global__ void __launch_bounds__(256) k_solve(DevCtx c) {
+  const int i = blockIdx.x + c.kb;
+  const int cap = c.cap, d = c.d;
+  extern __shared__ DD smd[];
+  DD* A = smd;                 // [cap][cap]
+  DD* Bm = smd + cap * cap;    // [cap][cap]
+  __shared__ int piv_row;
+  __shared__ double piv_abs[256];
+  __shared__ int piv_idx[256];
+  const int r = rec_rank(c.rec_cur, c.RS, i);
+  const int nc = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+  for (int t = threadIdx.x; t < r * r; t += blockDim.x) {
+    int a = t / r, b = t % r;
+    A[a * cap + b] = dd_make(c.M[((long long)i * cap + a) * cap + b]);
+  }
+  for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
+    int a = t / nc, b = t % nc;
+    Bm[a * cap + b] = c.W[((long long)(i + 1) * cap + a) * cap + b];
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    double best = -1.0;
+    int bi = k;
+    for (int row = k + threadIdx.x; row < r; row += blockDim.x) {
+      double v = fabs(A[row * cap + k].hi);
+      if (v > best) { best = v; bi = row; }
+    }
+    piv_abs[threadIdx.x] = best;
+    piv_idx[threadIdx.x] = bi;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = -1.0;
+      int bj = k;
+      for (int t = 0; t < blockDim.x; ++t)
+        if (piv_abs[t] > bb || (piv_abs[t] == bb && piv_idx[t] < bj)) { bb = piv_abs[t]; bj = piv_idx[t]; }
+      piv_row = bj;
+      if (!(bb > 0.0)) atomicOr(&c.flags[0], 1);
+    }
+    __syncthreads();
+    const int pr = piv_row;
+    if (pr != k) {
+      for (int t = threadIdx.x; t < cap; t += blockDim.x) {
+        if (t < r) { DD x = A[k * cap + t]; A[k * cap + t] = A[pr * cap + t]; A[pr * cap + t] = x; }
+        if (t < nc) { DD y = Bm[k * cap + t]; Bm[k * cap + t] = Bm[pr * cap + t]; Bm[pr * cap + t] = y; }
+      }
+    }
+    __syncthreads();
+    const DD akk = A[k * cap + k];
+    const int width = (r - k - 1) + nc;
+    for (int t = threadIdx.x; t < (r - k - 1) * width; t += blockDim.x) {
+      const int row = k + 1 + t / width;
+      const int colx = t % width;
+      const DD l = dd_div(A[row * cap + k], akk);
+      if (colx < r - k - 1) {
+        const int col = k + 1 + colx;
+        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l, A[k * cap + col]));
+      } else {
+        const int col = colx - (r - k - 1);
+        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l, Bm[k * cap + col]));
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = r - 1; k >= 0; --k) {
+    for (int col = threadIdx.x; col < nc; col += blockDim.x) {
+      DD acc = Bm[k * cap + col];
+      for (int q = k + 1; q < r; ++q) acc = dd_sub(acc, dd_mul(A[k * cap + q], Bm[q * cap + col]));
+      Bm[k * cap + col] = dd_div(acc, A[k * cap + k]);
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
+    int a = t / nc, b = t % nc;
+    c.H[((long long)i * cap + a) * cap + b] = Bm[a * cap + b];
+  }
+}
+
+// record layout (doubles): [rows, cols, log2scale, V_hi[cap*cap], V_lo[cap*cap]]
+__host__ __device__ __forceinline__ long long chain_record_size(int cap) { return 3 + 2LL * cap * cap; }
+
+__device__ double block_absmax(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s2 = blockDim.x / 2; s2; s2 >>= 1) {
+    if (threadIdx.x < s2) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s2]);
+    __syncthreads();
+  }
+  double m = red[0];
+  __syncthreads();
+  return m;
+}
+
+// Partial product of the quadrature chain over interfaces [i_begin, i_end) (one CTA):
+//   with_head: V = W_0 (1 x r_0), else V = identity (r_{i_begin} x r_{i_begin});
+//   V <- V H_i for every i (double-double), renormalised by an exact power of two.
+// rows = 0 marks an empty record (a rank that owns no interface).
+__global__ void __launch_bounds__(256) k_chain(DevCtx c, int i_begin, int i_end, int with_head, double* rec) {
+  const int cap = c.cap, d = c.d;
+  extern __shared__ DD smc[];
+  DD* V = smc;               // [cap][cap]
+  DD* V2 = smc + cap * cap;  // [cap][cap]
+  __shared__ double red[256];
+  __shared__ long long lg2;
+  int rows, len;
+  if (!with_head && i_begin >= i_end) {
+    if (threadIdx.x == 0) { rec[0] = 0; rec[1] = 0; rec[2] = 0; }
+    return;
+  }
+  if (with_head) {
+    rows = 1;
+    len = (d > 1) ? rec_rank(c.rec_cur, c.RS, 0) : 1;
+    for (int t = threadIdx.x; t < len; t += blockDim.x) V[t] = c.W[t];  // W_0, row 0
+  } else {
+    rows = rec_rank(c.rec_cur, c.RS, i_begin);
+    len = rows;
+    for (int t = threadIdx.x; t < rows * rows; t += blockDim.x)
+      V[(t / rows) * cap + t % rows] = dd_make((t / rows == t % rows) ? 1.0 : 0.0);
+  }
+  if (threadIdx.x == 0) lg2 = 0;
+  __syncthreads();
+  for (int i = i_begin; i < i_end; ++i) {
+    const int nc = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+    const DD* Hi = c.H + (long long)i * cap * cap;
+    double mx = 0.0;
+    for (int t = threadIdx.x; t < rows * nc; t += blockDim.x) {
+      const int a = t / nc, col = t % nc;
+      DD acc = dd_make(0.0);
+      for (int k = 0; k < len; ++k) acc = dd_add(acc, dd_mul(V[a * cap + k], Hi[k * cap + col]));
+      V2[a * cap + col] = acc;
+      mx = fmax(mx, fabs(acc.hi));
+    }
+    mx = block_absmax(mx, red);
+    int ex = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
+    for (int t = threadIdx.x; t < rows * nc; t += blockDim.x) {
+      const int a = t / nc, col = t % nc;
+      V[a * cap + col] = dd_ldexp(V2[a * cap + col], -ex);
+    }
+    if (threadIdx.x == 0) lg2 += ex;
+    len = nc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { rec[0] = rows; rec[1] = len; rec[2] = (double)lg2; }
+  for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
+    const int a = t / len, col = t % len;
+    rec[3 + a * cap + col] = V[a * cap + col].hi;
+    rec[3 + (long long)cap * cap + a * cap + col] = V[a * cap + col].lo;
+  }
+}
+
+// Multiply the world records in rank order: out = [core_hi, log2scale, core_lo]; one CTA.
+__global__ void __launch_bounds__(256) k_finish(const double* recs, int world, int cap, double* out) {
+  __shared__ DD v[TTC_MAX_RANK_DEV], v2[TTC_MAX_RANK_DEV];
+  __shared__ double red[256];
+  __shared__ long long lg2;
+  __shared__ int len;
+  const long long RSZ = chain_record_size(cap);
+  const long long LO = (long long)cap * cap;
+  if (threadIdx.x == 0) {
+    lg2 = (long long)recs[2];
+    len = (int)recs[1];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < len; t += blockDim.x) v[t] = DD{recs[3 + t], recs[3 + LO + t]};
+  __syncthreads();
+  for (int p = 1; p < world; ++p) {
+    const double* R = recs + p * RSZ;
+    const int rows = (int)R[0], cols = (int)R[1];
+    if (rows == 0) continue;
+    double mx = 0.0;
+    for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+      DD acc = dd_make(0.0);
+      for (int k = 0; k < rows; ++k)
+        acc = dd_add(acc, dd_mul(v[k], DD{R[3 + k * cap + col], R[3 + LO + k * cap + col]}));
+      v2[col] = acc;
+      mx = fmax(mx, fabs(acc.hi));
+    }
+    mx = block_absmax(mx, red);
+    int ex = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
+    for (int col = threadIdx.x; col < cols; col += blockDim.x) v[col] = dd_ldexp(v2[col], -ex);
+    if (threadIdx.x == 0) { lg2 += ex + (long long)R[2]; len = cols; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[0] = v[0].hi + v[0].lo; out[1] = (double)lg2; }
+}
+
+}  // namespace ttc

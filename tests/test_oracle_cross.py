@@ -289,3 +289,29 @@ def test_c4_converges_toward_brute_force():
     st, val, _ = X.run(prob, 4)
     ref = ig.brute_force(FAMILY_C, prob.u, prob.w)
     assert abs(val - ref) < 1e-6 * ref
+
+
+def test_integrate_exact_agrees_with_fp64_when_well_conditioned():
+    """R9: the near-exact contraction equals the fp64 one to rounding on a well-conditioned
+    cross, and equals the full-grid sum of the TT reconstruction (eq. (3))."""
+    prob = make_problem(FAMILY_D, 3, 6, 3.0, 4)
+    st = X.sweep(prob, X.initial_state(prob))
+    v64, l64, s64, _ = X.integrate(prob, st)
+    vex, lex, sex = X.integrate_exact(prob, st)
+    assert s64 == sex and abs(v64 - vex) <= 1e-13 * abs(vex)
+    assert abs(vex - brute_tt_integral(prob, st)) <= 1e-11 * abs(vex)
+
+
+def test_dd_weighted_sum_is_accurate():
+    import mpmath
+    rng = np.random.default_rng(5)
+    F = rng.standard_normal((3, 4, 200)) * np.exp(rng.uniform(-30, 30, (3, 4, 200)))
+    w = rng.uniform(0, 1, 200)
+    hi, lo = X._dd_weighted_sum(F, w)
+    mpmath.mp.dps = 60
+    for a in range(3):
+        for b in range(4):
+            terms = [mpmath.mpf(float(w[k])) * mpmath.mpf(float(F[a, b, k])) for k in range(200)]
+            ex = mpmath.fsum(terms)
+            bound = mpmath.fsum([abs(t) for t in terms]) * mpmath.mpf(2) ** -98  # ~ n * 2^-106
+            assert abs((mpmath.mpf(float(hi[a, b])) + mpmath.mpf(float(lo[a, b]))) - ex) <= bound
