@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 TT-cross quadrature hot path (arXiv:1903.11554).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload D5] [--impl ours|reference]
+
+A *step* is one whole solve of the workload: reset to the seed-fixed
+initial pivots, the workload's full sweeps (every half-sweep = enrichment, fiber
+evaluation, cross + maxvol, commit, over all interfaces at once; Alg. 6) and the
+TT quadrature (§4.1).  ``value`` = integrand evaluations per second (the device
+counter of evaluated tensor entries ÷ device time), whole job, inputs resident in HBM.
+
+N = 1: the solve is one CUDA graph replayed per step (tt_solve_launch).  N > 1 (torchrun,
+one process per GPU, NCCL): interfaces are partitioned over ranks and the new pivots are
+all-gathered after every half-sweep (paper_1903_11554_b200.dist); total work is fixed, so
+scaling is "strong".  Timing: CUDA events on the library's stream around each step, L2
+flushed (256 MiB memset) before every timed step, barrier + synchronize on both sides, max
+over ranks.  ``e2e`` runs the same steps through the public API from pinned host buffers:
+tt_cross_load_grid (H2D of nodes + weights) -> tt_solve_launch -> tt_integrate_read (D2H of
+the result), timed by the host clock.  ``roofline`` comes from a second pass of the same
+steps with per-kernel CUDA events enabled (tt_cross_set_timing), for the kernel with the
+largest device time.  ``cpu_baseline`` times the oracle (test infrastructure, never the
+product path) on a bounded sample on rank 0.
+
+--impl reference: the oracle as the reference arm: each step is a bounded
+sample of the same workload on the host cores, same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from workloads import FAMILY_NAMES, WORKLOADS  # noqa: E402
+
+DEFAULT_WORKLOAD = "D5"   # BASELINE.json configs[1]
+L2_FLUSH_BYTES = 256 << 20
+# fp64 peak: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (max SM clock)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# --------------------------------------------------------------------------------------
+# clocks during the timed region
+# --------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------------------
+# roofline of the dominant kernel
+# --------------------------------------------------------------------------------------
+def roofline(kt, stats, family, peaks, peak_src):
+    """kt: {name: (launches, ms)} of the profiling pass; stats: its counters."""
+    name = max(kt, key=lambda k: kt[k][1])
+    launches, ms = kt[name]
+    avg_s = ms / max(1, launches) / 1e3
+    out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
+    if name == "k_fiber":
+        ent = stats["fiber_entries"] / max(1, launches)
+        # algorithmic: 8 B written per entry; family D adds ~26 fp64 flops per entry
+        # (two double-double products, rounding, one division)
+        gbs = ent * 8 / avg_s / 1e9
+        hbm = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+               "frac": gbs / peaks["hbm_gbs"], "units_per_launch": ent, "per_unit": "8 B/entry"}
+        if family == 1:
+            tf = ent * 26 / avg_s / 1e12
+            alu = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                   "frac": tf / FP64_PEAK_TFLOPS, "units_per_launch": ent, "per_unit": "26 fp64 flop/entry"}
+            out.update(alu if alu["frac"] > hbm["frac"] else hbm)
+        else:
+            out.update(hbm)
+    elif name == "k_cross":
+        upd = stats["cross_updates"] / max(1, launches)
+        tf = upd * 2 / avg_s / 1e12  # one mul + one sub per element update (no FMA, R4)
+        out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": tf / FP64_PEAK_TFLOPS, "units_per_launch": upd, "per_unit": "2 fp64 flop/element update",
+                    "steps_per_launch": stats["cross_steps"] / max(1, launches),
+                    "us_per_step": avg_s * 1e6 / max(1e-9, stats["cross_steps"] / max(1, launches))})
+    else:
+        out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
+    out["peak_source"] = "derived fp64 (DESIGN.md §6)" if out.get("unit") == "TFLOP/s" else f"{peak_src} MEASURED_PEAKS.json"
+    return out
+
+
+# --------------------------------------------------------------------------------------
+# oracle leg (cpu_baseline and --impl reference)
+# --------------------------------------------------------------------------------------
+def oracle_sample(wl, budget_s):
+    """Run the oracle on a bounded sample of the workload; returns (evals, seconds, what).
+
+    Small workloads (every fiber of a sweep fits a few seconds): whole solves
+    (init + sweeps + quadrature), repeated while the budget lasts.  Large ones: the first
+    L->R half-sweep interface by interface (each interface = enrichment, fiber, cross,
+    maxvol), stopped when the budget is spent.
+    """
+    from threadpoolctl import threadpool_limits
+    from oracle import cross as X
+    u, w = wl.grid()
+    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_enrich, wl.maxvol_delta, wl.max_swaps, wl.seed)
+    evals, t0 = 0, time.perf_counter()
+    with threadpool_limits(1):
+        if wl.d <= 10 and wl.rank_cap <= 16:
+            solves = 0
+            while True:
+                st, val, _ = X.run(prob, wl.sweeps)
+                evals += st.n_evals
+                solves += 1
+                if time.perf_counter() - t0 > budget_s:
+                    break
+            return evals, time.perf_counter() - t0, f"{solves} full solve(s) ({wl.sweeps} sweeps + quadrature)"
+        st = X.initial_state(prob)
+        done = 0
+        for i in range(wl.d - 1):
+            _, info = X.update_interface(prob, st, i, X.DIR_LR)
+            evals += info["evals"]
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        return evals, time.perf_counter() - t0, f"{done} interface update(s) of the first L->R half-sweep"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    budget = max(0.5, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(wl, budget)
+    tot_e, tot_s, what = 0, 0.0, ""
+    for _ in range(args.steps):
+        e, s, what = oracle_sample(wl, budget)
+        tot_e += e
+        tot_s += s
+    v = tot_e / tot_s
+    line = {
+        "impl": "reference", "metric": "integrand evals/sec (fp64)", "value": v, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(wl, args.gpus),
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": 1, "kind": "oracle",
+                         "sample": f"per step: {what} of {wl.name} (numpy fp64, 1 thread)"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(wl, n):
+    return {"workload": f"{FAMILY_NAMES[wl.family]}_{wl.d}", "d": wl.d, "n": wl.n, "L": wl.L,
+            "rank_cap": wl.rank_cap, "tol": wl.tol, "sweeps": wl.sweeps, "n_enrich": wl.n_enrich,
+            "maxvol_delta": wl.maxvol_delta, "seed": wl.seed, "parallelism": f"interfaces/{n}",
+            "l2": "flushed (256 MiB memset) before every timed step"}
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1903_11554_b200 import TTCross
+    from paper_1903_11554_b200.dist import DistTTCross
+
+    wl = WORKLOADS[args.workload]
+    u, w = wl.grid()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    u_d = torch.from_numpy(u).to(dev)
+    w_d = torch.from_numpy(w).to(dev)
+    kw = dict(n_enrich=wl.n_enrich, max_swaps=wl.max_swaps, delta=wl.maxvol_delta, seed=wl.seed)
+    use_graph = world == 1 and not args.no_graph
+    if world == 1:
+        tt = TTCross(wl.family, u_d, w_d, wl.rank_cap, wl.tol, stream=stream.cuda_stream, **kw)
+
+        def step():
+            tt.solve_launch(wl.sweeps, graph=use_graph)
+
+        def result():
+            return tt.integrate_read()
+        core = tt
+    else:
+        dtt = DistTTCross(wl.family, u_d, w_d, wl.rank_cap, wl.tol, **kw)
+
+        last = {}
+
+        def step():
+            last["v"] = dtt.solve(wl.sweeps)
+
+        def result():
+            return last["v"]
+        core = dtt.tt
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_ramp = time.perf_counter()
+    while time.perf_counter() - t_ramp < 0.3:  # let the SM clock leave idle before warm-up
+        flush.zero_()
+        torch.cuda.synchronize()
+    for _ in range(max(3, args.warmup)):
+        step()
+        val = result()
+    barrier()
+    st0 = core.stats()
+    evals_step = st0["evals"]
+    launches_step = st0["launches"]
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    val = result()
+    t = torch.tensor([ms, float(evals_step)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_max, evals_total = float(tmax.item()), float(tsum.item())
+    else:
+        ms_max, evals_total = ms, float(evals_step)
+    value = evals_total * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the public API from pinned host buffers (host clock)
+    u_h = torch.from_numpy(u).pin_memory()
+    w_h = torch.from_numpy(w).pin_memory()
+    h2d = 2 * u.size * 8
+    d2h = 2 * 8 + 4
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        core.load_grid(u_h.numpy(), w_h.numpy())
+        if world == 1:
+            tt.solve_launch(wl.sweeps, graph=use_graph)
+            e2e_val = tt.integrate_read()
+        else:
+            dtt.sweep(wl.sweeps)
+            e2e_val = dtt.integrate()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+    e2e = {"value": evals_total * args.steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "timer": "host clock around synchronous steps"}
+
+    # ---- per-kernel profile pass (eager launches, CUDA events around every launch); every
+    # solve resets the library's counters, so they are accumulated here solve by solve
+    nprof = max(3, min(args.steps, 50))
+    barrier()
+    core.set_timing(True)
+    kt, st = {}, {}
+    for _ in range(nprof):
+        if world == 1:
+            tt.solve_launch(wl.sweeps, graph=False)
+            tt.integrate_read()
+        else:
+            dtt.solve(wl.sweeps)
+        for k, (nl, kms) in core.kernel_times().items():
+            a, b = kt.get(k, (0, 0.0))
+            kt[k] = (a + nl, b + kms)
+        for k, v in core.stats().items():
+            st[k] = st.get(k, 0) + v
+    core.set_timing(False)
+    peaks, peak_src = measured_peaks()
+    roof = roofline(kt, st, wl.family, peaks, peak_src)
+    kernel_ms = {k: v[1] / nprof for k, v in kt.items() if v[0]}
+
+    # ---- oracle on the host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        e, s, what = oracle_sample(wl, args.cpu_seconds)
+        cpu = {"value": e / s, "unit": "evals/s", "cores": 1, "kind": "oracle",
+               "sample": f"{what} of {wl.name} (numpy fp64, 1 thread), {s:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "integrand evals/sec (fp64)", "value": value, "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(wl, world),
+            "evals_per_step": evals_total, "sweep_ms": ms_max / args.steps,
+            "integral": {"value": val[0], "log10_abs": val[1], "sign": val[2]},
+            "graph": use_graph, "gpu_launches": int(launches_step) * args.steps,
+            "roofline": roof, "kernel_ms_per_solve": kernel_ms, "clocks": clocks, "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    core.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -69,9 +69,13 @@ typedef struct ttc_stats {
   double  ms_cross;        /* device time of the cross/maxvol kernel                       */
   double  ms_quad;         /* device time of the quadrature kernels                        */
   double  ms_other;        /* device time of the remaining kernels                         */
-  int64_t fiber_launches;  /* number of k_fiber launches timed                             */
-  int64_t cross_launches;  /* number of k_cross launches timed                             */
-  int64_t fiber_entries;   /* entries written by the timed k_fiber launches                */
+  int64_t fiber_launches;  /* k_fiber launches since the last reset                        */
+  int64_t cross_launches;  /* k_cross launches since the last reset                        */
+  int64_t fiber_entries;   /* entries written by k_fiber (device counter)                  */
+  int64_t cross_updates;   /* matrix elements updated by k_cross: sum over jobs of
+                              nrows*ncols*rank + nrows*rank*swaps (algorithmic)            */
+  int64_t cross_steps;     /* pivot + swap steps of k_cross, summed over jobs              */
+  int64_t cross_elems;     /* fiber-matrix elements loaded by k_cross (nrows*ncols per job) */
 } ttc_stats;
 
 /*
@@ -92,6 +96,34 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u,
 /* tt_cross_reset -- restore the initial pivots (device copy, no host work) and zero the
  * statistics.  Lets a benchmark time repeated solves from the same seed. */
 int tt_cross_reset(ttc_ctx* ctx);
+
+/*
+ * tt_cross_load_grid -- replace the grid of an existing context (same d and n) and restore
+ * the initial pivots (tt_cross_reset).  nodes_u / weights / mem_kind as in tt_cross_init;
+ * host arrays should be pinned for an asynchronous copy.  This is the per-problem input
+ * upload of the end-to-end path (§4.1: a new function on the tensor grid).
+ * Errors: TTC_ERR_ARG (non-positive host node), TTC_ERR_STATE (pending half-sweep).
+ */
+int tt_cross_load_grid(ttc_ctx* ctx, const double* nodes_u, const double* weights, int32_t mem_kind);
+
+/*
+ * tt_solve_launch -- enqueue one whole solve on the context stream, asynchronously:
+ * reset to the initial pivots, n_sweeps full sweeps (as tt_cross_sweep) and the quadrature
+ * (as tt_integrate_launch).  use_graph != 0 captures this sequence once as a CUDA graph
+ * (re-captured when n_sweeps changes) and replays it; the result is bit-identical to the
+ * eager sequence.  world == 1 only.  Read the result with tt_integrate_read.
+ */
+int tt_solve_launch(ttc_ctx* ctx, int32_t n_sweeps, int32_t use_graph);
+
+/*
+ * tt_integrate_launch / tt_integrate_read -- tt_integrate split in two: _launch enqueues
+ * the quadrature kernels and the device->host copy of the 16-byte result into pinned memory
+ * (no synchronisation); _read synchronises the stream and decodes value / log10|value| /
+ * sign exactly as tt_integrate.  world == 1 for _launch.  _read returns TTC_ERR_SINGULAR
+ * like tt_integrate.
+ */
+int tt_integrate_launch(ttc_ctx* ctx);
+int tt_integrate_read(ttc_ctx* ctx, double* value, double* log10_abs, int32_t* sign);
 
 /*
  * tt_cross_sweep -- n_sweeps full sweeps (L->R half-sweep then R->L half-sweep), each
@@ -157,6 +189,13 @@ int tt_cross_get_state(ttc_ctx* ctx, int32_t* ranks_out, int32_t* piv_out);
 int tt_cross_get_fiber(ttc_ctx* ctx, int32_t mode, double* out, int64_t capacity,
                        int32_t* rx, int32_t* ry);
 int tt_cross_get_stats(ttc_ctx* ctx, ttc_stats* out);
+
+/* tt_cross_get_kernel_time -- per-kernel launch count and accumulated device time (ms,
+ * timing enabled) for kernel id kid in [0, 13): 0 k_prep_nodes, 1 k_enrich,
+ * 2 k_frozen_sides, 3 k_frozen_q, 4 k_frozen_lr, 5 k_fiber, 6 k_cross, 7 k_commit, 8 k_wsum,
+ * 9 k_intersection, 10 k_solve, 11 k_chain, 12 k_finish.  *name is a static string.
+ * Errors: TTC_ERR_ARG for kid out of range. */
+int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64_t* launches, double* ms);
 
 /* tt_cross_set_timing -- 1: bracket every kernel launch with CUDA events on the context
  * stream and accumulate per-class device time (ttc_stats.ms_*); 0: off (default). */

@@ -28,8 +28,10 @@ EXPORTS = [
     "tt_cross_commit", "tt_cross_exchange_buffer", "tt_integrate", "tt_integrate_local",
     "tt_integrate_partials_buffer", "tt_integrate_finish", "tt_cross_get_state",
     "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_set_timing", "tt_cross_destroy",
-    "tt_last_error", "tt_build_info",
+    "tt_last_error", "tt_build_info", "tt_cross_load_grid", "tt_solve_launch",
+    "tt_integrate_launch", "tt_integrate_read", "tt_cross_get_kernel_time",
 ]
+N_KERNELS = 13
 
 
 class TtcConfig(ctypes.Structure):
@@ -47,6 +49,7 @@ class TtcStats(ctypes.Structure):
         ("half_sweeps", ctypes.c_int32), ("ms_fiber", ctypes.c_double), ("ms_cross", ctypes.c_double),
         ("ms_quad", ctypes.c_double), ("ms_other", ctypes.c_double), ("fiber_launches", ctypes.c_int64),
         ("cross_launches", ctypes.c_int64), ("fiber_entries", ctypes.c_int64),
+        ("cross_updates", ctypes.c_int64), ("cross_steps", ctypes.c_int64), ("cross_elems", ctypes.c_int64),
     ]
 
 
@@ -79,6 +82,12 @@ def load(path: str = LIB_PATH):
         "tt_cross_get_stats": (i32, [P, ctypes.POINTER(TtcStats)]),
         "tt_cross_set_timing": (i32, [P, i32]),
         "tt_cross_destroy": (None, [P]),
+        "tt_cross_load_grid": (i32, [P, P, P, i32]),
+        "tt_cross_get_kernel_time": (i32, [P, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64),
+                                           ctypes.POINTER(f64)]),
+        "tt_solve_launch": (i32, [P, i32, i32]),
+        "tt_integrate_launch": (i32, [P]),
+        "tt_integrate_read": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
         "tt_last_error": (ctypes.c_char_p, []),
         "tt_build_info": (ctypes.c_char_p, []),
     }
@@ -174,6 +183,25 @@ class TTCross:
                "tt_integrate")
         return v.value, l10.value, sg.value
 
+    def load_grid(self, u, w):
+        pu, ku, keep_u = _ptr_and_kind(u)
+        pw, kw, keep_w = _ptr_and_kind(w)
+        if ku != kw:
+            raise TypeError("nodes and weights must both be host or both be device arrays")
+        _check(self.lib, self.lib.tt_cross_load_grid(self._h, pu, pw, ku), "tt_cross_load_grid")
+
+    def solve_launch(self, n_sweeps, graph=True):
+        _check(self.lib, self.lib.tt_solve_launch(self._h, int(n_sweeps), 1 if graph else 0), "tt_solve_launch")
+
+    def integrate_launch(self):
+        _check(self.lib, self.lib.tt_integrate_launch(self._h), "tt_integrate_launch")
+
+    def integrate_read(self):
+        v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        _check(self.lib, self.lib.tt_integrate_read(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
+               "tt_integrate_read")
+        return v.value, l10.value, sg.value
+
     def integrate_local(self):
         _check(self.lib, self.lib.tt_integrate_local(self._h), "tt_integrate_local")
 
@@ -218,6 +246,17 @@ class TTCross:
         s = TtcStats()
         _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
         return {f: getattr(s, f) for f, _ in TtcStats._fields_}
+
+
+    def kernel_times(self):
+        """{kernel name: (launches, ms)} since the last reset (ms only with timing on)."""
+        out = {}
+        for k in range(N_KERNELS):
+            nm, nl, ms = ctypes.c_char_p(), ctypes.c_int64(), ctypes.c_double()
+            _check(self.lib, self.lib.tt_cross_get_kernel_time(self._h, k, ctypes.byref(nm), ctypes.byref(nl),
+                                                               ctypes.byref(ms)), "tt_cross_get_kernel_time")
+            out[nm.value.decode()] = (nl.value, ms.value)
+        return out
 
 
 def build_info():

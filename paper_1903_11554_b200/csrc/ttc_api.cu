@@ -35,10 +35,20 @@ int fail(int code, const std::string& msg) {
 
 enum KClass { KC_FIBER = 0, KC_CROSS = 1, KC_QUAD = 2, KC_OTHER = 3 };
 
+// per-kernel identifiers for tt_cross_get_kernel_time (class = accounting bucket of ttc_stats)
+enum KId {
+  K_PREP = 0, K_ENRICH, K_FROZEN_SIDES, K_FROZEN_Q, K_FROZEN_LR, K_FIBER, K_CROSS, K_COMMIT,
+  K_WSUM, K_INTERSECTION, K_SOLVE, K_CHAIN, K_FINISH, K_COUNT
+};
+const char* const kKernelName[K_COUNT] = {
+    "k_prep_nodes", "k_enrich", "k_frozen_sides", "k_frozen_q", "k_frozen_lr", "k_fiber", "k_cross",
+    "k_commit", "k_wsum", "k_intersection", "k_solve", "k_chain", "k_finish"};
+const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_FIBER, KC_FIBER, KC_FIBER, KC_FIBER, KC_CROSS,
+                                   KC_OTHER, KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD};
+
 struct EvRec {
   cudaEvent_t a, b;
-  int cls;
-  long long entries;
+  int kid;
 };
 
 }  // namespace
@@ -46,6 +56,12 @@ struct EvRec {
 struct ttc_ctx {
   ttc_config cfg{};
   cudaStream_t stream = nullptr;
+  cudaStream_t ls = nullptr;        // launch stream: `stream`, or the capture stream while a graph is built
+  cudaStream_t cap_stream = nullptr; // private stream used to capture the solve graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_sweeps = -1;
+  long long graph_launches = 0;
   DevCtx dc{};
   int chunk = 0, kb = 0, ke = 0, n_owned = 0, slots = 0;
   int sweeps = 0, half_sweeps = 0;
@@ -67,7 +83,8 @@ struct ttc_ctx {
   std::vector<EvRec> evs;
   std::vector<cudaEvent_t> ev_pool;
   double ms[4] = {0, 0, 0, 0};
-  long long fiber_launches = 0, cross_launches = 0, fiber_entries = 0;
+  double kms[K_COUNT] = {};
+  long long klaunch[K_COUNT] = {};
 };
 
 namespace {
@@ -98,21 +115,21 @@ cudaEvent_t get_event(ttc_ctx* c) {
 // bracket a launch with events when timing is enabled
 struct Timed {
   ttc_ctx* c;
-  int cls;
-  long long entries;
+  int kid;
   cudaEvent_t a = nullptr;
-  Timed(ttc_ctx* c_, int cls_, long long e_ = 0) : c(c_), cls(cls_), entries(e_) {
+  Timed(ttc_ctx* c_, int kid_) : c(c_), kid(kid_) {
     c->launches++;
+    c->klaunch[kid]++;
     if (c->timing) {
       a = get_event(c);
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, c->ls);
     }
   }
   ~Timed() {
     if (c->timing) {
       cudaEvent_t b = get_event(c);
-      cudaEventRecord(b, c->stream);
-      c->evs.push_back({a, b, cls, entries});
+      cudaEventRecord(b, c->ls);
+      c->evs.push_back({a, b, kid});
     }
   }
 };
@@ -196,30 +213,29 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
   const int nc = dc.ncols_max, n = dc.n;
   const int tup_max = std::max(nc, dc.cap);
   {
-    Timed t(c, KC_FIBER);
-    k_frozen_sides<<<dim3((tup_max + 63) / 64, 2, njobs), 64, 0, c->stream>>>(dc, kind, jbase);
+    Timed t(c, K_FROZEN_SIDES);
+    k_frozen_sides<<<dim3((tup_max + 63) / 64, 2, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
   }
   if (int e = check_launch("k_frozen_sides")) return e;
   if (dc.family == TTC_FAMILY_D) {
     {
-      Timed t(c, KC_FIBER);
-      k_frozen_q<<<dim3((n + 127) / 128, tup_max, 2 * njobs), 128, 0, c->stream>>>(dc, kind, jbase);
+      Timed t(c, K_FROZEN_Q);
+      k_frozen_q<<<dim3((n + 127) / 128, tup_max, 2 * njobs), 128, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_q")) return e;
     {
-      Timed t(c, KC_FIBER);
-      k_frozen_lr<<<dim3((tup_max + 63) / 64, tup_max, njobs), 64, 0, c->stream>>>(dc, kind, jbase);
+      Timed t(c, K_FROZEN_LR);
+      k_frozen_lr<<<dim3((tup_max + 63) / 64, tup_max, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_lr")) return e;
   }
   const int gx = std::min(4096, (tup_max * n + 255) / 256);
   {
-    Timed t(c, KC_FIBER, -1);
-    c->fiber_launches++;
+    Timed t(c, K_FIBER);
     if (dc.family == TTC_FAMILY_C)
-      k_fiber<0><<<dim3(gx, tup_max, njobs), 256, 0, c->stream>>>(dc, kind, jbase);
+      k_fiber<0><<<dim3(gx, tup_max, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
     else
-      k_fiber<1><<<dim3(gx, tup_max, njobs), 256, 0, c->stream>>>(dc, kind, jbase);
+      k_fiber<1><<<dim3(gx, tup_max, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
   }
   return check_launch("k_fiber");
 }
@@ -229,7 +245,7 @@ int launch_cross(ttc_ctx* c, int kind) {
   lc.gridDim = dim3(c->n_owned * c->G);
   lc.blockDim = dim3(CROSS_THREADS);
   lc.dynamicSmemBytes = c->cross_smem;
-  lc.stream = c->stream;
+  lc.stream = c->ls;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = c->G;
@@ -239,8 +255,7 @@ int launch_cross(ttc_ctx* c, int kind) {
   lc.numAttrs = 1;
   cudaError_t e;
   {
-    Timed t(c, KC_CROSS);
-    c->cross_launches++;
+    Timed t(c, K_CROSS);
     if (c->smem_mode)
       e = cudaLaunchKernelEx(&lc, k_cross<true>, c->dc, kind, c->G, c->rpc);
     else
@@ -254,15 +269,15 @@ int do_half_sweep(ttc_ctx* c, int dir) {
   if (c->n_owned > 0) {
     DevCtx& dc = c->dc;
     {
-      Timed t(c, KC_OTHER);
-      k_enrich<<<c->n_owned, 128, 0, c->stream>>>(dc, dir, c->sweeps);
+      Timed t(c, K_ENRICH);
+      k_enrich<<<c->n_owned, 128, 0, c->ls>>>(dc, dir, c->sweeps);
     }
     if (int e = check_launch("k_enrich")) return e;
     if (int e = launch_fibers(c, dir, 0, c->n_owned)) return e;
     if (int e = launch_cross(c, dir)) return e;
     {
-      Timed t(c, KC_OTHER);
-      k_commit<<<dim3(dc.cap, c->n_owned), 64, 0, c->stream>>>(dc, dir);
+      Timed t(c, K_COMMIT);
+      k_commit<<<dim3(dc.cap, c->n_owned), 64, 0, c->ls>>>(dc, dir);
     }
     if (int e = check_launch("k_commit")) return e;
   }
@@ -293,41 +308,48 @@ int do_integrate_local(ttc_ctx* c) {
   if (nm > 0) {
     if (int e = launch_fibers(c, JOB_INT, m_lo, nm)) return e;
     {
-      Timed t(c, KC_QUAD);
-      k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->stream>>>(dc, m_lo);
+      Timed t(c, K_WSUM);
+      k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->ls>>>(dc, m_lo);
     }
     if (int e = check_launch("k_wsum")) return e;
   }
-  CK(cudaMemsetAsync(dc.flags, 0, 4 * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(dc.flags, 0, 4 * sizeof(int), c->ls));
   if (c->n_owned > 0) {
     {
-      Timed t(c, KC_QUAD);
-      k_intersection<<<dim3((cap + 63) / 64, cap, c->n_owned), 64, 0, c->stream>>>(dc, c->kb);
+      Timed t(c, K_INTERSECTION);
+      k_intersection<<<dim3((cap + 63) / 64, cap, c->n_owned), 64, 0, c->ls>>>(dc, c->kb);
     }
     if (int e = check_launch("k_intersection")) return e;
     {
-      Timed t(c, KC_QUAD);
-      k_solve<<<c->n_owned, 256, 2 * cap * cap * sizeof(DD), c->stream>>>(dc);
+      Timed t(c, K_SOLVE);
+      k_solve<<<c->n_owned, 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc);
     }
     if (int e = check_launch("k_solve")) return e;
   }
   double* rec = c->partials + (long long)rank * chain_record_size(cap);
   {
-    Timed t(c, KC_QUAD);
-    k_chain<<<1, 256, 2 * cap * cap * sizeof(DD), c->stream>>>(dc, c->kb, c->ke, rank == 0 ? 1 : 0, rec);
+    Timed t(c, K_CHAIN);
+    k_chain<<<1, 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc, c->kb, c->ke, rank == 0 ? 1 : 0, rec);
   }
   return check_launch("k_chain");
 }
 
-int do_integrate_finish(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
-  const int cap = c->dc.cap, d = c->dc.d;
+// enqueue k_finish and the D2H copy of the result into pinned host memory (no sync)
+int do_integrate_finish_launch(ttc_ctx* c) {
+  const int cap = c->dc.cap;
   {
-    Timed t(c, KC_QUAD);
-    k_finish<<<1, 256, 0, c->stream>>>(c->partials, c->cfg.world, cap, c->out_dev);
+    Timed t(c, K_FINISH);
+    k_finish<<<1, 256, 0, c->ls>>>(c->partials, c->cfg.world, cap, c->out_dev);
   }
   if (int e = check_launch("k_finish")) return e;
-  CK(cudaMemcpyAsync(c->out_host, c->out_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->out_host + 2, c->dc.flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->out_host, c->out_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->ls));
+  CK(cudaMemcpyAsync(c->out_host + 2, c->dc.flags, sizeof(int), cudaMemcpyDeviceToHost, c->ls));
+  return TTC_OK;
+}
+
+// wait for the enqueued result and decode it (value outside the fp64 range -> +-0/inf)
+int do_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  const int d = c->dc.d;
   CK(cudaStreamSynchronize(c->stream));
   int flag = 0;
   std::memcpy(&flag, c->out_host + 2, sizeof(int));
@@ -367,12 +389,72 @@ int resolve_timing(ttc_ctx* c) {
   for (auto& r : c->evs) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
-    c->ms[r.cls] += ms;
+    c->ms[kKernelClass[r.kid]] += ms;
+    c->kms[r.kid] += ms;
     c->ev_pool.push_back(r.a);
     c->ev_pool.push_back(r.b);
   }
   c->evs.clear();
   return TTC_OK;
+}
+
+// device part of a reset (async, capturable): initial pivots and the evaluation counter
+int reset_device(ttc_ctx* c) {
+  CK(cudaMemcpyAsync(c->dc.rec_cur, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->ls));
+  CK(cudaMemcpyAsync(c->dc.rec_next, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->ls));
+  CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
+  return TTC_OK;
+}
+
+int reset_host(ttc_ctx* c) {
+  c->sweeps = 0;
+  c->half_sweeps = 0;
+  c->pending = 0;
+  c->launches = 0;
+  if (int e = resolve_timing(c)) return e;
+  for (double& m : c->ms) m = 0.0;
+  for (int k = 0; k < K_COUNT; ++k) { c->kms[k] = 0.0; c->klaunch[k] = 0; }
+  return TTC_OK;
+}
+
+// n_sweeps full sweeps + the quadrature, enqueued on c->ls (world == 1)
+int enqueue_solve(ttc_ctx* c, int n_sweeps) {
+  for (int s = 0; s < n_sweeps; ++s)
+    for (int dir : {TTC_DIR_LR, TTC_DIR_RL}) {
+      if (int e = do_half_sweep(c, dir)) return e;
+      if (int e = do_commit(c)) return e;
+    }
+  if (int e = do_integrate_local(c)) return e;
+  return do_integrate_finish_launch(c);
+}
+
+// Capture reset + n_sweeps sweeps + quadrature as one CUDA graph.  Every launch shape
+// depends only on (d, n, cap, p); ranks are read on the device, so the graph is valid for
+// any grid loaded into this context.
+int capture_solve(ttc_ctx* c, int n_sweeps) {
+  if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  if (int e = reset_host(c)) return e;
+  const bool timing = c->timing;
+  c->timing = false;
+  c->ls = c->cap_stream;
+  int rc = TTC_OK;
+  cudaError_t ce = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (ce != cudaSuccess) rc = fail(TTC_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(ce));
+  if (!rc) rc = reset_device(c);
+  if (!rc) rc = enqueue_solve(c, n_sweeps);
+  cudaGraph_t g = nullptr;
+  ce = cudaStreamEndCapture(c->cap_stream, &g);
+  c->ls = c->stream;
+  c->timing = timing;
+  if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+  if (ce != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+  c->graph = g;
+  CK(cudaGraphInstantiate(&c->graph_exec, g, 0));
+  c->graph_sweeps = n_sweeps;
+  c->graph_launches = c->launches;
+  return reset_host(c);
 }
 
 }  // namespace
@@ -412,6 +494,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   c->cfg = k;
   if (c->cfg.max_swaps == 0) c->cfg.max_swaps = 2 * k.rank_cap;
   c->stream = static_cast<cudaStream_t>(stream);
+  c->ls = c->stream;
   const int d = k.d, n = k.n, cap = k.rank_cap, p = k.n_enrich;
   DevCtx& dc = c->dc;
   dc.family = k.family;
@@ -465,7 +548,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.sel_rank, (size_t)c->slots)) || (e = dalloc(c, &dc.sel_nsw, (size_t)c->slots)) ||
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
-      (e = dalloc(c, &dc.counters, 4)) ||
+      (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) ||
       (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)))
     return bail(e);
   if (k.family == TTC_FAMILY_D) {
@@ -484,7 +567,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("grid upload: ") + cudaGetErrorString(ce)));
   }
   {
-    Timed t(c, KC_OTHER);
+    Timed t(c, K_PREP);
     k_prep_nodes<<<(d * n + 255) / 256, 256, 0, c->stream>>>(u, chi, clo, d * n);
   }
   if ((e = check_launch("k_prep_nodes"))) return bail(e);
@@ -539,17 +622,63 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
 
 int tt_cross_reset(ttc_ctx* c) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  CK(cudaMemcpyAsync(c->dc.rec_cur, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->dc.rec_next, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemsetAsync(c->dc.counters, 0, 4 * sizeof(unsigned long long), c->stream));
-  c->sweeps = 0;
-  c->half_sweeps = 0;
-  c->pending = 0;
-  c->launches = 0;
-  if (int e = resolve_timing(c)) return e;
-  for (double& m : c->ms) m = 0.0;
-  c->fiber_launches = c->cross_launches = c->fiber_entries = 0;
+  if (int e = reset_device(c)) return e;
+  return reset_host(c);
+}
+
+int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights, int32_t mem_kind) {
+  if (!c || !nodes_u || !weights) return fail(TTC_ERR_ARG, "null argument");
+  if (mem_kind != TTC_MEM_HOST && mem_kind != TTC_MEM_DEVICE) return fail(TTC_ERR_ARG, "mem_kind");
+  const int d = c->dc.d, n = c->dc.n;
+  if (mem_kind == TTC_MEM_HOST)
+    for (long long t = 0; t < (long long)d * n; ++t)
+      if (!(nodes_u[t] > 0.0) || !std::isfinite(nodes_u[t])) return fail(TTC_ERR_ARG, "u-nodes must be finite and > 0");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  const cudaMemcpyKind kind = mem_kind == TTC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CK(cudaMemcpyAsync(const_cast<double*>(c->dc.u), nodes_u, sizeof(double) * d * n, kind, c->stream));
+  CK(cudaMemcpyAsync(const_cast<double*>(c->dc.w), weights, sizeof(double) * d * n, kind, c->stream));
+  {
+    Timed t(c, K_PREP);
+    k_prep_nodes<<<(d * n + 255) / 256, 256, 0, c->stream>>>(c->dc.u, const_cast<long long*>(c->dc.chi),
+                                                             const_cast<long long*>(c->dc.clo), d * n);
+  }
+  if (int e = check_launch("k_prep_nodes")) return e;
+  return tt_cross_reset(c);
+}
+
+int tt_solve_launch(ttc_ctx* c, int32_t n_sweeps, int32_t use_graph) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_solve_launch needs world == 1");
+  if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (!use_graph) {
+    if (int e = reset_device(c)) return e;
+    if (int e = reset_host(c)) return e;
+    if (int e = enqueue_solve(c, n_sweeps)) return e;
+    return TTC_OK;
+  }
+  if (!c->graph_exec || c->graph_sweeps != n_sweeps) {
+    if (int e = capture_solve(c, n_sweeps)) return e;
+  }
+  if (int e = reset_host(c)) return e;
+  CK(cudaGraphLaunch(c->graph_exec, c->stream));
+  c->launches = c->graph_launches;
+  c->sweeps = n_sweeps;
+  c->half_sweeps = 2 * n_sweeps;
   return TTC_OK;
+}
+
+int tt_integrate_launch(ttc_ctx* c) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate_launch needs world == 1");
+  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (int e = do_integrate_local(c)) return e;
+  return do_integrate_finish_launch(c);
+}
+
+int tt_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  return do_integrate_read(c, value, log10_abs, sign);
 }
 
 int tt_cross_half_sweep(ttc_ctx* c, int32_t direction) {
@@ -591,7 +720,8 @@ int tt_integrate(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
   if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate needs world == 1");
   if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
   if (int e = do_integrate_local(c)) return e;
-  return do_integrate_finish(c, value, log10_abs, sign);
+  if (int e = do_integrate_finish_launch(c)) return e;
+  return do_integrate_read(c, value, log10_abs, sign);
 }
 
 int tt_integrate_local(ttc_ctx* c) {
@@ -611,7 +741,8 @@ int tt_integrate_partials_buffer(ttc_ctx* c, void** dev_ptr, int64_t* bytes_tota
 
 int tt_integrate_finish(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  return do_integrate_finish(c, value, log10_abs, sign);
+  if (int e = do_integrate_finish_launch(c)) return e;
+  return do_integrate_read(c, value, log10_abs, sign);
 }
 
 int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out) {
@@ -653,12 +784,12 @@ int tt_cross_get_fiber(ttc_ctx* c, int32_t mode, double* out, int64_t capacity, 
 
 int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
   if (!c || !out) return fail(TTC_ERR_ARG, "null argument");
-  unsigned long long cnt = 0;
-  CK(cudaMemcpyAsync(&cnt, c->dc.counters, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long cnt[TTC_NCOUNTERS] = {};
+  CK(cudaMemcpyAsync(cnt, c->dc.counters, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (int e = resolve_timing(c)) return e;
   std::memset(out, 0, sizeof(*out));
-  out->evals = (int64_t)cnt;
+  out->evals = (int64_t)cnt[CNT_EVALS];
   out->launches = c->launches;
   out->sweeps = c->sweeps;
   out->half_sweeps = c->half_sweeps;
@@ -666,9 +797,22 @@ int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
   out->ms_cross = c->ms[KC_CROSS];
   out->ms_quad = c->ms[KC_QUAD];
   out->ms_other = c->ms[KC_OTHER];
-  out->fiber_launches = c->fiber_launches;
-  out->cross_launches = c->cross_launches;
-  out->fiber_entries = c->fiber_entries;
+  out->fiber_launches = c->klaunch[K_FIBER];
+  out->cross_launches = c->klaunch[K_CROSS];
+  out->fiber_entries = (int64_t)cnt[CNT_FIBER_ENTRIES];
+  out->cross_updates = (int64_t)cnt[CNT_CROSS_UPDATES];
+  out->cross_steps = (int64_t)cnt[CNT_CROSS_STEPS];
+  out->cross_elems = (int64_t)cnt[CNT_CROSS_ELEMS];
+  return TTC_OK;
+}
+
+int tt_cross_get_kernel_time(ttc_ctx* c, int32_t kid, const char** name, int64_t* launches, double* ms) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (kid < 0 || kid >= K_COUNT) return fail(TTC_ERR_ARG, "kernel id out of range");
+  if (int e = resolve_timing(c)) return e;
+  if (name) *name = kKernelName[kid];
+  if (launches) *launches = c->klaunch[kid];
+  if (ms) *ms = c->kms[kid];
   return TTC_OK;
 }
 
@@ -686,6 +830,9 @@ void tt_cross_destroy(ttc_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->out_host) cudaFreeHost(c->out_host);
   delete c;

@@ -269,6 +269,12 @@ __global__ void __launch_bounds__(CROSS_THREADS, 1) k_cross(DevCtx c, int kind, 
     if (tid == 0) {
       c.sel_rank[job] = r;
       c.sel_nsw[job] = nsw;
+      if (c.counters) {
+        atomicAdd(&c.counters[CNT_CROSS_UPDATES],
+                  (unsigned long long)(nrows * ncols * r + nrows * (long long)r * nsw));
+        atomicAdd(&c.counters[CNT_CROSS_STEPS], (unsigned long long)(r + nsw));
+        atomicAdd(&c.counters[CNT_CROSS_ELEMS], (unsigned long long)(nrows * ncols));
+      }
     }
     if (tid < r) {
       c.sel_row[(long long)job * c.cap + tid] = (int)S.row_of_slot[tid];

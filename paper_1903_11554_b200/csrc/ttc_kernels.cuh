@@ -99,7 +99,10 @@ __global__ void k_frozen_sides(DevCtx c, int kind, int jbase) {
   Job jb = make_job(c, kind, j);
   const int d = c.d, n = c.n, m = jb.m;
   const long long so = (long long)j * c.ncols_max + t;
-  if (side == 0 && t == 0 && c.counters) atomicAdd(&c.counters[0], (unsigned long long)jb.rx * jb.ry * n);
+  if (side == 0 && t == 0 && c.counters) {
+    atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)jb.rx * jb.ry * n);
+    atomicAdd(&c.counters[CNT_FIBER_ENTRIES], (unsigned long long)jb.rx * jb.ry * n);
+  }
   if (side == 0) {
     if (t >= jb.rx) return;
     ESum s = esum_zero();
@@ -271,7 +274,7 @@ __global__ void k_intersection(DevCtx c, int ibase) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int d = c.d, n = c.n;
   const int r = rec_rank(c.rec_cur, c.RS, i);
-  if (s == 0 && t == 0 && c.counters) atomicAdd(&c.counters[0], (unsigned long long)r * r);
+  if (s == 0 && t == 0 && c.counters) atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)r * r);
   if (s >= r || t >= r) return;
   const int* Ps = rec_piv(c.rec_cur, c.RS, i) + (long long)s * d;
   const int* Pt = rec_piv(c.rec_cur, c.RS, i) + (long long)t * d;
