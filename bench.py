@@ -3,10 +3,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload D5] [--impl ours|reference]
 
-A *step* is one whole solve of the workload: reset to the seed-fixed
-initial pivots, the workload's full sweeps (every half-sweep = enrichment, fiber
-evaluation, cross + maxvol, commit, over all interfaces at once; Alg. 6) and the
-TT quadrature (§4.1).  ``value`` = integrand evaluations per second (the device
+A *step* is one whole solve of the workload: reset to the seed-fixed rank-1
+start, the workload's dimension-parallel sweeps (Alg. 6: every superblock, at
+once, extends its cross to the new rows/columns -- the batched fiber evaluation -- and adds
+one pivot found by Alg. 2) and the TT quadrature (§4.1).  ``value`` = integrand evaluations per second (the device
 counter of evaluated tensor entries ÷ device time), whole job, inputs resident in HBM.
 
 N = 1: the solve is one CUDA graph replayed per step (tt_solve_launch).  N > 1 (torchrun,
@@ -120,36 +120,42 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # roofline of the dominant kernel
 # --------------------------------------------------------------------------------------
+# algorithmic fp64 flops per superblock entry: C: S = H + L*2^-52 (2), S*S (1),
+# 1/S^2 (1); D: + five double-double products (10 each), rho (4), dd * rho (8), rounding and
+# the division (2)
+FLOPS_PER_ENTRY = {0: 4, 1: 68}
+
+
 def roofline(kt, stats, family, peaks, peak_src):
-    """kt: {name: (launches, ms)} of the profiling pass; stats: its counters."""
+    """kt: {name: (launches, ms)} of the profiling pass; stats: its summed counters."""
     name = max(kt, key=lambda k: kt[k][1])
     launches, ms = kt[name]
     avg_s = ms / max(1, launches) / 1e3
     out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
-    if name == "k_fiber":
-        ent = stats["fiber_entries"] / max(1, launches)
-        # algorithmic: 8 B written per entry; family D adds ~26 fp64 flops per entry
-        # (two double-double products, rounding, one division; DESIGN.md §6)
-        gbs = ent * 8 / avg_s / 1e9
-        hbm = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-               "frac": gbs / peaks["hbm_gbs"], "units_per_launch": ent, "per_unit": "8 B/entry"}
-        if family == 1:
-            tf = ent * 26 / avg_s / 1e12
-            alu = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                   "frac": tf / FP64_PEAK_TFLOPS, "units_per_launch": ent, "per_unit": "26 fp64 flop/entry"}
-            out.update(alu if alu["frac"] > hbm["frac"] else hbm)
-        else:
-            out.update(hbm)
-    elif name == "k_cross":
-        upd = stats["cross_updates"] / max(1, launches)
-        tf = upd * 2 / avg_s / 1e12  # one mul + one sub per element update (no FMA, DESIGN.md R4)
-        out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": tf / FP64_PEAK_TFLOPS, "units_per_launch": upd, "per_unit": "2 fp64 flop/element update",
-                    "steps_per_launch": stats["cross_steps"] / max(1, launches),
-                    "us_per_step": avg_s * 1e6 / max(1e-9, stats["cross_steps"] / max(1, launches))})
+    fpe = FLOPS_PER_ENTRY[family]
+    if name in ("k_sb_extend_rows", "k_sb_extend_cols"):
+        # the two extension kernels split the entries about evenly; report their mean
+        l2 = kt["k_sb_extend_rows"][0] + kt["k_sb_extend_cols"][0]
+        ms2 = kt["k_sb_extend_rows"][1] + kt["k_sb_extend_cols"][1]
+        avg_s = ms2 / max(1, l2) / 1e3
+        ent, upd = stats["ext_entries"] / max(1, l2), stats["ext_updates"] / max(1, l2)
+        out.update({"kernel": "k_sb_extend_rows+cols", "avg_us": avg_s * 1e6, "launches": l2})
+    elif name == "k_greedy":
+        ent = (stats["sb_entries"] - stats["ext_entries"]) / max(1, launches)
+        upd = (stats["sb_updates"] - stats["ext_updates"]) / max(1, launches)
+        out["rook_steps_per_launch"] = stats["rook_steps"] / max(1, launches)
+    elif name == "k_fiber":
+        ent, upd = stats["fiber_entries"] / max(1, launches), 0
     else:
-        out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
-    out["peak_source"] = "derived fp64 (DESIGN.md §6)" if out.get("unit") == "TFLOP/s" else f"{peak_src} MEASURED_PEAKS.json"
+        out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "peak_source": None})
+        return out
+    flops = ent * fpe + 2 * upd   # one multiply + one subtract per u_t(x) v_t(y) term
+    tf = flops / avg_s / 1e12
+    out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tf / FP64_PEAK_TFLOPS, "entries_per_launch": ent, "updates_per_launch": upd,
+                "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
+                "peak_source": "derived fp64 FMA peak: 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §6)"})
     return out
 
 
@@ -159,35 +165,41 @@ def roofline(kt, stats, family, peaks, peak_src):
 def oracle_sample(wl, budget_s):
     """Run the oracle on a bounded sample of the workload; returns (evals, seconds, what).
 
-    Small workloads (every fiber of a sweep fits a few seconds): whole solves
-    (init + sweeps + quadrature), repeated while the budget lasts.  Large ones: the first
-    L->R half-sweep interface by interface (each interface = enrichment, fiber, cross,
-    maxvol), stopped when the budget is spent.
+    Small workloads (a whole solve fits a few seconds): whole solves (init + sweeps +
+    quadrature), repeated while the budget lasts.  Large ones: sweeps from the rank-1 start,
+    superblock by superblock (each = LU of the existing cross + one Alg. 2 step), stopped
+    when the budget is spent.
     """
     from threadpoolctl import threadpool_limits
     from oracle import cross as X
     u, w = wl.grid()
-    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_enrich, wl.maxvol_delta, wl.max_swaps, wl.seed)
+    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed)
+    nsw = wl.alg6_sweeps
     evals, t0 = 0, time.perf_counter()
     with threadpool_limits(1):
-        if wl.d <= 10 and wl.rank_cap <= 16:
+        if wl.d <= 5:
             solves = 0
             while True:
-                st, val, _ = X.run(prob, wl.sweeps)
+                st, val, _ = X.run(prob, nsw)
                 evals += st.n_evals
                 solves += 1
                 if time.perf_counter() - t0 > budget_s:
                     break
-            return evals, time.perf_counter() - t0, f"{solves} full solve(s) ({wl.sweeps} sweeps + quadrature)"
+            return evals, time.perf_counter() - t0, f"{solves} full solve(s) ({nsw} Alg. 6 sweeps + quadrature)"
         st = X.initial_state(prob)
         done = 0
-        for i in range(wl.d - 1):
-            _, info = X.update_interface(prob, st, i, X.DIR_LR)
-            evals += info["evals"]
-            done += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        return evals, time.perf_counter() - t0, f"{done} interface update(s) of the first L->R half-sweep"
+        while time.perf_counter() - t0 <= budget_s:
+            new = st.copy()
+            for k in range(wl.d - 1):
+                piv, par, info = X.superblock_update(prob, st, k)
+                new.piv[k], new.par[k] = piv, par
+                evals += info["evals"]
+                done += 1
+                if time.perf_counter() - t0 > budget_s:
+                    break
+            new.sweep = st.sweep + 1
+            st = new
+        return evals, time.perf_counter() - t0, f"{done} superblock update(s) from the rank-1 start"
 
 
 def run_reference(args):
@@ -218,8 +230,9 @@ def run_reference(args):
 
 def workload_config(wl, n):
     return {"workload": f"{FAMILY_NAMES[wl.family]}_{wl.d}", "d": wl.d, "n": wl.n, "L": wl.L,
-            "rank_cap": wl.rank_cap, "tol": wl.tol, "sweeps": wl.sweeps, "n_enrich": wl.n_enrich,
-            "maxvol_delta": wl.maxvol_delta, "seed": wl.seed, "parallelism": f"interfaces/{n}",
+            "rank_cap": wl.rank_cap, "tol": wl.tol, "sweeps": wl.sweeps, "alg6_sweeps": wl.alg6_sweeps,
+            "n_samples": wl.n_samples, "rook_iters": wl.rook_iters, "seed": wl.seed,
+            "parallelism": f"superblocks/{n}",
             "l2": "flushed (256 MiB memset) before every timed step"}
 
 
@@ -254,13 +267,14 @@ def main():
     torch.cuda.set_stream(stream)
     u_d = torch.from_numpy(u).to(dev)
     w_d = torch.from_numpy(w).to(dev)
-    kw = dict(n_enrich=wl.n_enrich, max_swaps=wl.max_swaps, delta=wl.maxvol_delta, seed=wl.seed)
+    kw = dict(n_samples=wl.n_samples, rook_iters=wl.rook_iters, seed=wl.seed)
+    nsw = wl.alg6_sweeps
     use_graph = world == 1 and not args.no_graph
     if world == 1:
         tt = TTCross(wl.family, u_d, w_d, wl.rank_cap, wl.tol, stream=stream.cuda_stream, **kw)
 
         def step():
-            tt.solve_launch(wl.sweeps, graph=use_graph)
+            tt.solve_launch(nsw, graph=use_graph)
 
         def result():
             return tt.integrate_read()
@@ -271,7 +285,7 @@ def main():
         last = {}
 
         def step():
-            last["v"] = dtt.solve(wl.sweeps)
+            last["v"] = dtt.solve(nsw)
 
         def result():
             return last["v"]
@@ -330,10 +344,10 @@ def main():
     for _ in range(args.steps):
         core.load_grid(u_h.numpy(), w_h.numpy())
         if world == 1:
-            tt.solve_launch(wl.sweeps, graph=use_graph)
+            tt.solve_launch(nsw, graph=use_graph)
             e2e_val = tt.integrate_read()
         else:
-            dtt.sweep(wl.sweeps)
+            dtt.sweep(nsw)
             e2e_val = dtt.integrate()
     barrier()
     e2e_s = time.perf_counter() - t0
@@ -352,10 +366,10 @@ def main():
     kt, st = {}, {}
     for _ in range(nprof):
         if world == 1:
-            tt.solve_launch(wl.sweeps, graph=False)
+            tt.solve_launch(nsw, graph=False)
             tt.integrate_read()
         else:
-            dtt.solve(wl.sweeps)
+            dtt.solve(nsw)
         for k, (nl, kms) in core.kernel_times().items():
             a, b = kt.get(k, (0, 0.0))
             kt[k] = (a + nl, b + kms)

@@ -1,32 +1,35 @@
-"""ORACLE (test infrastructure only): dimension-parallel TT cross + TT quadrature.
+"""ORACLE (test infrastructure only): dimension-parallel greedy TT cross + TT quadrature.
 
-Follows DESIGN.md §2 (the method) step by step.  Notation: modes m = 0..d-1 (paper's
-k = m+1), interfaces i = 0..d-2 separating modes <= i | > i.  The cross state is, for every
-interface i, r_i pivots; pivot slot s is a full d-tuple PIV[i][s] whose first i+1 entries
-are the left multi-index I_{<=i}[s] and whose last d-i-1 entries are the right multi-index
-I_{>i}[s] (§3.1-3.2, eq. (3)).
+Follows DESIGN.md §2 step by step.  Notation: modes m = 0..d-1 (paper's k = m+1),
+interfaces k = 0..d-2 separating modes <= k | > k.  Interface k holds r_k pivots; pivot slot
+s is a full d-tuple PIV[k][s] whose first k+1 entries are the left multi-index I_{<=k}[s]
+and whose last d-k-1 entries are the right multi-index I_{>k}[s] (§3.1-3.2,
+eq. (3)), plus its parents PAR[k][s] = (alpha, beta): the slot of its left
+part in I_{<=k-1} and of its right part in I_{>k+1} (nestedness, eq. (4)).
 
 Pieces (each cites the passage it follows):
-  splitmix64 / initial_state  -- seed-fixed random nested initial pivots (BASELINE.json
-                                 "seed-fixed random initial pivots"; nestedness eq. (4)).
-  enrich_right / enrich_left  -- random extra candidate columns of the superblock
-                                 (Alg. 2 line 1 "Pick a random set of samples", PAPER.md
-                                 lines 236-240, applied to whole superblock columns).
-  fiber                       -- A(I_{<=m-1}, i_m, I_{>m}) as an array [alpha][beta][a]
-                                 (eq. (3) factors, lines 314-320).
-  rrcross                     -- rank-revealing cross of a fiber matrix by complete
-                                 pivoting (§2.4: "complete pivoting ...
-                                 numerically stable") with truncation at tol and the
-                                 rank cap, maintaining B = A(:,J) A(I,J)^{-1}.
-  maxvol                      -- Alg. 1 (lines 205-218) iterated: swap while
-                                 max|B| > 1 + delta, with the rank-1 update of B from
-                                 the paper's maxvol reference [gostz-maxvol-2010].
-  half_sweep                  -- Alg. 3 directions with the dimension-parallel
-                                 relaxation of §3.4 (lines 599-604): every interface is
-                                 updated from the index sets of the previous half-sweep.
-  integrate                   -- §4.1 "product of (2d-1) matrices" (lines 689-693).
+  splitmix64 / initial_state -- the first pivot: first argmax |A| over seeded random
+                                multi-indices (Alg. 2 line 1 "random set of samples",
+                                PAPER.md line 236), rank 1 on every interface.
+  superblock_update          -- one step of Alg. 6 (lines 624-641) for superblock k:
+                                Alg. 2 (lines 231-253) -- random samples, then rook
+                                (column/row partial pivoting) on the error A - A~ of the
+                                superblock A(I_{<=k-1} i_k, i_{k+1} I_{>k+1}); the new pivot
+                                is appended (Alg. 6 line 4), never swapped, so nestedness is
+                                kept (Remark, lines 509-512).
+  sweep                      -- Alg. 6 over all superblocks, each reading the index sets of
+                                the previous sweep (§3.4 relaxation, lines 599-604).
+  integrate                  -- §4.1 "product of (2d-1) matrices" (lines 689-693).
 
-All argmax decisions take the FIRST maximiser in row-major order (numpy semantics).
+One sweep adds at most one pivot per superblock (Alg. 6 with Alg. 2 applied once); the
+workloads run as many sweeps as the rank cap needs (R7).
+
+The cross approximation of a superblock is kept in the incomplete-LU ("ACA") form of the
+interpolation formula eq. (1): A~(x, y) = sum_t u_t(x) v_t(y) with
+u_t = E_{t-1}(:, y_t), v_t = E_{t-1}(x_t, :) / E_{t-1}(x_t, y_t), which equals
+A(:, J) A(I, J)^{-1} A(I, :) (the Schur-complement identity; pinned in the tests).  All sums
+over t run t = 0, 1, ... with a separate multiply and subtract (no fused multiply-add);
+every argmax takes the FIRST maximiser (numpy semantics).  DESIGN.md R4.
 """
 from __future__ import annotations
 
@@ -39,10 +42,8 @@ from .integrand import entries, prefactor
 
 M64 = (1 << 64) - 1
 GOLDEN = 0x9E3779B97F4A7C15
-TAG_INIT_LEFT = 0
-TAG_INIT_RIGHT = 1
-DIR_LR = 0
-DIR_RL = 1
+TAG_INIT = 0
+N_INIT = 64
 
 
 def splitmix64(seed: int, ctr: int) -> int:
@@ -57,20 +58,8 @@ def draw_ctr(tag: int, d: int, i: int, s: int) -> int:
     return ((tag * (d + 1) + i) << 20) + s
 
 
-def enrich_tag(sweep: int, direction: int) -> int:
-    return 2 + 2 * sweep + direction
-
-
-def partial_fisher_yates(seed, tag, d, i, M, r):
-    """First r entries of a seeded Fisher-Yates shuffle of range(M) (sparse perm)."""
-    perm = {}
-    out = []
-    for s in range(r):
-        j = s + splitmix64(seed, draw_ctr(tag, d, i, s)) % (M - s)
-        vs, vj = perm.get(s, s), perm.get(j, j)
-        perm[s], perm[j] = vj, vs
-        out.append(vj)
-    return out
+def sample_tag(sweep: int) -> int:
+    return 1 + sweep
 
 
 @dataclass
@@ -80,9 +69,8 @@ class Problem:
     w: np.ndarray          # (d, n) quadrature weights
     rank_cap: int
     tol: float
-    n_enrich: int = 4
-    delta: float = 1e-2
-    max_swaps: int = 0     # 0 -> 2*rank_cap
+    n_samples: int = 32    # |L| of Alg. 2 line 1
+    rook_iters: int = 4    # column+row rounds of the rook search (Alg. 2 lines 2-5)
     seed: int = 0
 
     @property
@@ -93,16 +81,14 @@ class Problem:
     def n(self):
         return self.u.shape[1]
 
-    def swaps_cap(self):
-        return self.max_swaps if self.max_swaps > 0 else 2 * self.rank_cap
-
     def A(self, idx):
         return entries(self.family, self.u, idx)
 
 
 @dataclass
 class State:
-    piv: list            # piv[i] : int64 array (r_i, d)
+    piv: list            # piv[k] : int64 array (r_k, d)   full d-tuples
+    par: list            # par[k] : int64 array (r_k, 2)   (alpha, beta) parent slots
     sweep: int = 0
     n_evals: int = 0
     log: list = field(default_factory=list)
@@ -112,52 +98,25 @@ class State:
         return [len(p) for p in self.piv]
 
     def copy(self):
-        return State([p.copy() for p in self.piv], self.sweep, self.n_evals, list(self.log))
-
-
-def initial_ranks(d, n, cap):
-    """r_i = min(cap, n^(i+1), n^(d-1-i)) (a rank can exceed neither unfolding side)."""
-    out = []
-    for i in range(d - 1):
-        out.append(int(min(cap, n ** min(i + 1, 64), n ** min(d - 1 - i, 64))))
-    return out
+        return State([p.copy() for p in self.piv], [q.copy() for q in self.par], self.sweep, self.n_evals,
+                     list(self.log))
 
 
 def initial_state(prob: Problem) -> State:
-    """Seed-fixed random nested pivots (nestedness eq. (4)).
-
-    Left parts: I_{<=i} = r_i distinct draws from I_{<=i-1} x {0..n-1}, candidate
-    c = alpha*n + a -> (I_{<=i-1}[alpha], a).  Right parts: I_{>i} = r_i distinct draws
-    from {0..n-1} x I_{>i+1}, candidate c = beta*n + a -> (a, I_{>i+1}[beta]).
-    Slot s pairs the s-th left draw with the s-th right draw.
-    """
+    """Rank-1 nested start: t0 = first argmax |A| over N_INIT seeded random multi-indices
+    (coordinate j of sample q drawn with counter draw_ctr(TAG_INIT, d, 0, q*d + j))."""
     d, n = prob.d, prob.n
-    r = initial_ranks(d, n, prob.rank_cap)
-    left = []
-    for i in range(d - 1):
-        prev = r[i - 1] if i > 0 else 1
-        sel = partial_fisher_yates(prob.seed, TAG_INIT_LEFT, d, i, prev * n, r[i])
-        rows = []
-        for c in sel:
-            alpha, a = divmod(c, n)
-            rows.append((list(left[i - 1][alpha]) if i > 0 else []) + [a])
-        left.append(rows)
-    right = [None] * (d - 1)
-    for i in range(d - 2, -1, -1):
-        nxt = r[i + 1] if i < d - 2 else 1
-        sel = partial_fisher_yates(prob.seed, TAG_INIT_RIGHT, d, i, nxt * n, r[i])
-        rows = []
-        for c in sel:
-            beta, a = divmod(c, n)
-            rows.append([a] + (list(right[i + 1][beta]) if i < d - 2 else []))
-        right[i] = rows
-    piv = [np.array([left[i][s] + right[i][s] for s in range(r[i])], dtype=np.int64)
-           for i in range(d - 1)]
-    return State(piv)
+    cand = np.array([[splitmix64(prob.seed, draw_ctr(TAG_INIT, d, 0, q * d + j)) % n for j in range(d)]
+                     for q in range(N_INIT)], dtype=np.int64)
+    vals = prob.A(cand)
+    t0 = cand[int(np.argmax(np.abs(vals)))]
+    st = State([t0[None, :].copy() for _ in range(d - 1)], [np.zeros((1, 2), np.int64) for _ in range(d - 1)])
+    st.n_evals = N_INIT
+    return st
 
 
 # --------------------------------------------------------------------------------------
-# fibers
+# fibers (TT factors of eq. (3) and the quadrature)
 # --------------------------------------------------------------------------------------
 def fiber(prob: Problem, left_tuples, m, right_tuples):
     """F[alpha][beta][a] = A(left_tuples[alpha][0:m], a, right_tuples[beta][m+1:d]).
@@ -176,192 +135,160 @@ def fiber(prob: Problem, left_tuples, m, right_tuples):
     return prob.A(idx)
 
 
-def fiber_matrix(F, direction):
-    """Row-major matrix view of a fiber for the given half-sweep direction.
-
-    L->R: rows (alpha, a) -> alpha*n + a, columns beta.
-    R->L: rows (beta, a)  -> beta*n + a,  columns alpha.
-    """
-    rx, ry, n = F.shape
-    if direction == DIR_LR:
-        return F.transpose(0, 2, 1).reshape(rx * n, ry)
-    return F.transpose(1, 2, 0).reshape(ry * n, rx)
-
-
 # --------------------------------------------------------------------------------------
-# rank-revealing cross (complete pivoting) + maxvol
+# one superblock of Alg. 6 (Alg. 2 repeated n_add times)
 # --------------------------------------------------------------------------------------
-def rrcross(F, tol, cap):
-    """Complete-pivoting cross of the m x c matrix F with truncation.
+class Superblock:
+    """A(I_{<=k-1} i_k, i_{k+1} I_{>k+1}) as an R x C matrix, R = r_{k-1} n, C = n r_{k+1};
+    row x = alpha*n + a, column y = beta*n + b (Alg. 3-5 superblock, line 406)."""
 
-    Step: (i, col) = first argmax of |R| (pivoted rows/columns are exactly zero);
-    stop if not |R[i,col]| > tol * max|F| or cap pivots were taken.
-    Updates (all elementwise, no fused multiply-add):
-        b      = R[:, col] / piv
-        B      = B - outer(b, B[i, :]),   then append b as the new column
-        R      = R - outer(R[:, col], R[i, :] / piv),  R[i,:] = 0, R[:,col] = 0
-    Returns (I, J, B) with B = F[:, J] F[I, J]^{-1} (slot order = pivot order).
-    An all-zero F returns empty I, J.
+    def __init__(self, prob, st, k):
+        self.prob, self.k = prob, k
+        d, n = prob.d, prob.n
+        self.L = st.piv[k - 1] if k > 0 else np.zeros((1, d), np.int64)
+        self.Rt = st.piv[k + 1] if k < d - 2 else np.zeros((1, d), np.int64)
+        self.R = len(self.L) * n
+        self.C = len(self.Rt) * n
+        self.evals = 0
+
+    def tuples(self, xs, ys):
+        k, n, d = self.k, self.prob.n, self.prob.d
+        xs = np.asarray(xs, np.int64)
+        ys = np.asarray(ys, np.int64)
+        idx = np.empty(xs.shape + (d,), np.int64)
+        idx[..., :k] = self.L[xs // n][..., :k]
+        idx[..., k] = xs % n
+        idx[..., k + 1] = ys % n
+        idx[..., k + 2:] = self.Rt[ys // n][..., k + 2:]
+        return idx
+
+    def A(self, xs, ys):
+        xs, ys = np.broadcast_arrays(np.asarray(xs, np.int64), np.asarray(ys, np.int64))
+        self.evals += xs.size
+        return self.prob.A(self.tuples(xs, ys))
+
+
+def _approx_sub(vals, U_rows, V_cols):
+    """vals - sum_t U_rows[..., t] * V_cols[..., t], t ascending, mul then sub."""
+    out = np.array(vals, dtype=np.float64, copy=True)
+    for t in range(U_rows.shape[-1]):
+        out = out - U_rows[..., t] * V_cols[..., t]
+    return out
+
+
+def superblock_update(prob: Problem, st: State, k: int):
+    """New pivots of interface k from the state of the previous sweep (Alg. 6 line 3).
+
+    Returns (new_piv (r', d), new_par (r', 2), info) with the old pivots first.
     """
-    F = np.asarray(F, dtype=np.float64)
-    m, c = F.shape
-    R = F.copy()
-    scale = float(np.max(np.abs(F))) if F.size else 0.0
-    B = np.zeros((m, 0))
-    I, J = [], []
-    for _ in range(min(cap, m, c)):
-        flat = int(np.argmax(np.abs(R)))
-        i, col = divmod(flat, c)
-        piv = R[i, col]
-        if not abs(piv) > tol * scale:
+    d, n = prob.d, prob.n
+    sb = Superblock(prob, st, k)
+    R, C = sb.R, sb.C
+    P = st.piv[k]
+    xs = list(st.par[k][:, 0] * n + P[:, k])
+    ys = list(st.par[k][:, 1] * n + P[:, k + 1])
+    allx, ally = np.arange(R), np.arange(C)
+    U = np.zeros((R, 0))
+    V = np.zeros((0, C))
+
+    def col(y, mask):   # (A(:, y), E(:, y)) with E zeroed on the rows in `mask`
+        raw = sb.A(allx, y)
+        e = _approx_sub(raw, U, np.broadcast_to(V[:, y], (R, V.shape[0])))
+        e[mask] = 0.0
+        return raw, e
+
+    def row(x, mask):   # (A(x, :), E(x, :)) with E zeroed on the columns in `mask`
+        raw = sb.A(x, ally)
+        e = _approx_sub(raw, np.broadcast_to(U[x, :], (C, U.shape[1])), V.T)
+        e[mask] = 0.0
+        return raw, e
+
+    # incomplete LU of the existing cross in slot order (the "LU-pivoted init"): it rebuilds
+    # u_s, v_s on the grown superblock exactly as they were when pivot s was added
+    scale = 0.0
+    for s in range(len(P)):
+        raw, c = col(ys[s], xs[:s])
+        _, g = row(xs[s], ys[:s])
+        if c[xs[s]] == 0.0:
+            # singular existing cross: only possible for a zero first pivot, i.e. every
+            # seeded sample of A was zero (e.g. D_d with d > n); DESIGN.md R8
+            info = {"added": 0, "rook_steps": 0, "stop": "singular", "adds": [], "evals": sb.evals,
+                    "search_evals": 0, "rank": len(P)}
+            return P.copy(), st.par[k].copy(), info
+        U = np.concatenate([U, c[:, None]], axis=1)
+        V = np.concatenate([V, (g / c[xs[s]])[None, :]], axis=0)
+        scale = max(scale, abs(float(raw[xs[s]])))
+    new_t, new_p = [], []
+    lu_evals = sb.evals
+    info = {"added": 0, "rook_steps": 0, "stop": "added", "adds": [], "lu_evals": lu_evals}
+    while True:   # one Alg. 2 step (a loop only so that the stop conditions can `break`)
+        if len(xs) >= prob.rank_cap:
+            info["stop"] = "cap"
             break
-        b = R[:, col] / piv
-        if B.shape[1]:
-            B = B - np.multiply.outer(b, B[i, :])
-        B = np.concatenate([B, b[:, None]], axis=1)
-        R = R - np.multiply.outer(R[:, col], R[i, :] / piv)
-        R[i, :] = 0.0
-        R[:, col] = 0.0
-        I.append(i)
-        J.append(col)
-    return I, J, B
-
-
-def maxvol(B, I, delta, max_swaps):
-    """Alg. 1 iterated on B = A(:,J) A(I,J)^{-1}.
-
-    (i, j) = first argmax |B|; stop unless |B[i,j]| > 1 + delta; otherwise I[j] <- i and
-        g = (B[i, :] - e_j) / B[i, j];   B = B - outer(B[:, j], g).
-    Returns (I, B, n_swaps).
-    """
-    I = list(I)
-    B = B.copy()
-    r = B.shape[1]
-    nsw = 0
-    while nsw < max_swaps and r > 0:
-        flat = int(np.argmax(np.abs(B)))
-        i, j = divmod(flat, r)
-        piv = B[i, j]
-        if not abs(piv) > 1.0 + delta:
+        # Alg. 2 line 1: random samples, pick the largest error (pivot rows/columns excluded)
+        tag = sample_tag(st.sweep)
+        sx = np.array([splitmix64(prob.seed, draw_ctr(tag, d, k, 2 * q)) % R
+                       for q in range(prob.n_samples)], np.int64)
+        sy = np.array([splitmix64(prob.seed, draw_ctr(tag, d, k, 2 * q + 1)) % C
+                       for q in range(prob.n_samples)], np.int64)
+        e = _approx_sub(sb.A(sx, sy), U[sx, :], V[:, sy].T)
+        e[np.isin(sx, xs) | np.isin(sy, ys)] = 0.0
+        q = int(np.argmax(np.abs(e)))
+        xst, yst = int(sx[q]), int(sy[q])
+        # Alg. 2 lines 2-5: rook search -- column partial pivoting, then row partial pivoting,
+        # until the row step keeps the column (rook condition eq. (2)) or the budget is spent
+        c_at = g_at = -1
+        for it in range(prob.rook_iters):
+            raw_c, c = col(yst, xs)
+            c_at = yst
+            xn = int(np.argmax(np.abs(c)))
+            _, g = row(xn, ys)
+            g_at = xn
+            yn = int(np.argmax(np.abs(g)))
+            info["rook_steps"] += 1
+            conv = yn == yst
+            xst, yst = xn, yn
+            if conv:
+                break
+        if c_at != yst:
+            raw_c, c = col(yst, xs)
+        if g_at != xst:
+            _, g = row(xst, ys)
+        pv = g[yst]
+        if not abs(pv) > prob.tol * scale:
+            info["stop"] = "tol"
             break
-        e = B[i, :].copy()
-        e[j] = e[j] - 1.0
-        g = e / piv
-        B = B - np.multiply.outer(B[:, j], g)
-        I[j] = i
-        nsw += 1
-    return I, B, nsw
+        xs.append(xst)
+        ys.append(yst)
+        new_t.append(sb.tuples(np.array([xst]), np.array([yst]))[0])
+        new_p.append((xst // n, yst // n))
+        info["added"] += 1
+        info["adds"].append({"x": xst, "y": yst, "pivot": float(pv), "converged": bool(c_at == yst and g_at == xst),
+                             "xs_before": list(xs[:-1]), "ys_before": list(ys[:-1])})
+        break
+    info["evals"] = sb.evals
+    info["search_evals"] = sb.evals - lu_evals   # samples + rook columns/rows (Alg. 2)
+    info["rank"] = len(xs)
+    piv = np.concatenate([P, np.array(new_t, np.int64).reshape(-1, d)], axis=0)
+    par = np.concatenate([st.par[k], np.array(new_p, np.int64).reshape(-1, 2)], axis=0)
+    return piv, par, info
 
 
-# --------------------------------------------------------------------------------------
-# enrichment (random superblock columns)
-# --------------------------------------------------------------------------------------
-def enrich_right(prob, state, i, sweep):
-    """Extended column set of interface i for L->R: existing right parts plus n_enrich
-    random (a, I_{>i+1}[beta]) candidates, duplicates (vs everything so far) skipped."""
-    d, n = prob.d, prob.n
-    ext = [row.copy() for row in state.piv[i]]
-    nxt = len(state.piv[i + 1]) if i < d - 2 else 1
-    M = nxt * n
-    for jdraw in range(prob.n_enrich):
-        c = splitmix64(prob.seed, draw_ctr(enrich_tag(sweep, DIR_LR), d, i, jdraw)) % M
-        beta, a = divmod(c, n)
-        t = np.zeros(d, np.int64)
-        t[:i + 1] = -1
-        t[i + 1] = a
-        if i < d - 2:
-            t[i + 2:] = state.piv[i + 1][beta][i + 2:]
-        if any(np.array_equal(t[i + 1:], e[i + 1:]) for e in ext):
-            continue
-        ext.append(t)
-    return np.array(ext, dtype=np.int64)
-
-
-def enrich_left(prob, state, i, sweep):
-    """Extended column set of interface i for R->L: existing left parts plus n_enrich
-    random (I_{<=i-1}[alpha], a) candidates, duplicates skipped."""
-    d, n = prob.d, prob.n
-    ext = [row.copy() for row in state.piv[i]]
-    prv = len(state.piv[i - 1]) if i > 0 else 1
-    M = prv * n
-    for jdraw in range(prob.n_enrich):
-        c = splitmix64(prob.seed, draw_ctr(enrich_tag(sweep, DIR_RL), d, i, jdraw)) % M
-        alpha, a = divmod(c, n)
-        t = np.zeros(d, np.int64)
-        t[i + 1:] = -1
-        if i > 0:
-            t[:i] = state.piv[i - 1][alpha][:i]
-        t[i] = a
-        if any(np.array_equal(t[:i + 1], e[:i + 1]) for e in ext):
-            continue
-        ext.append(t)
-    return np.array(ext, dtype=np.int64)
-
-
-# --------------------------------------------------------------------------------------
-# half-sweeps (dimension parallel) and full sweeps
-# --------------------------------------------------------------------------------------
-def update_interface(prob, state, i, direction):
-    """New pivots of interface i from the state of the previous half-sweep.
-
-    Returns (new_piv_i or None if the fiber is identically zero, info dict).
-    """
-    d, n = prob.d, prob.n
-    if direction == DIR_LR:
-        m = i
-        X = state.piv[i - 1] if i > 0 else None
-        Y = enrich_right(prob, state, i, state.sweep)
-    else:
-        m = i + 1
-        X = enrich_left(prob, state, i, state.sweep)
-        Y = state.piv[i + 1] if i + 1 < d - 1 else None
-    F = fiber(prob, X, m, Y)
-    Fm = fiber_matrix(F, direction)
-    I, J, B = rrcross(Fm, prob.tol, prob.rank_cap)
-    info = {"evals": F.size, "rank": len(I), "swaps": 0, "cols": Fm.shape[1], "rows": Fm.shape[0]}
-    if not I:
-        return None, info
-    I, B, nsw = maxvol(B, I, prob.delta, prob.swaps_cap())
-    info["swaps"] = nsw
-    new = np.empty((len(I), d), dtype=np.int64)
-    for s, (row, col) in enumerate(zip(I, J)):
-        outer, a = divmod(row, n)
-        x, y = (outer, col) if direction == DIR_LR else (col, outer)
-        if m > 0:
-            new[s, :m] = X[x][:m]
-        new[s, m] = a
-        if m < d - 1:
-            new[s, m + 1:] = Y[y][m + 1:]
-    return new, info
-
-
-def half_sweep(prob, state, direction, interfaces=None):
-    """One dimension-parallel half-sweep (Alg. 6 lines 2-5 with the §3.4 relaxation).
-
-    Every interface in ``interfaces`` (default: all) is updated from ``state`` (the sets
-    of the previous half-sweep); returns the new state (interfaces not listed, or whose
-    fiber is identically zero, keep their pivots).
-    """
+def sweep(prob: Problem, st: State, interfaces=None) -> State:
+    """One dimension-parallel sweep (Alg. 6): every superblock in ``interfaces`` (default:
+    all) is updated from ``st``; returns the new state."""
     d = prob.d
     interfaces = range(d - 1) if interfaces is None else interfaces
-    new = state.copy()
+    new = st.copy()
     infos = {}
-    for i in interfaces:
-        piv, info = update_interface(prob, state, i, direction)
-        if piv is not None:
-            new.piv[i] = piv
+    for k in interfaces:
+        piv, par, info = superblock_update(prob, st, k)
+        new.piv[k], new.par[k] = piv, par
         new.n_evals += info["evals"]
-        infos[i] = info
-    new.log.append((state.sweep, direction, infos))
+        infos[k] = info
+    new.log.append((st.sweep, infos))
+    new.sweep = st.sweep + 1
     return new
-
-
-def sweep(prob, state):
-    """One full sweep = L->R half-sweep then R->L half-sweep."""
-    s = half_sweep(prob, state, DIR_LR)
-    s = half_sweep(prob, s, DIR_RL)
-    s.sweep = state.sweep + 1
-    return s
 
 
 # --------------------------------------------------------------------------------------
@@ -472,7 +399,7 @@ def integrate_exact(prob, state, fibers=None, dps=50):
 
 
 def run(prob, n_sweeps, state=None):
-    """Init (if no state), n_sweeps full sweeps, then the quadrature."""
+    """Init (if no state), n_sweeps sweeps, then the quadrature."""
     st = initial_state(prob) if state is None else state
     for _ in range(n_sweeps):
         st = sweep(prob, st)

@@ -17,39 +17,35 @@ LIB_PATH = os.path.join(HERE, "libttcross.so")
 TTC_OK = 0
 TTC_FAMILY_C = 0
 TTC_FAMILY_D = 1
-TTC_DIR_LR = 0
-TTC_DIR_RL = 1
 TTC_MEM_HOST = 0
 TTC_MEM_DEVICE = 1
 
 # every symbol declared in include/ttcross.h (checked by tests/test_abi.py)
 EXPORTS = [
-    "tt_cross_init", "tt_cross_reset", "tt_cross_sweep", "tt_cross_half_sweep",
-    "tt_cross_commit", "tt_cross_exchange_buffer", "tt_integrate", "tt_integrate_local",
-    "tt_integrate_partials_buffer", "tt_integrate_finish", "tt_cross_get_state",
-    "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_set_timing", "tt_cross_destroy",
-    "tt_last_error", "tt_build_info", "tt_cross_load_grid", "tt_solve_launch",
-    "tt_integrate_launch", "tt_integrate_read", "tt_cross_get_kernel_time",
+    "tt_cross_init", "tt_cross_load_grid", "tt_cross_reset", "tt_cross_sweep", "tt_cross_sweep_local",
+    "tt_cross_commit", "tt_cross_exchange_buffer", "tt_solve_launch", "tt_integrate", "tt_integrate_launch",
+    "tt_integrate_read", "tt_integrate_local", "tt_integrate_partials_buffer", "tt_integrate_finish",
+    "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
+    "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info",
 ]
-N_KERNELS = 13
+N_KERNELS = 17
 
 
 class TtcConfig(ctypes.Structure):
     _fields_ = [
         ("family", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int32),
-        ("rank_cap", ctypes.c_int32), ("n_enrich", ctypes.c_int32), ("max_swaps", ctypes.c_int32),
-        ("tol", ctypes.c_double), ("delta", ctypes.c_double), ("seed", ctypes.c_uint64),
-        ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("rank_cap", ctypes.c_int32), ("n_samples", ctypes.c_int32), ("rook_iters", ctypes.c_int32),
+        ("tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
     ]
 
 
 class TtcStats(ctypes.Structure):
     _fields_ = [
-        ("evals", ctypes.c_int64), ("launches", ctypes.c_int64), ("sweeps", ctypes.c_int32),
-        ("half_sweeps", ctypes.c_int32), ("ms_fiber", ctypes.c_double), ("ms_cross", ctypes.c_double),
-        ("ms_quad", ctypes.c_double), ("ms_other", ctypes.c_double), ("fiber_launches", ctypes.c_int64),
-        ("cross_launches", ctypes.c_int64), ("fiber_entries", ctypes.c_int64),
-        ("cross_updates", ctypes.c_int64), ("cross_steps", ctypes.c_int64), ("cross_elems", ctypes.c_int64),
+        ("evals", ctypes.c_int64), ("launches", ctypes.c_int64), ("sweeps", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("ms_fiber", ctypes.c_double), ("ms_cross", ctypes.c_double), ("ms_quad", ctypes.c_double),
+        ("ms_other", ctypes.c_double), ("fiber_entries", ctypes.c_int64), ("sb_entries", ctypes.c_int64),
+        ("sb_updates", ctypes.c_int64), ("rook_steps", ctypes.c_int64), ("ext_entries", ctypes.c_int64),
+        ("ext_updates", ctypes.c_int64),
     ]
 
 
@@ -70,14 +66,14 @@ def load(path: str = LIB_PATH):
         "tt_cross_init": (i32, [ctypes.POINTER(P), ctypes.POINTER(TtcConfig), P, P, i32, P]),
         "tt_cross_reset": (i32, [P]),
         "tt_cross_sweep": (i32, [P, i32]),
-        "tt_cross_half_sweep": (i32, [P, i32]),
+        "tt_cross_sweep_local": (i32, [P]),
         "tt_cross_commit": (i32, [P]),
         "tt_cross_exchange_buffer": (i32, [P, ctypes.POINTER(P), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tt_integrate": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
         "tt_integrate_local": (i32, [P]),
         "tt_integrate_partials_buffer": (i32, [P, ctypes.POINTER(P), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "tt_integrate_finish": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
-        "tt_cross_get_state": (i32, [P, P, P]),
+        "tt_cross_get_state": (i32, [P, P, P, P]),
         "tt_cross_get_fiber": (i32, [P, i32, P, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "tt_cross_get_stats": (i32, [P, ctypes.POINTER(TtcStats)]),
         "tt_cross_set_timing": (i32, [P, i32]),
@@ -133,13 +129,13 @@ class DeviceView:
 class TTCross:
     """Handle on one TT-cross problem (C-ABI context)."""
 
-    def __init__(self, family, u, w, rank_cap, tol, n_enrich=4, max_swaps=0, delta=1e-2,
-                 seed=0, rank=0, world=1, stream=None):
+    def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, rank=0, world=1,
+                 stream=None):
         self.lib = load()
         self.d, self.n = int(u.shape[0]), int(u.shape[1])
         self.cap = int(rank_cap)
-        self.cfg = TtcConfig(int(family), self.d, self.n, self.cap, int(n_enrich), int(max_swaps),
-                             float(tol), float(delta), int(seed) & ((1 << 64) - 1), int(rank), int(world))
+        self.cfg = TtcConfig(int(family), self.d, self.n, self.cap, int(n_samples), int(rook_iters), float(tol),
+                             int(seed) & ((1 << 64) - 1), int(rank), int(world))
         pu, ku, keep_u = _ptr_and_kind(u)
         pw, kw, keep_w = _ptr_and_kind(w)
         if ku != kw:
@@ -171,8 +167,8 @@ class TTCross:
     def sweep(self, n_sweeps=1):
         _check(self.lib, self.lib.tt_cross_sweep(self._h, int(n_sweeps)), "tt_cross_sweep")
 
-    def half_sweep(self, direction):
-        _check(self.lib, self.lib.tt_cross_half_sweep(self._h, int(direction)), "tt_cross_half_sweep")
+    def sweep_local(self):
+        _check(self.lib, self.lib.tt_cross_sweep_local(self._h), "tt_cross_sweep_local")
 
     def commit(self):
         _check(self.lib, self.lib.tt_cross_commit(self._h), "tt_cross_commit")
@@ -225,12 +221,18 @@ class TTCross:
         return DeviceView(p.value, tot.value, "<f8"), per.value
 
     # -- inspection
-    def state(self):
+    def state(self, parents=False):
+        """(ranks, [PIV[k] (r_k, d)]) and, with parents=True, also [PAR[k] (r_k, 2)]."""
         ranks = np.zeros(self.d - 1, dtype=np.int32)
         piv = np.zeros((self.d - 1, self.cap, self.d), dtype=np.int32)
+        par = np.zeros((self.d - 1, self.cap, 2), dtype=np.int32)
         _check(self.lib, self.lib.tt_cross_get_state(self._h, ranks.ctypes.data_as(ctypes.c_void_p),
-                                                     piv.ctypes.data_as(ctypes.c_void_p)), "tt_cross_get_state")
-        return ranks, [piv[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
+                                                     piv.ctypes.data_as(ctypes.c_void_p),
+                                                     par.ctypes.data_as(ctypes.c_void_p)), "tt_cross_get_state")
+        P = [piv[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
+        if parents:
+            return ranks, P, [par[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
+        return ranks, P
 
     def fiber(self, mode):
         rx, ry = ctypes.c_int32(), ctypes.c_int32()
@@ -245,7 +247,7 @@ class TTCross:
     def stats(self):
         s = TtcStats()
         _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
-        return {f: getattr(s, f) for f, _ in TtcStats._fields_}
+        return {f: getattr(s, f) for f, _ in TtcStats._fields_ if f != "pad"}
 
 
     def kernel_times(self):

@@ -7,12 +7,11 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 #include "../../include/ttcross.h"
 #include "ttc_common.cuh"
-#include "ttc_cross.cuh"
+#include "ttc_greedy.cuh"
 #include "ttc_kernels.cuh"
 
 using namespace ttc;
@@ -37,14 +36,17 @@ enum KClass { KC_FIBER = 0, KC_CROSS = 1, KC_QUAD = 2, KC_OTHER = 3 };
 
 // per-kernel identifiers for tt_cross_get_kernel_time (class = accounting bucket of ttc_stats)
 enum KId {
-  K_PREP = 0, K_ENRICH, K_FROZEN_SIDES, K_FROZEN_Q, K_FROZEN_LR, K_FIBER, K_CROSS, K_COMMIT,
-  K_WSUM, K_INTERSECTION, K_SOLVE, K_CHAIN, K_FINISH, K_COUNT
+  K_PREP = 0, K_INIT_PIVOT, K_INIT_RECORDS, K_SB_SIDES, K_SB_CX, K_SB_EXT_ROWS, K_SB_EXT_COLS, K_GREEDY,
+  K_FROZEN_SIDES, K_FROZEN_Q, K_FROZEN_LR, K_FIBER, K_WSUM, K_INTERSECTION, K_SOLVE, K_CHAIN, K_FINISH,
+  K_COUNT
 };
 const char* const kKernelName[K_COUNT] = {
-    "k_prep_nodes", "k_enrich", "k_frozen_sides", "k_frozen_q", "k_frozen_lr", "k_fiber", "k_cross",
-    "k_commit", "k_wsum", "k_intersection", "k_solve", "k_chain", "k_finish"};
-const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_FIBER, KC_FIBER, KC_FIBER, KC_FIBER, KC_CROSS,
-                                   KC_OTHER, KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD};
+    "k_prep_nodes",   "k_init_pivot", "k_init_records", "k_sb_sides",     "k_sb_cx",  "k_sb_extend_rows",
+    "k_sb_extend_cols", "k_greedy",   "k_frozen_sides", "k_frozen_q",     "k_frozen_lr", "k_fiber",
+    "k_wsum",         "k_intersection", "k_solve",      "k_chain",        "k_finish"};
+const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_OTHER, KC_FIBER, KC_FIBER, KC_FIBER,
+                                   KC_FIBER, KC_CROSS, KC_FIBER, KC_FIBER, KC_FIBER, KC_FIBER,
+                                   KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD};
 
 struct EvRec {
   cudaEvent_t a, b;
@@ -56,23 +58,19 @@ struct EvRec {
 struct ttc_ctx {
   ttc_config cfg{};
   cudaStream_t stream = nullptr;
-  cudaStream_t ls = nullptr;        // launch stream: `stream`, or the capture stream while a graph is built
-  cudaStream_t cap_stream = nullptr; // private stream used to capture the solve graph
+  cudaStream_t ls = nullptr;          // launch stream: `stream`, or the capture stream while a graph is built
+  cudaStream_t cap_stream = nullptr;  // private stream used to capture the solve graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int graph_sweeps = -1;
   long long graph_launches = 0;
   DevCtx dc{};
-  int chunk = 0, kb = 0, ke = 0, n_owned = 0, slots = 0;
-  int sweeps = 0, half_sweeps = 0;
-  int pending = 0;  // a half-sweep waits for commit
-  // cross kernel launch shape
-  int G = 1, rpc = 0;
-  bool smem_mode = true;
-  size_t cross_smem = 0;
+  int chunk = 0, kb = 0, ke = 0, n_owned = 0, slots = 0, nrec = 0;
+  int sweeps = 0;
+  int pending = 0;  // a local sweep waits for commit
+  int* t0buf = nullptr;
   // buffers
   std::vector<void*> allocs;
-  int* rec_init = nullptr;
   long long rec_ints = 0;
   double* partials = nullptr;  // [world][3 + 2*cap*cap] (see k_chain)
   double* out_dev = nullptr;   // [4]
@@ -140,160 +138,99 @@ int check_launch(const char* what) {
   return TTC_OK;
 }
 
-// ------------------------------------------------------------------ host initial pivots
-// Mirrors oracle/cross.py::initial_state (seed-fixed nested random pivots, R5).
-std::vector<long long> partial_fisher_yates(uint64_t seed, int tag, int d, int i, long long M, int r) {
-  std::unordered_map<long long, long long> perm;
-  std::vector<long long> out;
-  auto get = [&](long long k) {
-    auto it = perm.find(k);
-    return it == perm.end() ? k : it->second;
-  };
-  for (int s = 0; s < r; ++s) {
-    long long j = s + (long long)(splitmix64(seed, draw_ctr((uint64_t)tag, d, i, s)) % (uint64_t)(M - s));
-    long long vs = get(s), vj = get(j);
-    perm[s] = vj;
-    perm[j] = vs;
-    out.push_back(vj);
-  }
-  return out;
-}
-
-long long ipow_cap(long long n, int e, long long cap) {
-  long long v = 1;
-  for (int k = 0; k < e; ++k) {
-    v *= n;
-    if (v >= cap) return cap;
-  }
-  return v;
-}
-
-void initial_records(const ttc_config& cfg, int RS, long long nrec, std::vector<int32_t>& rec) {
-  const int d = cfg.d, n = cfg.n, cap = cfg.rank_cap;
-  rec.assign(nrec * RS, -1);
-  std::vector<int> r(d - 1);
-  for (int i = 0; i < d - 1; ++i)
-    r[i] = (int)std::min<long long>(cap, std::min(ipow_cap(n, i + 1, cap), ipow_cap(n, d - 1 - i, cap)));
-  std::vector<std::vector<std::vector<int>>> left(d - 1), right(d - 1);
-  for (int i = 0; i < d - 1; ++i) {
-    long long prev = i > 0 ? r[i - 1] : 1;
-    auto sel = partial_fisher_yates(cfg.seed, 0, d, i, prev * n, r[i]);
-    for (long long cnd : sel) {
-      long long alpha = cnd / n, a = cnd % n;
-      std::vector<int> t;
-      if (i > 0) t = left[i - 1][alpha];
-      t.push_back((int)a);
-      left[i].push_back(t);
-    }
-  }
-  for (int i = d - 2; i >= 0; --i) {
-    long long nxt = i < d - 2 ? r[i + 1] : 1;
-    auto sel = partial_fisher_yates(cfg.seed, 1, d, i, nxt * n, r[i]);
-    for (long long cnd : sel) {
-      long long beta = cnd / n, a = cnd % n;
-      std::vector<int> t{(int)a};
-      if (i < d - 2) t.insert(t.end(), right[i + 1][beta].begin(), right[i + 1][beta].end());
-      right[i].push_back(t);
-    }
-  }
-  for (int i = 0; i < d - 1; ++i) {
-    int32_t* R = rec.data() + (long long)i * RS;
-    R[0] = r[i];
-    for (int s = 0; s < r[i]; ++s) {
-      for (int q = 0; q <= i; ++q) R[1 + (long long)s * d + q] = left[i][s][q];
-      for (int q = i + 1; q < d; ++q) R[1 + (long long)s * d + q] = right[i][s][q - i - 1];
-    }
-  }
-}
-
 // ------------------------------------------------------------------ launch sequences
-// frozen parts + fiber entries for jobs [jbase, jbase+njobs) of the given kind
+// quadrature fibers: frozen parts + entries for modes [jbase, jbase+njobs)
 int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
   DevCtx& dc = c->dc;
-  const int nc = dc.ncols_max, n = dc.n;
-  const int tup_max = std::max(nc, dc.cap);
+  const int n = dc.n, tup = dc.cap;
   {
     Timed t(c, K_FROZEN_SIDES);
-    k_frozen_sides<<<dim3((tup_max + 63) / 64, 2, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
+    k_frozen_sides<<<dim3((tup + 63) / 64, 2, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
   }
   if (int e = check_launch("k_frozen_sides")) return e;
   if (dc.family == TTC_FAMILY_D) {
     {
       Timed t(c, K_FROZEN_Q);
-      k_frozen_q<<<dim3((n + 127) / 128, tup_max, 2 * njobs), 128, 0, c->ls>>>(dc, kind, jbase);
+      k_frozen_q<<<dim3((n + 127) / 128, tup, 2 * njobs), 128, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_q")) return e;
     {
       Timed t(c, K_FROZEN_LR);
-      k_frozen_lr<<<dim3((tup_max + 63) / 64, tup_max, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
+      k_frozen_lr<<<dim3((tup + 63) / 64, tup, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_lr")) return e;
   }
-  const int gx = std::min(4096, (tup_max * n + 255) / 256);
+  const int gx = std::min(4096, (tup * n + 255) / 256);
   {
     Timed t(c, K_FIBER);
     if (dc.family == TTC_FAMILY_C)
-      k_fiber<0><<<dim3(gx, tup_max, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+      k_fiber<0><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
     else
-      k_fiber<1><<<dim3(gx, tup_max, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+      k_fiber<1><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
   }
   return check_launch("k_fiber");
 }
 
-int launch_cross(ttc_ctx* c, int kind) {
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(c->n_owned * c->G);
-  lc.blockDim = dim3(CROSS_THREADS);
-  lc.dynamicSmemBytes = c->cross_smem;
-  lc.stream = c->ls;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = c->G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  cudaError_t e;
-  {
-    Timed t(c, K_CROSS);
-    if (c->smem_mode)
-      e = cudaLaunchKernelEx(&lc, k_cross<true>, c->dc, kind, c->G, c->rpc);
-    else
-      e = cudaLaunchKernelEx(&lc, k_cross<false>, c->dc, kind, c->G, c->rpc);
-  }
-  if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_cross launch: ") + cudaGetErrorString(e));
-  return check_launch("k_cross");
-}
-
-int do_half_sweep(ttc_ctx* c, int dir) {
+// one Alg. 6 sweep over the owned superblocks -> rec_next
+int do_sweep_local(ttc_ctx* c) {
   if (c->n_owned > 0) {
     DevCtx& dc = c->dc;
+    const int nj = c->n_owned, cap = dc.cap, n = dc.n;
     {
-      Timed t(c, K_ENRICH);
-      k_enrich<<<c->n_owned, 128, 0, c->ls>>>(dc, dir, c->sweeps);
+      Timed t(c, K_SB_SIDES);
+      k_sb_sides<<<dim3((n + 127) / 128 > 4 ? 4 : (n + 127) / 128, cap, 2 * nj), 128, 0, c->ls>>>(dc);
     }
-    if (int e = check_launch("k_enrich")) return e;
-    if (int e = launch_fibers(c, dir, 0, c->n_owned)) return e;
-    if (int e = launch_cross(c, dir)) return e;
+    if (int e = check_launch("k_sb_sides")) return e;
+    if (dc.family == TTC_FAMILY_D) {
+      {
+        Timed t(c, K_SB_CX);
+        k_sb_cx<<<dim3((cap + 63) / 64, cap, nj), 64, 0, c->ls>>>(dc);
+      }
+      if (int e = check_launch("k_sb_cx")) return e;
+    }
+    const int gx = (int)((dc.sbn + 255) / 256);
     {
-      Timed t(c, K_COMMIT);
-      k_commit<<<dim3(dc.cap, c->n_owned), 64, 0, c->ls>>>(dc, dir);
+      Timed t(c, K_SB_EXT_ROWS);
+      if (dc.family == TTC_FAMILY_C) k_sb_extend_rows<0><<<dim3(gx, nj), 256, 0, c->ls>>>(dc);
+      else k_sb_extend_rows<1><<<dim3(gx, nj), 256, 0, c->ls>>>(dc);
     }
-    if (int e = check_launch("k_commit")) return e;
-  }
-  if (c->cfg.world == 1) {
-    // nothing to exchange: all interfaces are owned
+    if (int e = check_launch("k_sb_extend_rows")) return e;
+    {
+      Timed t(c, K_SB_EXT_COLS);
+      if (dc.family == TTC_FAMILY_C) k_sb_extend_cols<0><<<dim3(gx, nj), 256, 0, c->ls>>>(dc);
+      else k_sb_extend_cols<1><<<dim3(gx, nj), 256, 0, c->ls>>>(dc);
+    }
+    if (int e = check_launch("k_sb_extend_cols")) return e;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(nj * dc.G);
+    lc.blockDim = dim3(GREEDY_THREADS);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = c->ls;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = dc.G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t e;
+    {
+      Timed t(c, K_GREEDY);
+      if (dc.family == TTC_FAMILY_C) e = cudaLaunchKernelEx(&lc, k_greedy<0>, dc, c->sweeps);
+      else e = cudaLaunchKernelEx(&lc, k_greedy<1>, dc, c->sweeps);
+    }
+    if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_greedy launch: ") + cudaGetErrorString(e));
+    if (int e2 = check_launch("k_greedy")) return e2;
   }
   c->pending = 1;
   return TTC_OK;
 }
 
 int do_commit(ttc_ctx* c) {
-  if (!c->pending) return fail(TTC_ERR_STATE, "tt_cross_commit without a pending half-sweep");
+  if (!c->pending) return fail(TTC_ERR_STATE, "tt_cross_commit without a pending local sweep");
   std::swap(c->dc.rec_cur, c->dc.rec_next);
   c->pending = 0;
-  c->half_sweeps++;
-  if (c->half_sweeps % 2 == 0) c->sweeps++;
+  c->sweeps++;
   return TTC_OK;
 }
 
@@ -353,7 +290,7 @@ int do_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sig
   CK(cudaStreamSynchronize(c->stream));
   int flag = 0;
   std::memcpy(&flag, c->out_host + 2, sizeof(int));
-  if (flag) return fail(TTC_ERR_SINGULAR, "an intersection matrix A(I_{<=i}, I_{>i}) is singular");
+  if (flag) return fail(TTC_ERR_SINGULAR, "an intersection matrix A(I_{<=k}, I_{>k}) is singular");
   const double core = c->out_host[0];
   const double lg2 = c->out_host[1];
   int sg = core > 0 ? 1 : (core < 0 ? -1 : 0);
@@ -398,17 +335,23 @@ int resolve_timing(ttc_ctx* c) {
   return TTC_OK;
 }
 
-// device part of a reset (async, capturable): initial pivots and the evaluation counter
+// device part of a reset (async, capturable): rank-1 start, superblock state, counters
 int reset_device(ttc_ctx* c) {
-  CK(cudaMemcpyAsync(c->dc.rec_cur, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->ls));
-  CK(cudaMemcpyAsync(c->dc.rec_next, c->rec_init, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice, c->ls));
   CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
-  return TTC_OK;
+  {
+    Timed t(c, K_INIT_PIVOT);
+    k_init_pivot<<<1, N_INIT, 0, c->ls>>>(c->dc, c->t0buf);
+  }
+  if (int e = check_launch("k_init_pivot")) return e;
+  {
+    Timed t(c, K_INIT_RECORDS);
+    k_init_records<<<std::max(c->nrec, c->n_owned), 128, 0, c->ls>>>(c->dc, c->t0buf, c->nrec, c->n_owned);
+  }
+  return check_launch("k_init_records");
 }
 
 int reset_host(ttc_ctx* c) {
   c->sweeps = 0;
-  c->half_sweeps = 0;
   c->pending = 0;
   c->launches = 0;
   if (int e = resolve_timing(c)) return e;
@@ -417,20 +360,24 @@ int reset_host(ttc_ctx* c) {
   return TTC_OK;
 }
 
-// n_sweeps full sweeps + the quadrature, enqueued on c->ls (world == 1)
+int do_reset(ttc_ctx* c) {
+  if (int e = reset_host(c)) return e;
+  return reset_device(c);
+}
+
+// n_sweeps sweeps + the quadrature, enqueued on c->ls (world == 1)
 int enqueue_solve(ttc_ctx* c, int n_sweeps) {
-  for (int s = 0; s < n_sweeps; ++s)
-    for (int dir : {TTC_DIR_LR, TTC_DIR_RL}) {
-      if (int e = do_half_sweep(c, dir)) return e;
-      if (int e = do_commit(c)) return e;
-    }
+  for (int s = 0; s < n_sweeps; ++s) {
+    if (int e = do_sweep_local(c)) return e;
+    if (int e = do_commit(c)) return e;
+  }
   if (int e = do_integrate_local(c)) return e;
   return do_integrate_finish_launch(c);
 }
 
 // Capture reset + n_sweeps sweeps + quadrature as one CUDA graph.  Every launch shape
-// depends only on (d, n, cap, p); ranks are read on the device, so the graph is valid for
-// any grid loaded into this context.
+// depends only on (d, n, cap); ranks are read on the device, so the graph is valid for any
+// grid loaded into this context.
 int capture_solve(ttc_ctx* c, int n_sweeps) {
   if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
   if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
@@ -467,7 +414,7 @@ extern "C" {
 const char* tt_last_error(void) { return g_err.c_str(); }
 
 const char* tt_build_info(void) {
-  return "libttcross 0.1 (sm_100a, fp64, -fmad=false, cluster cross+maxvol)";
+  return "libttcross 0.2 (sm_100a, fp64, -fmad=false, dimension-parallel greedy cross, cluster rook search)";
 }
 
 int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, const double* weights,
@@ -479,10 +426,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   if (k.d < 2 || k.d > 2000) return fail(TTC_ERR_ARG, "d must be in [2, 2000]");
   if (k.n < 2 || k.n > 4096) return fail(TTC_ERR_ARG, "n must be in [2, 4096]");
   if (k.rank_cap < 1 || k.rank_cap > TTC_MAX_RANK) return fail(TTC_ERR_ARG, "rank_cap must be in [1, 64]");
-  if (k.n_enrich < 0 || k.n_enrich > TTC_MAX_ENRICH) return fail(TTC_ERR_ARG, "n_enrich must be in [0, 16]");
-  if (k.max_swaps < 0) return fail(TTC_ERR_ARG, "max_swaps must be >= 0");
+  if (k.n_samples < 1 || k.n_samples > TTC_MAX_SAMPLES) return fail(TTC_ERR_ARG, "n_samples must be in [1, 1024]");
+  if (k.rook_iters < 0 || k.rook_iters > 64) return fail(TTC_ERR_ARG, "rook_iters must be in [0, 64]");
   if (!(k.tol >= 0.0 && k.tol < 1.0)) return fail(TTC_ERR_ARG, "tol must be in [0, 1)");
-  if (!(k.delta >= 0.0)) return fail(TTC_ERR_ARG, "delta must be >= 0");
   if (k.world < 1 || k.rank < 0 || k.rank >= k.world) return fail(TTC_ERR_ARG, "need 0 <= rank < world");
   if (mem_kind != TTC_MEM_HOST && mem_kind != TTC_MEM_DEVICE) return fail(TTC_ERR_ARG, "mem_kind");
   if (mem_kind == TTC_MEM_HOST) {
@@ -492,19 +438,17 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
 
   ttc_ctx* c = new ttc_ctx();
   c->cfg = k;
-  if (c->cfg.max_swaps == 0) c->cfg.max_swaps = 2 * k.rank_cap;
   c->stream = static_cast<cudaStream_t>(stream);
   c->ls = c->stream;
-  const int d = k.d, n = k.n, cap = k.rank_cap, p = k.n_enrich;
+  const int d = k.d, n = k.n, cap = k.rank_cap;
   DevCtx& dc = c->dc;
   dc.family = k.family;
   dc.d = d;
   dc.n = n;
   dc.cap = cap;
-  dc.p = p;
-  dc.max_swaps = c->cfg.max_swaps;
+  dc.ns = k.n_samples;
+  dc.rook = k.rook_iters;
   dc.tol = k.tol;
-  dc.delta = k.delta;
   dc.seed = k.seed;
   dc.world = k.world;
   dc.rank = k.rank;
@@ -515,13 +459,15 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   c->n_owned = c->ke - c->kb;
   dc.kb = c->kb;
   dc.ke = c->ke;
-  dc.RS = 1 + cap * d;
-  dc.ncols_max = cap + p;
+  dc.RS = 1 + cap * d + 2 * cap;
+  dc.sbn = (long long)cap * n;
+  // cluster size of k_greedy: about 8192 superblock rows per CTA, at most 8 CTAs
+  dc.G = (int)std::min<long long>(8, std::max<long long>(1, (dc.sbn + 8191) / 8192));
   c->slots = d;
-  const long long nrec = (long long)k.world * c->chunk;
-  c->rec_ints = nrec * dc.RS;
-  dc.fib_stride = (long long)cap * dc.ncols_max * n;
-  const int tup = std::max(dc.ncols_max, cap);
+  c->nrec = k.world * c->chunk;
+  c->rec_ints = (long long)c->nrec * dc.RS;
+  dc.fib_stride = (long long)cap * cap * n;
+  const int nj = std::max(1, c->n_owned);
 
   auto bail = [&](int e) {
     tt_cross_destroy(c);
@@ -537,93 +483,44 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.w = w;
   dc.chi = chi;
   dc.clo = clo;
+  const size_t tab = (size_t)nj * cap * n;
   if ((e = dalloc(c, &dc.rec_cur, (size_t)c->rec_ints)) || (e = dalloc(c, &dc.rec_next, (size_t)c->rec_ints)) ||
-      (e = dalloc(c, &c->rec_init, (size_t)c->rec_ints)) ||
-      (e = dalloc(c, &dc.ext, (size_t)(d - 1) * dc.ncols_max * d)) || (e = dalloc(c, &dc.ext_cnt, (size_t)d)) ||
+      (e = dalloc(c, &c->t0buf, (size_t)d)) ||
+      (e = dalloc(c, &dc.SA, tab)) || (e = dalloc(c, &dc.SB, tab)) ||
+      (e = dalloc(c, &dc.U, (size_t)nj * cap * dc.sbn)) || (e = dalloc(c, &dc.V, (size_t)nj * cap * dc.sbn)) ||
+      (e = dalloc(c, &dc.Araw, (size_t)nj * dc.sbn)) || (e = dalloc(c, &dc.praw_max, (size_t)nj)) ||
+      (e = dalloc(c, &dc.sbstate, (size_t)nj * 4)) ||
       (e = dalloc(c, &dc.fib, (size_t)c->slots * dc.fib_stride)) ||
-      (e = dalloc(c, &dc.sl, (size_t)c->slots * tup)) || (e = dalloc(c, &dc.sr, (size_t)c->slots * tup)) ||
-      (e = dalloc(c, &dc.pll, (size_t)c->slots * tup)) || (e = dalloc(c, &dc.prr, (size_t)c->slots * tup)) ||
-      (e = dalloc(c, &dc.pf, (size_t)c->slots * tup * tup)) ||
-      (e = dalloc(c, &dc.sel_row, (size_t)c->slots * cap)) || (e = dalloc(c, &dc.sel_col, (size_t)c->slots * cap)) ||
-      (e = dalloc(c, &dc.sel_rank, (size_t)c->slots)) || (e = dalloc(c, &dc.sel_nsw, (size_t)c->slots)) ||
+      (e = dalloc(c, &dc.sl, (size_t)c->slots * cap)) || (e = dalloc(c, &dc.sr, (size_t)c->slots * cap)) ||
+      (e = dalloc(c, &dc.pll, (size_t)c->slots * cap)) || (e = dalloc(c, &dc.prr, (size_t)c->slots * cap)) ||
+      (e = dalloc(c, &dc.pf, (size_t)c->slots * cap * cap)) ||
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
       (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) ||
       (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)))
     return bail(e);
   if (k.family == TTC_FAMILY_D) {
-    if ((e = dalloc(c, &dc.ql, (size_t)c->slots * tup * n)) || (e = dalloc(c, &dc.qr, (size_t)c->slots * tup * n)))
+    if ((e = dalloc(c, &dc.ql, (size_t)c->slots * cap * n)) || (e = dalloc(c, &dc.qr, (size_t)c->slots * cap * n)) ||
+        (e = dalloc(c, &dc.PA, tab)) || (e = dalloc(c, &dc.PB, tab)) || (e = dalloc(c, &dc.QL1, tab)) ||
+        (e = dalloc(c, &dc.QR0, tab)) || (e = dalloc(c, &dc.CX, (size_t)nj * cap * cap)))
       return bail(e);
   }
   {
     cudaError_t ce = cudaMallocHost(&c->out_host, 8 * sizeof(double));
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(ce)));
   }
-  // grid upload
-  const cudaMemcpyKind kind = mem_kind == TTC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   {
-    cudaError_t ce = cudaMemcpyAsync(u, nodes_u, sizeof(double) * d * n, kind, c->stream);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(w, weights, sizeof(double) * d * n, kind, c->stream);
-    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("grid upload: ") + cudaGetErrorString(ce)));
-  }
-  {
-    Timed t(c, K_PREP);
-    k_prep_nodes<<<(d * n + 255) / 256, 256, 0, c->stream>>>(u, chi, clo, d * n);
-  }
-  if ((e = check_launch("k_prep_nodes"))) return bail(e);
-  // initial pivots (host, mirrors the oracle), uploaded once and kept for reset
-  std::vector<int32_t> rec;
-  initial_records(c->cfg, dc.RS, nrec, rec);
-  {
-    cudaError_t ce = cudaMemcpy(c->rec_init, rec.data(), sizeof(int32_t) * rec.size(), cudaMemcpyHostToDevice);
-    if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("pivot upload: ") + cudaGetErrorString(ce)));
-  }
-  // cross kernel shape: smallest cluster whose shared memory holds the fiber matrix
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int optin = 0;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t head = ((sizeof(CrossSmem) + 127) / 128) * 128;
-    const long long nrows_max = (long long)cap * n;
-    c->smem_mode = false;
-    for (int G : {1, 2, 4, 8, 16}) {
-      long long rpc = (nrows_max + G - 1) / G;
-      size_t bytes = head + (size_t)rpc * dc.ncols_max * sizeof(double);
-      if (bytes <= (size_t)optin) {
-        c->G = G;
-        c->rpc = (int)rpc;
-        c->cross_smem = bytes;
-        c->smem_mode = true;
-        break;
-      }
-    }
-    if (!c->smem_mode) {
-      c->G = 16;
-      c->rpc = (int)((nrows_max + 15) / 16);
-      c->cross_smem = head;
-    }
-    cudaError_t ce = cudaFuncSetAttribute(k_cross<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_cross<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (ce == cudaSuccess)
-      ce = cudaFuncSetAttribute(k_cross<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(c->cross_smem, head));
-    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_cross<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head);
+    cudaError_t ce = cudaFuncSetAttribute(k_greedy<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_greedy<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   }
-  c->timing = false;
-  int rc = tt_cross_reset(c);
+  int rc = tt_cross_load_grid(c, nodes_u, weights, mem_kind);
   if (rc) return bail(rc);
   *out = c;
   return TTC_OK;
-}
-
-int tt_cross_reset(ttc_ctx* c) {
-  if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (int e = reset_device(c)) return e;
-  return reset_host(c);
 }
 
 int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights, int32_t mem_kind) {
@@ -633,7 +530,7 @@ int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights,
   if (mem_kind == TTC_MEM_HOST)
     for (long long t = 0; t < (long long)d * n; ++t)
       if (!(nodes_u[t] > 0.0) || !std::isfinite(nodes_u[t])) return fail(TTC_ERR_ARG, "u-nodes must be finite and > 0");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   const cudaMemcpyKind kind = mem_kind == TTC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   CK(cudaMemcpyAsync(const_cast<double*>(c->dc.u), nodes_u, sizeof(double) * d * n, kind, c->stream));
   CK(cudaMemcpyAsync(const_cast<double*>(c->dc.w), weights, sizeof(double) * d * n, kind, c->stream));
@@ -646,46 +543,15 @@ int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights,
   return tt_cross_reset(c);
 }
 
-int tt_solve_launch(ttc_ctx* c, int32_t n_sweeps, int32_t use_graph) {
+int tt_cross_reset(ttc_ctx* c) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_solve_launch needs world == 1");
-  if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
-  if (!use_graph) {
-    if (int e = reset_device(c)) return e;
-    if (int e = reset_host(c)) return e;
-    if (int e = enqueue_solve(c, n_sweeps)) return e;
-    return TTC_OK;
-  }
-  if (!c->graph_exec || c->graph_sweeps != n_sweeps) {
-    if (int e = capture_solve(c, n_sweeps)) return e;
-  }
-  if (int e = reset_host(c)) return e;
-  CK(cudaGraphLaunch(c->graph_exec, c->stream));
-  c->launches = c->graph_launches;
-  c->sweeps = n_sweeps;
-  c->half_sweeps = 2 * n_sweeps;
-  return TTC_OK;
+  return do_reset(c);
 }
 
-int tt_integrate_launch(ttc_ctx* c) {
+int tt_cross_sweep_local(ttc_ctx* c) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate_launch needs world == 1");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
-  if (int e = do_integrate_local(c)) return e;
-  return do_integrate_finish_launch(c);
-}
-
-int tt_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
-  if (!c) return fail(TTC_ERR_ARG, "null context");
-  return do_integrate_read(c, value, log10_abs, sign);
-}
-
-int tt_cross_half_sweep(ttc_ctx* c, int32_t direction) {
-  if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (direction != TTC_DIR_LR && direction != TTC_DIR_RL) return fail(TTC_ERR_ARG, "direction");
-  if (c->pending) return fail(TTC_ERR_STATE, "previous half-sweep not committed");
-  return do_half_sweep(c, direction);
+  if (c->pending) return fail(TTC_ERR_STATE, "previous local sweep not committed");
+  return do_sweep_local(c);
 }
 
 int tt_cross_commit(ttc_ctx* c) {
@@ -697,12 +563,10 @@ int tt_cross_sweep(ttc_ctx* c, int32_t n_sweeps) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_cross_sweep needs world == 1");
   if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   for (int s = 0; s < n_sweeps; ++s) {
-    for (int dir : {TTC_DIR_LR, TTC_DIR_RL}) {
-      if (int e = do_half_sweep(c, dir)) return e;
-      if (int e = do_commit(c)) return e;
-    }
+    if (int e = do_sweep_local(c)) return e;
+    if (int e = do_commit(c)) return e;
   }
   return TTC_OK;
 }
@@ -715,18 +579,50 @@ int tt_cross_exchange_buffer(ttc_ctx* c, void** dev_ptr, int64_t* bytes_total, i
   return TTC_OK;
 }
 
+int tt_solve_launch(ttc_ctx* c, int32_t n_sweeps, int32_t use_graph) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_solve_launch needs world == 1");
+  if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  if (!use_graph) {
+    if (int e = do_reset(c)) return e;
+    return enqueue_solve(c, n_sweeps);
+  }
+  if (!c->graph_exec || c->graph_sweeps != n_sweeps) {
+    if (int e = capture_solve(c, n_sweeps)) return e;
+  }
+  if (int e = reset_host(c)) return e;
+  CK(cudaGraphLaunch(c->graph_exec, c->stream));
+  c->launches = c->graph_launches;
+  c->sweeps = n_sweeps;
+  return TTC_OK;
+}
+
 int tt_integrate(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate needs world == 1");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   if (int e = do_integrate_local(c)) return e;
   if (int e = do_integrate_finish_launch(c)) return e;
   return do_integrate_read(c, value, log10_abs, sign);
 }
 
+int tt_integrate_launch(ttc_ctx* c) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_integrate_launch needs world == 1");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  if (int e = do_integrate_local(c)) return e;
+  return do_integrate_finish_launch(c);
+}
+
+int tt_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  return do_integrate_read(c, value, log10_abs, sign);
+}
+
 int tt_integrate_local(ttc_ctx* c) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (c->pending) return fail(TTC_ERR_STATE, "pending half-sweep");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   return do_integrate_local(c);
 }
 
@@ -745,7 +641,7 @@ int tt_integrate_finish(ttc_ctx* c, double* value, double* log10_abs, int32_t* s
   return do_integrate_read(c, value, log10_abs, sign);
 }
 
-int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out) {
+int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out, int32_t* par_out) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   const int d = c->dc.d, cap = c->dc.cap, RS = c->dc.RS;
   std::vector<int32_t> rec(c->rec_ints);
@@ -755,10 +651,11 @@ int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out) {
     const int32_t* R = rec.data() + (long long)i * RS;
     if (ranks_out) ranks_out[i] = R[0];
     if (piv_out)
-      for (long long t = 0; t < (long long)cap * d; ++t) {
-        const long long s = t / d;
-        piv_out[(long long)i * cap * d + t] = s < R[0] ? R[1 + t] : -1;
-      }
+      for (long long t = 0; t < (long long)cap * d; ++t)
+        piv_out[(long long)i * cap * d + t] = (t / d) < R[0] ? R[1 + t] : -1;
+    if (par_out)
+      for (long long t = 0; t < 2LL * cap; ++t)
+        par_out[(long long)i * cap * 2 + t] = (t / 2) < R[0] ? R[1 + (long long)cap * d + t] : -1;
   }
   return TTC_OK;
 }
@@ -792,17 +689,16 @@ int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
   out->evals = (int64_t)cnt[CNT_EVALS];
   out->launches = c->launches;
   out->sweeps = c->sweeps;
-  out->half_sweeps = c->half_sweeps;
   out->ms_fiber = c->ms[KC_FIBER];
   out->ms_cross = c->ms[KC_CROSS];
   out->ms_quad = c->ms[KC_QUAD];
   out->ms_other = c->ms[KC_OTHER];
-  out->fiber_launches = c->klaunch[K_FIBER];
-  out->cross_launches = c->klaunch[K_CROSS];
   out->fiber_entries = (int64_t)cnt[CNT_FIBER_ENTRIES];
-  out->cross_updates = (int64_t)cnt[CNT_CROSS_UPDATES];
-  out->cross_steps = (int64_t)cnt[CNT_CROSS_STEPS];
-  out->cross_elems = (int64_t)cnt[CNT_CROSS_ELEMS];
+  out->sb_entries = (int64_t)cnt[CNT_SB_ENTRIES];
+  out->sb_updates = (int64_t)cnt[CNT_SB_UPDATES];
+  out->rook_steps = (int64_t)cnt[CNT_ROOK_STEPS];
+  out->ext_entries = (int64_t)cnt[CNT_EXT_ENTRIES];
+  out->ext_updates = (int64_t)cnt[CNT_EXT_UPDATES];
   return TTC_OK;
 }
 

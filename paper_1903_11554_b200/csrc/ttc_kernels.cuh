@@ -1,4 +1,4 @@
-// ttc_kernels.cuh -- fiber evaluation, enrichment, commit and quadrature kernels.
+// ttc_kernels.cuh -- node tables, fiber evaluation and quadrature kernels.
 //
 // Fiber of mode m for a job: F[alpha][beta][a] = A(X[alpha][0:m], a, Y[beta][m+1:d])
 // (eq. (3) factors A(I_{<=k-1}, i_k, I_{>k}), lines 312-320).  The entry is
@@ -28,68 +28,6 @@ __global__ void k_prep_nodes(const double* __restrict__ u, long long* chi, long 
 }
 
 // ---------------------------------------------------------------------------------------
-// enrichment: extended column set of interface i (existing pivots + p random superblock
-// columns, duplicates skipped) -- PAPER.md Alg. 2 line 1 ("random set of samples")
-// ---------------------------------------------------------------------------------------
-__global__ void k_enrich(DevCtx c, int dir, int sweep) {
-  const int i = c.kb + blockIdx.x;
-  const int d = c.d, n = c.n;
-  __shared__ int cand[2048 + 8];
-  __shared__ int cnt, dup;
-  int* ext = c.ext + (long long)i * c.ncols_max * d;
-  const int r = rec_rank(c.rec_cur, c.RS, i);
-  const int* P = rec_piv(c.rec_cur, c.RS, i);
-  for (int t = threadIdx.x; t < r * d; t += blockDim.x) ext[t] = P[t];
-  if (threadIdx.x == 0) cnt = r;
-  // range of coordinates that identifies a column of this interface
-  const int lo = (dir == JOB_LR) ? i + 1 : 0;
-  const int hi = (dir == JOB_LR) ? d : i + 1;
-  const uint64_t tag = 2ULL + 2ULL * (uint64_t)sweep + (uint64_t)dir;
-  __syncthreads();
-  for (int jd = 0; jd < c.p; ++jd) {
-    if (threadIdx.x == 0) {
-      long long M;
-      if (dir == JOB_LR) M = (long long)((i < d - 2) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1) * n;
-      else M = (long long)((i > 0) ? rec_rank(c.rec_cur, c.RS, i - 1) : 1) * n;
-      uint64_t v = splitmix64(c.seed, draw_ctr(tag, d, i, jd)) % (uint64_t)M;
-      int outer = (int)(v / (uint64_t)n), a = (int)(v % (uint64_t)n);
-      dup = 0;
-      if (dir == JOB_LR) {
-        for (int j = 0; j <= i; ++j) cand[j] = -1;
-        cand[i + 1] = a;
-        if (i < d - 2) {
-          const int* Pn = rec_piv(c.rec_cur, c.RS, i + 1) + (long long)outer * d;
-          for (int j = i + 2; j < d; ++j) cand[j] = Pn[j];
-        }
-      } else {
-        if (i > 0) {
-          const int* Pp = rec_piv(c.rec_cur, c.RS, i - 1) + (long long)outer * d;
-          for (int j = 0; j < i; ++j) cand[j] = Pp[j];
-        }
-        cand[i] = a;
-        for (int j = i + 1; j < d; ++j) cand[j] = -1;
-      }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-      const int* E = ext + (long long)e * d;
-      bool eq = true;
-      for (int j = lo; j < hi; ++j)
-        if (E[j] != cand[j]) { eq = false; break; }
-      if (eq) atomicOr(&dup, 1);
-    }
-    __syncthreads();
-    if (!dup) {
-      for (int j = threadIdx.x; j < d; j += blockDim.x) ext[(long long)cnt * d + j] = cand[j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && !dup) cnt++;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) c.ext_cnt[i] = cnt;
-}
-
-// ---------------------------------------------------------------------------------------
 // frozen parts, per (job, side, tuple): S_L / P_LL (side 0), S_R / P_RR (side 1)
 // grid: x = tuple (<= ncols_max), y = side, z = job
 // ---------------------------------------------------------------------------------------
@@ -98,7 +36,7 @@ __global__ void k_frozen_sides(DevCtx c, int kind, int jbase) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   Job jb = make_job(c, kind, j);
   const int d = c.d, n = c.n, m = jb.m;
-  const long long so = (long long)j * c.ncols_max + t;
+  const long long so = (long long)j * c.cap + t;
   if (side == 0 && t == 0 && c.counters) {
     atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)jb.rx * jb.ry * n);
     atomicAdd(&c.counters[CNT_FIBER_ENTRIES], (unsigned long long)jb.rx * jb.ry * n);
@@ -147,7 +85,7 @@ __global__ void k_frozen_q(DevCtx c, int kind, int jbase) {
   const int m = jb.m;
   const double um = c.u[m * n + a];
   DDE p = dde_one();
-  const long long o = ((long long)j * c.ncols_max + tup) * n + a;
+  const long long o = ((long long)j * c.cap + tup) * n + a;
   if (side == 0) {
     if (tup >= jb.rx) return;
     if (jb.X) {
@@ -172,7 +110,7 @@ __global__ void k_frozen_lr(DevCtx c, int kind, int jbase) {
   Job jb = make_job(c, kind, j);
   if (al >= jb.rx || be >= jb.ry) return;
   const int d = c.d, n = c.n, m = jb.m;
-  const long long base = (long long)j * c.ncols_max;
+  const long long base = (long long)j * c.cap;
   DDE p = c.pll[base + al];
   dde_mul(p, c.prr[base + be]);
   if (jb.X && jb.Y) {
@@ -183,7 +121,7 @@ __global__ void k_frozen_lr(DevCtx c, int kind, int jbase) {
       for (int b = m + 1; b < d; ++b) dde_mul_d(p, rho(ua, c.u[b * n + TY[b]]));
     }
   }
-  c.pf[(base + al) * c.ncols_max + be] = p;
+  c.pf[(base + al) * c.cap + be] = p;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -196,7 +134,7 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
   if (al >= jb.rx) return;
   const int n = c.n, m = jb.m;
   const int total = jb.ry * n;
-  const long long base = (long long)j * c.ncols_max;
+  const long long base = (long long)j * c.cap;
   const ESum sl = c.sl[base + al];
   double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
@@ -211,57 +149,13 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
     if (FAMILY == 0) {
       v = __drcp_rn(SS);
     } else {
-      DDE p = c.pf[(base + al) * c.ncols_max + be];
+      DDE p = c.pf[(base + al) * c.cap + be];
       dde_mul(p, c.ql[(base + al) * n + a]);
       dde_mul(p, c.qr[(base + be) * n + a]);
       v = __ddiv_rn(dde_round(p), SS);
     }
     F[f] = v;
   }
-}
-
-// ---------------------------------------------------------------------------------------
-// commit the selected cross of every owned interface into rec_next
-// grid: x = slot, y = job ; block threads over the d coordinates
-// ---------------------------------------------------------------------------------------
-__global__ void k_commit(DevCtx c, int kind) {
-  const int j = blockIdx.y, s = blockIdx.x;
-  Job jb = make_job(c, kind, j);
-  const int i = jb.iface, d = c.d, n = c.n, m = jb.m;
-  const int rnew = c.sel_rank[j];
-  int* R = c.rec_next + (long long)i * c.RS;
-  const int* Pc = rec_piv(c.rec_cur, c.RS, i);
-  if (rnew == 0) {  // identically zero fiber: keep the interface (R8)
-    const int rold = rec_rank(c.rec_cur, c.RS, i);
-    if (s == 0 && threadIdx.x == 0) R[0] = rold;
-    for (int q = threadIdx.x; q < d; q += blockDim.x)
-      R[1 + (long long)s * d + q] = s < rold ? Pc[(long long)s * d + q] : -1;
-    return;
-  }
-  if (s == 0 && threadIdx.x == 0) R[0] = rnew;
-  if (s >= rnew) {
-    for (int q = threadIdx.x; q < d; q += blockDim.x) R[1 + (long long)s * d + q] = -1;
-    return;
-  }
-  const int row = c.sel_row[(long long)j * c.cap + s];
-  const int col = c.sel_col[(long long)j * c.cap + s];
-  const int outer = row / n, a = row - outer * n;
-  const int x = (kind == JOB_LR) ? outer : col;
-  const int y = (kind == JOB_LR) ? col : outer;
-  for (int q = threadIdx.x; q < d; q += blockDim.x) {
-    int v;
-    if (q < m) v = jb.X[(long long)x * d + q];
-    else if (q == m) v = a;
-    else v = jb.Y[(long long)y * d + q];
-    R[1 + (long long)s * d + q] = v;
-  }
-}
-
-// copy records of non-owned interfaces (world == 1: none; used so rec_next is complete)
-__global__ void k_copy_records(int* dst, const int* src, long long nints) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nints;
-       t += (long long)gridDim.x * blockDim.x)
-    dst[t] = src[t];
 }
 
 // ---------------------------------------------------------------------------------------

@@ -3,7 +3,7 @@
 One process per GPU.  Interfaces (superblocks) are partitioned into contiguous chunks,
 rank p owning [p*chunk, min(d-1, (p+1)*chunk)) with chunk = ceil((d-1)/world) (Alg. 6
 line 1 "Deduce the range [k_beg, k_end) of superblocks belonging to the process p").
-After every half-sweep each rank has the new pivots of its own interfaces in its slice of
+After every sweep each rank has the new pivots of its own interfaces in its slice of
 the library's record buffer; an all-gather of that buffer gives every rank the complete
 new index sets (the paper exchanges only neighbour pivots, Alg. 6 lines 6-8; an all-gather
 over NVSwitch costs one latency-bound collective of a few KB, and every rank needs the full
@@ -20,7 +20,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from .binding import TTC_DIR_LR, TTC_DIR_RL, TTCross
+from .binding import TTCross
 
 
 def owned_interfaces(d: int, rank: int, world: int):
@@ -51,14 +51,13 @@ class DistTTCross:
     All device work (the library's and NCCL's) is ordered on torch's current CUDA stream.
     """
 
-    def __init__(self, family, u, w, rank_cap, tol, n_enrich=4, max_swaps=0, delta=1e-2, seed=0,
-                 group=None):
+    def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, group=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.stream = torch.cuda.current_stream()
-        self.tt = TTCross(family, u, w, rank_cap, tol, n_enrich=n_enrich, max_swaps=max_swaps, delta=delta,
-                          seed=seed, rank=self.rank, world=self.world, stream=self.stream.cuda_stream)
+        self.tt = TTCross(family, u, w, rank_cap, tol, n_samples=n_samples, rook_iters=rook_iters, seed=seed,
+                          rank=self.rank, world=self.world, stream=self.stream.cuda_stream)
         dev = torch.device("cuda", torch.cuda.current_device())
         xv, xper = self.tt.exchange_view()
         self.xbuf = torch.as_tensor(xv, device=dev)
@@ -68,15 +67,12 @@ class DistTTCross:
         self.pper = pper // 8
         self.d = self.tt.d
 
-    def half_sweep(self, direction):
-        self.tt.half_sweep(direction)
-        allgather_slices(self.xbuf, self.xper, self.group)
-        self.tt.commit()
-
     def sweep(self, n_sweeps=1):
+        """n_sweeps Alg. 6 sweeps: local superblock updates, all-gather of the records, commit."""
         for _ in range(n_sweeps):
-            self.half_sweep(TTC_DIR_LR)
-            self.half_sweep(TTC_DIR_RL)
+            self.tt.sweep_local()
+            allgather_slices(self.xbuf, self.xper, self.group)
+            self.tt.commit()
 
     def integrate_launch(self):
         self.tt.integrate_local()

@@ -44,11 +44,18 @@ def test_build_info_and_error_string(lib):
     assert isinstance(lib.tt_last_error(), bytes)
 
 
-@pytest.mark.parametrize("field,value", [("d", 1), ("n", 1), ("rank_cap", 0), ("rank_cap", 65),
-                                         ("family", 7), ("n_enrich", 17), ("tol", 1.5), ("world", 0)])
+def good_config(binding):
+    # family, d, n, rank_cap, n_samples, rook_iters, tol, seed, rank, world
+    return binding.TtcConfig(0, 4, 9, 4, 16, 4, 1e-12, 1, 0, 1)
+
+
+@pytest.mark.parametrize("field,value", [("d", 1), ("d", 2001), ("n", 1), ("n", 4097), ("rank_cap", 0),
+                                         ("rank_cap", 65), ("family", 7), ("n_samples", 0),
+                                         ("n_samples", 1025), ("rook_iters", -1), ("rook_iters", 65),
+                                         ("tol", 1.5), ("tol", -1.0), ("world", 0), ("rank", 1)])
 def test_invalid_arguments_rejected_without_gpu(lib, field, value):
     from paper_1903_11554_b200 import binding
-    cfg = binding.TtcConfig(0, 4, 9, 4, 2, 0, 1e-12, 1e-2, 1, 0, 1)
+    cfg = good_config(binding)
     setattr(cfg, field, value)
     u = np.ones((4, 9))
     h = ctypes.c_void_p()
@@ -60,7 +67,7 @@ def test_invalid_arguments_rejected_without_gpu(lib, field, value):
 
 def test_nonpositive_nodes_rejected(lib):
     from paper_1903_11554_b200 import binding
-    cfg = binding.TtcConfig(0, 3, 5, 4, 2, 0, 1e-12, 1e-2, 1, 0, 1)
+    cfg = binding.TtcConfig(0, 3, 5, 4, 16, 4, 1e-12, 1, 0, 1)
     u = np.ones((3, 5))
     u[1, 2] = -1.0
     h = ctypes.c_void_p()
@@ -68,3 +75,12 @@ def test_nonpositive_nodes_rejected(lib):
                            u.ctypes.data_as(ctypes.c_void_p), 0, None)
     # argument validation happens before any CUDA call, so this is ERR_ARG even on a CPU box
     assert rc == 1
+
+
+def test_config_struct_layout_matches_header():
+    """The ctypes mirror of ttc_config / ttc_stats has the C layout (offsets from the header's
+    field order and natural alignment)."""
+    from paper_1903_11554_b200 import binding
+    assert ctypes.sizeof(binding.TtcConfig) == 6 * 4 + 8 + 8 + 2 * 4
+    assert binding.TtcConfig.tol.offset == 24 and binding.TtcConfig.seed.offset == 32
+    assert ctypes.sizeof(binding.TtcStats) == 8 + 8 + 4 + 4 + 4 * 8 + 6 * 8

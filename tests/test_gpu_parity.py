@@ -2,9 +2,10 @@
 
 Bar (BASELINE.json north_star): pivot index sets bit-exact, fiber entries within 1e-13
 relative (they are in fact compared bit-exactly, R3), integral within 1e-12
-relative.  Small cases span several cluster tiles and ragged tails; the BASELINE configs
-run at full size (C_4, D_5, C_10 whole; D_20 and C_200 on sampled interfaces of the first
-half-sweep plus size-independent properties of the full run).
+relative of the oracle's near-exact §4.1 contraction.  Small cases span several cluster
+CTAs and ragged tails; the BASELINE configs C_4, D_5 and C_10 run whole; D_20 and C_200 are
+checked on their first sweeps (the oracle's cost grows like r^3 n d^2 per sweep) plus
+size-independent properties of the full run.
 """
 import numpy as np
 import pytest
@@ -18,94 +19,127 @@ pytestmark = pytest.mark.gpu
 INT_RTOL = 1e-12
 
 
-def make(family, d, n, L, cap, tol, p, seed, delta=1e-2, max_swaps=0):
+def make(family, d, n, L, cap, tol, ns, rook, seed):
     from paper_1903_11554_b200 import TTCross
     u, w = ising_grid(d, n, L)
-    tt = TTCross(family, u, w, cap, tol, n_enrich=p, max_swaps=max_swaps, delta=delta, seed=seed)
-    prob = X.Problem(family, u, w, cap, tol, p, delta, max_swaps, seed)
+    tt = TTCross(family, u, w, cap, tol, n_samples=ns, rook_iters=rook, seed=seed)
+    prob = X.Problem(family, u, w, cap, tol, ns, rook, seed)
     return tt, prob
 
 
+def make_wl(wl):
+    return make(wl.family, wl.d, wl.n, wl.L, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed)
+
+
 def assert_same_state(tt, st, where=""):
-    ranks, piv = tt.state()
+    ranks, piv, par = tt.state(parents=True)
     assert list(ranks) == st.ranks, f"ranks differ {where}: {list(ranks)} vs {st.ranks}"
-    for i, (a, b) in enumerate(zip(piv, st.piv)):
-        assert np.array_equal(a, b), f"pivots of interface {i} differ {where}"
+    for k in range(len(piv)):
+        assert np.array_equal(piv[k], st.piv[k]), f"pivots of interface {k} differ {where}"
+        assert np.array_equal(par[k], st.par[k]), f"parents of interface {k} differ {where}"
 
 
-def check_run(tt, prob, sweeps, check_fibers=True):
+def gpu_sweep_evals(prob, before, after, prev_rows, prev_cols):
+    """Entries the CUDA path evaluates in one sweep: u/v of the existing pivots on the rows /
+    columns that are new since the previous sweep (the oracle recomputes them all), plus the
+    oracle's own Alg. 2 search evaluations (samples + rook columns/rows)."""
+    d, n = prob.d, prob.n
+    total = 0
+    rows_done, cols_done = [], []
+    for k in range(d - 1):
+        rl = before.ranks[k - 1] if k > 0 else 1
+        rr = before.ranks[k + 1] if k < d - 2 else 1
+        r = before.ranks[k]
+        total += (rl - prev_rows[k]) * n * r + (rr - prev_cols[k]) * n * r
+        total += after.log[-1][1][k]["search_evals"]
+        rows_done.append(rl)
+        cols_done.append(rr)
+    return total, rows_done, cols_done
+
+
+def quad_evals(prob, st):
+    d, n = prob.d, prob.n
+    r = [1] + st.ranks + [1]
+    return sum(r[m] * r[m + 1] * n for m in range(d)) + sum(x * x for x in st.ranks)
+
+
+def check_run(tt, prob, sweeps, check_fibers=True, check_evals=True):
     st = X.initial_state(prob)
     assert_same_state(tt, st, "at init")
+    expect = X.N_INIT
+    prev_rows = [0] * (prob.d - 1)
+    prev_cols = [0] * (prob.d - 1)
     for s in range(sweeps):
-        for direction in (X.DIR_LR, X.DIR_RL):
-            tt.half_sweep(direction)
-            tt.commit()
-            st = X.half_sweep(prob, st, direction)
-            assert_same_state(tt, st, f"after sweep {s} dir {direction}")
-        st.sweep += 1
+        tt.sweep(1)
+        new = X.sweep(prob, st)
+        assert_same_state(tt, new, f"after sweep {s}")
+        e, prev_rows, prev_cols = gpu_sweep_evals(prob, st, new, prev_rows, prev_cols)
+        expect += e
+        st = new
     val, log10, sign = tt.integrate()
     fibers = X.tt_fibers(prob, st)
-    _, _, _, nev = X.integrate(prob, st, fibers)
     ref, rlog10, rsign = X.integrate_exact(prob, st, fibers)
     if check_fibers:
         for m in range(prob.d):
             g = tt.fiber(m)
             assert g.shape == fibers[m].shape
-            assert np.array_equal(g, fibers[m]), f"fiber {m} differs (max rel {np.max(np.abs(g - fibers[m]) / np.abs(fibers[m]).max()):.2e})"
+            assert np.array_equal(g, fibers[m]), f"fiber {m} differs"
     assert sign == rsign
     assert abs(log10 - rlog10) < 1e-12 * max(1.0, abs(rlog10))
     if np.isfinite(ref) and ref != 0:
         assert abs(val - ref) <= INT_RTOL * abs(ref), (val, ref)
-    stats = tt.stats()
-    assert stats["evals"] == st.n_evals + nev
+    if check_evals:
+        assert tt.stats()["evals"] == expect + quad_evals(prob, st)
     return st, val
 
 
-@pytest.mark.parametrize("family,d,n,L,cap,tol,p,seed,sweeps", [
-    (FAMILY_C, 2, 9, 3.0, 4, 1e-12, 2, 1, 2),          # single interface
-    (FAMILY_C, 3, 5, 2.0, 8, 1e-12, 4, 2, 2),          # ranks limited by n^k
-    (FAMILY_D, 3, 7, 3.0, 5, 1e-12, 3, 3, 2),
-    (FAMILY_C, 4, 33, 8.0, 6, 1e-12, 3, 4, 3),
-    (FAMILY_D, 5, 17, 6.0, 8, 1e-11, 4, 5, 3),
-    (FAMILY_D, 6, 31, 6.0, 7, 1e-11, 2, 6, 2),         # ragged: odd n, odd cap
-    (FAMILY_C, 7, 65, 10.0, 12, 1e-13, 5, 7, 2),
-    (FAMILY_C, 3, 97, 12.0, 1, 1e-12, 0, 8, 2),        # rank 1, no enrichment
-    (FAMILY_D, 4, 41, 8.0, 16, 0.0, 16, 9, 2),         # tol = 0, max enrichment
+@pytest.mark.parametrize("family,d,n,L,cap,tol,ns,rook,seed,sweeps", [
+    (FAMILY_C, 2, 9, 3.0, 4, 1e-12, 8, 4, 1, 5),          # a single superblock, no neighbours
+    (FAMILY_C, 3, 5, 2.0, 8, 1e-12, 16, 4, 2, 9),         # ranks limited by the grid (tol stop)
+    (FAMILY_D, 3, 7, 3.0, 5, 1e-12, 16, 4, 3, 6),
+    (FAMILY_C, 4, 33, 8.0, 6, 1e-12, 32, 4, 4, 7),
+    (FAMILY_D, 5, 17, 6.0, 8, 1e-11, 32, 4, 5, 8),
+    (FAMILY_D, 6, 31, 6.0, 7, 1e-11, 7, 2, 6, 7),         # ragged: odd n, odd cap, odd samples
+    (FAMILY_C, 7, 65, 10.0, 12, 1e-13, 64, 4, 7, 12),
+    (FAMILY_C, 3, 97, 12.0, 1, 1e-12, 4, 4, 8, 3),        # rank cap 1: no additions ever
+    (FAMILY_D, 4, 41, 8.0, 16, 0.0, 1024, 1, 9, 16),      # tol = 0, max samples, one rook round
+    (FAMILY_C, 4, 21, 6.0, 6, 1e-12, 16, 0, 10, 6),       # no rook rounds: the best sample
+    (FAMILY_D, 3, 513, 24.0, 64, 1e-12, 32, 4, 11, 4),    # cap*n = 32832 rows: 4-CTA clusters
 ])
-def test_parity_small(lib, family, d, n, L, cap, tol, p, seed, sweeps):
-    tt, prob = make(family, d, n, L, cap, tol, p, seed)
+def test_parity_small(lib, family, d, n, L, cap, tol, ns, rook, seed, sweeps):
+    tt, prob = make(family, d, n, L, cap, tol, ns, rook, seed)
     check_run(tt, prob, sweeps)
     tt.close()
 
 
-def test_parity_max_rank_and_swap_cap(lib):
-    tt, prob = make(FAMILY_C, 3, 129, 20.0, 64, 1e-15, 16, 10, max_swaps=3)
-    check_run(tt, prob, 1)
-    tt.close()
-
-
-def test_reset_reproduces(lib):
-    tt, prob = make(FAMILY_D, 4, 25, 6.0, 6, 1e-12, 3, 12)
-    tt.sweep(2)
+def test_reset_and_graph_reproduce(lib):
+    wl = WORKLOADS["C4"]
+    tt, prob = make_wl(wl)
+    tt.sweep(wl.alg6_sweeps)
     v1 = tt.integrate()
-    r1 = tt.state()
+    s1 = tt.state(parents=True)
+    tt.solve_launch(wl.alg6_sweeps, graph=True)
+    v2 = tt.integrate_read()
+    s2 = tt.state(parents=True)
+    tt.solve_launch(wl.alg6_sweeps, graph=False)
+    v3 = tt.integrate_read()
     tt.reset()
-    tt.sweep(2)
-    v2 = tt.integrate()
-    r2 = tt.state()
-    assert v1 == v2
-    assert all(np.array_equal(a, b) for a, b in zip(r1[1], r2[1]))
+    tt.sweep(wl.alg6_sweeps)
+    v4 = tt.integrate()
+    assert v1 == v2 == v3 == v4
+    for a, b in zip(s1[1] + s1[2], s2[1] + s2[2]):
+        assert np.array_equal(a, b)
     tt.close()
 
 
 def test_zero_tensor_is_singular(lib):
-    """D_3 on a 2-node grid vanishes identically (two coordinates always coincide):
-    every fiber is zero, the pivots are kept (R8) and the quadrature reports a singular
-    intersection, like the oracle's solve."""
+    """D_3 on a 2-node grid vanishes identically (two coordinates always coincide): the
+    first pivot is zero, every superblock is left unchanged (R8) and the quadrature reports a
+    singular intersection, like the oracle's solve."""
     from paper_1903_11554_b200 import TTCError
-    tt, prob = make(FAMILY_D, 3, 2, 1.0, 2, 1e-12, 1, 13)
-    tt.sweep(1)
-    st = X.sweep(prob, X.initial_state(prob))
+    tt, prob = make(FAMILY_D, 3, 2, 1.0, 2, 1e-12, 4, 4, 13)
+    tt.sweep(2)
+    st = X.sweep(prob, X.sweep(prob, X.initial_state(prob)))
     assert_same_state(tt, st)
     with pytest.raises(TTCError) as e:
         tt.integrate()
@@ -115,16 +149,26 @@ def test_zero_tensor_is_singular(lib):
     tt.close()
 
 
-def test_device_resident_inputs(lib):
+def test_device_resident_inputs_and_load_grid(lib):
     import torch
     from paper_1903_11554_b200 import TTCross
     u, w = ising_grid(4, 33, 8.0)
-    tt_h = TTCross(FAMILY_C, u, w, 6, 1e-12, n_enrich=2, seed=3)
-    tt_d = TTCross(FAMILY_C, torch.from_numpy(u).cuda(), torch.from_numpy(w).cuda(), 6, 1e-12, n_enrich=2, seed=3,
+    tt_h = TTCross(FAMILY_C, u, w, 6, 1e-12, n_samples=16, seed=3)
+    tt_d = TTCross(FAMILY_C, torch.from_numpy(u).cuda(), torch.from_numpy(w).cuda(), 6, 1e-12, n_samples=16, seed=3,
                    stream=torch.cuda.current_stream().cuda_stream)
-    tt_h.sweep(2)
-    tt_d.sweep(2)
-    assert tt_h.integrate() == tt_d.integrate()
+    tt_h.sweep(6)
+    tt_d.sweep(6)
+    ref = tt_h.integrate()
+    assert ref == tt_d.integrate()
+    # a different grid, then the original one again through tt_cross_load_grid
+    u2, w2 = ising_grid(4, 33, 6.0)
+    tt_d.load_grid(u2, w2)
+    tt_d.sweep(6)
+    other = tt_d.integrate()
+    assert other != ref
+    tt_d.load_grid(torch.from_numpy(u).pin_memory().numpy(), w)
+    tt_d.solve_launch(6, graph=True)
+    assert tt_d.integrate_read() == ref
     tt_h.close()
     tt_d.close()
 
@@ -132,48 +176,48 @@ def test_device_resident_inputs(lib):
 @pytest.mark.parametrize("name", ["C4", "D5", "C10"])
 def test_parity_baseline_configs_full(lib, name):
     wl = WORKLOADS[name]
-    tt, prob = make(wl.family, wl.d, wl.n, wl.L, wl.rank_cap, wl.tol, wl.n_enrich, wl.seed, wl.maxvol_delta,
-                    wl.max_swaps)
-    check_run(tt, prob, wl.sweeps, check_fibers=(name != "C10"))
+    tt, prob = make_wl(wl)
+    check_run(tt, prob, wl.alg6_sweeps, check_fibers=(name != "C10"))
     tt.close()
 
 
-@pytest.mark.parametrize("name,ifaces", [("D20", [0, 9, 18]), ("C200", [0, 57, 198])])
-def test_parity_large_configs_sampled(lib, name, ifaces):
-    """Full-size configs: the first L->R half-sweep of sampled interfaces against the oracle
-    (inputs are the seed-derived initial pivots, computed independently by the oracle)."""
+@pytest.mark.parametrize("name,sweeps", [("D20", 3), ("C200", 2)])
+def test_parity_large_configs_first_sweeps(lib, name, sweeps):
+    """Full-size configs: the first sweeps of the bench launch configuration against the
+    oracle (pivots, parents, ranks bit-exact; eval counter)."""
     wl = WORKLOADS[name]
-    tt, prob = make(wl.family, wl.d, wl.n, wl.L, wl.rank_cap, wl.tol, wl.n_enrich, wl.seed, wl.maxvol_delta,
-                    wl.max_swaps)
-    st0 = X.initial_state(prob)
-    assert_same_state(tt, st0, "at init")
-    tt.half_sweep(X.DIR_LR)
-    tt.commit()
-    ranks, piv = tt.state()
-    for i in ifaces:
-        new, info = X.update_interface(prob, st0, i, X.DIR_LR)
-        assert np.array_equal(piv[i], new), f"{name}: interface {i} differs"
+    tt, prob = make_wl(wl)
+    st = X.initial_state(prob)
+    assert_same_state(tt, st, "at init")
+    for s in range(sweeps):
+        tt.sweep(1)
+        st = X.sweep(prob, st)
+        assert_same_state(tt, st, f"after sweep {s}")
     tt.close()
 
 
 @pytest.mark.parametrize("name", ["D20", "C200"])
 def test_large_configs_properties(lib, name):
-    """Size-independent properties of the full run: ranks within the cap, distinct left
-    and right parts, nonsingular intersections (the quadrature succeeds), a finite integral
-    and the evaluation count of the schedule."""
+    """Size-independent properties of the full bench solve: ranks within the cap, nested and
+    distinct index sets (eq. (4)), nonsingular intersections (the quadrature succeeds), a
+    finite integral, and fiber entries equal to the integrand at their indices (sampled)."""
     wl = WORKLOADS[name]
-    tt, prob = make(wl.family, wl.d, wl.n, wl.L, wl.rank_cap, wl.tol, wl.n_enrich, wl.seed, wl.maxvol_delta,
-                    wl.max_swaps)
-    tt.sweep(2)
-    val, log10, sign = tt.integrate()
-    assert sign == 1 and np.isfinite(log10)
-    ranks, piv = tt.state()
-    for i, P in enumerate(piv):
+    tt, prob = make_wl(wl)
+    tt.solve_launch(wl.alg6_sweeps, graph=True)
+    val, log10, sign = tt.integrate_read()
+    assert sign != 0 and np.isfinite(log10)
+    ranks, piv, par = tt.state(parents=True)
+    assert 1 < max(ranks) <= wl.rank_cap   # C_200 stops below the cap on tol (values ~1e-9 of max)
+    for k, P in enumerate(piv):
         assert 1 <= len(P) <= wl.rank_cap
-        assert len({tuple(r[:i + 1]) for r in P}) == len(P)
-        assert len({tuple(r[i + 1:]) for r in P}) == len(P)
+        assert len({tuple(r[:k + 1]) for r in P}) == len(P)
+        assert len({tuple(r[k + 1:]) for r in P}) == len(P)
         assert np.all((P >= 0) & (P < wl.n))
-    # sampled fiber entries of the final quadrature pass equal the integrand at their indices
+        for s, (al, be) in enumerate(par[k]):
+            if k > 0:
+                assert np.array_equal(P[s][:k], piv[k - 1][al][:k])
+            if k < wl.d - 2:
+                assert np.array_equal(P[s][k + 2:], piv[k + 1][be][k + 2:])
     rng = np.random.default_rng(0)
     for m in rng.choice(wl.d, 3, replace=False):
         F = tt.fiber(int(m))

@@ -1,11 +1,11 @@
 """Pins of oracle/cross.py against things other than itself (CPU only).
 
-What fixes each expectation: the published splitmix64 test vector; an explicit list-based
-Fisher-Yates; nestedness (eq. (4)); numpy.linalg inverses / determinants and
-explicit Schur complements (independent arithmetic) for the cross and Alg. 1; exhaustive
-swap search for maxvol local optimality; Theorem 1 (interpolation on nested crosses) and
-Theorem 2 (exact recovery of exact-rank tensors); the TT formula eq. (3) evaluated entry by
-entry against the full-grid sum for the §4.1 contraction.
+What fixes each expectation: the published splitmix64 test vector; explicit loops for the
+first pivot; nestedness (eq. (4)); numpy.linalg solves of the cross formula
+eq. (1) (independent arithmetic) for the error of every added pivot and for the rook
+condition eq. (2); Theorem 1 (interpolation on nested crosses) and Theorem 2 (exact
+recovery of exact-rank tensors); the TT formula eq. (3) evaluated entry by entry against
+the full-grid sum for the §4.1 contraction; closed forms / brute force for the integral.
 """
 import itertools
 
@@ -17,9 +17,9 @@ from oracle import integrand as ig
 from workloads import FAMILY_C, FAMILY_D, ising_grid
 
 
-def make_problem(fam, d, n, L, cap, tol=1e-12, p=4, seed=7, delta=1e-2):
+def make_problem(fam, d, n, L, cap, tol=1e-12, ns=16, rook=4, seed=7):
     u, w = ising_grid(d, n, L)
-    return X.Problem(fam, u, w, cap, tol, p, delta, 0, seed)
+    return X.Problem(fam, u, w, cap, tol, ns, rook, seed)
 
 
 # ---------------------------------------------------------------- counter-based RNG
@@ -30,139 +30,141 @@ def test_splitmix64_reference_vector():
     assert [X.splitmix64(0, c) for c in range(4)] == ref
 
 
-def test_partial_fisher_yates_matches_explicit_shuffle():
-    for M, r in [(10, 10), (257, 16), (4112, 16), (5, 1)]:
-        got = X.partial_fisher_yates(99, 0, 5, 2, M, r)
-        arr = list(range(M))
-        for s in range(r):
-            j = s + X.splitmix64(99, X.draw_ctr(0, 5, 2, s)) % (M - s)
-            arr[s], arr[j] = arr[j], arr[s]
-        assert got == arr[:r]
-        assert len(set(got)) == r
-
-
-# ---------------------------------------------------------------- initial pivots
-@pytest.mark.parametrize("d,n,cap", [(2, 5, 8), (4, 9, 8), (5, 7, 16), (6, 3, 4)])
-def test_initial_state_nested_distinct(d, n, cap):
-    prob = make_problem(FAMILY_C, d, n, 4.0, cap)
+# ---------------------------------------------------------------- first pivot
+@pytest.mark.parametrize("fam,d,n", [(FAMILY_C, 2, 5), (FAMILY_D, 4, 9), (FAMILY_D, 7, 33)])
+def test_initial_state_is_argmax_of_seeded_samples(fam, d, n):
+    prob = make_problem(fam, d, n, 4.0, 8)
     st = X.initial_state(prob)
-    assert st.ranks == [min(cap, n ** (i + 1), n ** (d - 1 - i)) for i in range(d - 1)]
-    for i, P in enumerate(st.piv):
-        lefts = {tuple(r[:i + 1]) for r in P}
-        rights = {tuple(r[i + 1:]) for r in P}
-        assert len(lefts) == len(P) == len(rights)
-        assert np.all((P >= 0) & (P < n))
-        if i > 0:  # I_{<=i} subset of I_{<=i-1} x [n]   (eq. (4))
-            prev = {tuple(r[:i]) for r in st.piv[i - 1]}
-            assert all(t[:i] in prev for t in lefts)
-        if i < d - 2:  # I_{>i} subset of [n] x I_{>i+1}
-            nxt = {tuple(r[i + 2:]) for r in st.piv[i + 1]}
-            assert all(t[1:] in nxt for t in rights)
+    best, bv = None, -1.0
+    for q in range(X.N_INIT):
+        t = [X.splitmix64(prob.seed, ((0 * (d + 1) + 0) << 20) + q * d + j) % n for j in range(d)]
+        v = abs(ig.entries(fam, prob.u, np.array([t]))[0])
+        if v > bv:
+            best, bv = t, v
+    assert st.ranks == [1] * (d - 1)
+    for k in range(d - 1):
+        assert list(st.piv[k][0]) == best
+        assert list(st.par[k][0]) == [0, 0]
 
 
-# ---------------------------------------------------------------- fibers
-def test_fiber_indexing_against_explicit_loop():
-    prob = make_problem(FAMILY_D, 5, 7, 3.0, 4)
+# ---------------------------------------------------------------- superblock update
+def superblock_dense(prob, st, k):
+    sb = X.Superblock(prob, st, k)
+    xs, ys = np.meshgrid(np.arange(sb.R), np.arange(sb.C), indexing="ij")
+    return sb, prob.A(sb.tuples(xs, ys))
+
+
+def cross_error(Asb, I, J):
+    """E = A - A(:, J) A(I, J)^{-1} A(I, :)  (eq. (1)), via numpy.linalg.solve."""
+    if not I:
+        return Asb.copy()
+    return Asb - Asb[:, J] @ np.linalg.solve(Asb[np.ix_(I, J)], Asb[I, :])
+
+
+@pytest.mark.parametrize("fam,d,n,cap,rook", [(FAMILY_C, 3, 9, 6, 4), (FAMILY_D, 4, 7, 5, 4),
+                                              (FAMILY_D, 3, 11, 8, 1), (FAMILY_C, 2, 13, 6, 0)])
+def test_added_pivots_follow_alg2(fam, d, n, cap, rook):
+    """Every added pivot's value is the cross error E(x*, y*) of the cross before it (eq. (1),
+    computed with numpy.linalg, not the oracle's ACA updates); a converged rook search ends
+    on an entry that dominates its row and column of |E| (eq. (2)); pivots are never
+    removed; the tolerance test uses the largest |A| at the pivots."""
+    prob = make_problem(fam, d, n, 3.0, cap, rook=rook)
     st = X.initial_state(prob)
-    for m in range(5):
-        Lt = st.piv[m - 1] if m > 0 else None
-        Rt = st.piv[m] if m < 4 else None
-        F = X.fiber(prob, Lt, m, Rt)
-        rx = 1 if Lt is None else len(Lt)
-        ry = 1 if Rt is None else len(Rt)
-        assert F.shape == (rx, ry, 7)
-        for al in range(rx):
-            for be in range(ry):
-                for a in range(7):
-                    t = (list(Lt[al][:m]) if m > 0 else []) + [a] + (list(Rt[be][m + 1:]) if m < 4 else [])
-                    assert F[al, be, a] == ig.entries(FAMILY_D, prob.u, np.array([t]))[0]
-        Mlr = X.fiber_matrix(F, X.DIR_LR)
-        Mrl = X.fiber_matrix(F, X.DIR_RL)
-        assert Mlr[2 * 7 + 3 if rx > 2 else 3, 0] == F[2 if rx > 2 else 0, 0, 3]
-        assert Mrl[(ry - 1) * 7 + 5, rx - 1] == F[rx - 1, ry - 1, 5]
+    for sweep in range(7):
+        new = X.sweep(prob, st)
+        for k in range(d - 1):
+            info = new.log[-1][1][k]
+            sb, Asb = superblock_dense(prob, st, k)
+            scale = np.max(np.abs(Asb))
+            for add in info["adds"]:
+                E = cross_error(Asb, add["xs_before"], add["ys_before"])
+                E[add["xs_before"], :] = 0.0
+                E[:, add["ys_before"]] = 0.0
+                x, y = add["x"], add["y"]
+                assert abs(add["pivot"] - E[x, y]) <= 1e-9 * scale
+                if add["converged"]:
+                    assert abs(E[x, y]) >= np.max(np.abs(E[:, y])) - 1e-9 * scale
+                    assert abs(E[x, y]) >= np.max(np.abs(E[x, :])) - 1e-9 * scale
+            assert np.array_equal(new.piv[k][:st.ranks[k]], st.piv[k])   # append-only (Alg. 6 line 4)
+            assert new.ranks[k] <= cap
+        st = new
 
 
-# ---------------------------------------------------------------- rank-revealing cross
-def test_rrcross_exact_rank_and_B():
-    rng = np.random.default_rng(0)
-    for (m, c, k) in [(40, 10, 3), (100, 20, 7), (12, 12, 12)]:
-        F = rng.standard_normal((m, k)) @ rng.standard_normal((k, c))
-        I, J, B = X.rrcross(F, 1e-10, 64)
-        assert len(I) == k and len(set(I)) == k and len(set(J)) == k
-        Bref = F[:, J] @ np.linalg.inv(F[np.ix_(I, J)])
-        assert np.max(np.abs(B - Bref)) < 1e-9 * max(1, np.max(np.abs(Bref)))
-        assert np.array_equal(B[I, :], np.eye(k))  # exact identity on the pivot rows
-        # cap is honoured
-        I2, J2, _ = X.rrcross(F, 1e-10, 2)
-        assert len(I2) == 2 and I2 == I[:2] and J2 == J[:2]
-    I, J, B = X.rrcross(np.zeros((5, 3)), 1e-12, 4)
-    assert I == [] and J == []
+def test_aca_form_equals_cross_formula():
+    """The u/v factors rebuilt by the LU init reproduce A(:, J) A(I, J)^{-1} A(I, :)."""
+    prob = make_problem(FAMILY_D, 4, 9, 3.0, 6)
+    st = X.initial_state(prob)
+    for _ in range(5):
+        st = X.sweep(prob, st)
+    k = 1
+    sb, Asb = superblock_dense(prob, st, k)
+    n = prob.n
+    I = list(st.par[k][:, 0] * n + st.piv[k][:, k])
+    J = list(st.par[k][:, 1] * n + st.piv[k][:, k + 1])
+    approx = Asb[:, J] @ np.linalg.solve(Asb[np.ix_(I, J)], Asb[I, :])
+    # interpolation property of the matrix cross: exact on its rows and columns
+    assert np.max(np.abs(approx[I, :] - Asb[I, :])) <= 1e-10 * np.max(np.abs(Asb))
+    assert np.max(np.abs(approx[:, J] - Asb[:, J])) <= 1e-10 * np.max(np.abs(Asb))
 
 
-def test_rrcross_is_complete_pivoting():
-    """Pivot s+1 is the max |Schur complement| entry after pivots 1..s (explicit formula)."""
-    rng = np.random.default_rng(1)
-    F = rng.standard_normal((30, 8)) * np.exp(rng.standard_normal((30, 1)))
-    I, J, _ = X.rrcross(F, 1e-14, 8)
-    for s in range(len(I)):
-        if s == 0:
-            Rs = F
-        else:
-            Is, Js = I[:s], J[:s]
-            Rs = F - F[:, Js] @ np.linalg.solve(F[np.ix_(Is, Js)], F[Is, :])
-            Rs[Is, :] = 0
-            Rs[:, Js] = 0
-        assert abs(Rs[I[s], J[s]]) >= np.max(np.abs(Rs)) * (1 - 1e-9)
+def test_tolerance_stops_exact_rank_superblock():
+    """A rank-2 tensor: additions stop once the error is below tol (Alg. 2 with tol)."""
+    u, w = ising_grid(4, 7, 2.0)
+    prob = ExactRankProblem(FAMILY_C, u, w, 8, 1e-11, 16, 4, 5)
+    st = X.initial_state(prob)
+    for _ in range(4):
+        st = X.sweep(prob, st)
+    assert max(st.ranks) == 2
+    for k in range(3):
+        assert st.log[-1][1][k]["stop"] in ("tol", "cap", "n_add")
 
 
-# ---------------------------------------------------------------- maxvol (Alg. 1)
-def test_maxvol_paper_toy_example():
-    # A = [[1],[3]], J = {0}, I = {0}: B = [1; 3] -> swap to I = {1}, volume x3
-    F = np.array([[1.0], [3.0]])
-    B = F / F[0, 0]
-    I, B2, nsw = X.maxvol(B, [0], 1e-2, 10)
-    assert I == [1] and nsw == 1
-    assert np.allclose(B2, F / F[1, 0])
+@pytest.mark.parametrize("d,n,cap", [(3, 5, 8), (5, 7, 6), (6, 4, 5)])
+def test_sweeps_keep_nestedness_and_distinctness(d, n, cap):
+    prob = make_problem(FAMILY_D, d, n, 3.0, cap)
+    st = X.initial_state(prob)
+    for _ in range(6):
+        st = X.sweep(prob, st)
+        for k, P in enumerate(st.piv):
+            assert len({tuple(r[:k + 1]) for r in P}) == len(P) == len({tuple(r[k + 1:]) for r in P})
+            assert np.all((P >= 0) & (P < n))
+            for s, (al, be) in enumerate(st.par[k]):
+                if k > 0:   # I_{<=k} subset of I_{<=k-1} x [n]   (eq. (4)), via the parent slot
+                    assert np.array_equal(P[s][:k], st.piv[k - 1][al][:k])
+                if k < d - 2:   # I_{>k} subset of [n] x I_{>k+1}
+                    assert np.array_equal(P[s][k + 2:], st.piv[k + 1][be][k + 2:])
 
 
-def test_maxvol_volume_growth_and_bound():
-    rng = np.random.default_rng(2)
-    for trial in range(20):
-        m, r = rng.integers(8, 60), rng.integers(1, 7)
-        F = rng.standard_normal((m, r))
-        I0 = list(rng.choice(m, r, replace=False))
-        if abs(np.linalg.det(F[I0])) < 1e-6:
-            continue
-        B0 = F @ np.linalg.inv(F[I0])
-        I = list(I0)
-        vol = abs(np.linalg.det(F[I]))
-        for step in range(1, 200):
-            Inew, Bnew, nsw = X.maxvol(B0, I0, 1e-2, step)
-            if nsw < step:  # converged
-                Bref = F @ np.linalg.inv(F[Inew])
-                assert np.max(np.abs(Bref)) <= 1 + 1e-2 + 1e-9
-                assert np.max(np.abs(Bnew - Bref)) < 1e-9
-                break
-            v = abs(np.linalg.det(F[Inew]))
-            assert v > vol * (1 + 1e-2) * (1 - 1e-9)  # every swap grows the volume (Alg. 1)
-            vol = v
+def test_parallel_partition_equals_all_at_once():
+    """Alg. 6: updating disjoint superblock chunks separately and merging equals one sweep
+    over all superblocks (each superblock only reads the previous state)."""
+    prob = make_problem(FAMILY_C, 7, 9, 4.0, 5)
+    st = X.sweep(prob, X.initial_state(prob))
+    full = X.sweep(prob, st)
+    merged = st.copy()
+    for chunk in ([0, 1], [2, 3, 4], [5]):
+        part = X.sweep(prob, st, chunk)
+        for i in chunk:
+            merged.piv[i], merged.par[i] = part.piv[i], part.par[i]
+    for a, b in zip(full.piv, merged.piv):
+        assert np.array_equal(a, b)
 
 
-def test_maxvol_local_optimality_exhaustive():
-    rng = np.random.default_rng(3)
-    for trial in range(30):
-        m, r = 9, 2
-        F = rng.standard_normal((m, r))
-        I, J, B = X.rrcross(F, 1e-14, r)
-        I, B, nsw = X.maxvol(B, I, 1e-2, 100)
-        v = abs(np.linalg.det(F[I]))
-        for j in range(r):
-            for i in range(m):
-                if i in I:
-                    continue
-                I2 = list(I)
-                I2[j] = i
-                assert abs(np.linalg.det(F[I2])) <= v * (1 + 1e-2) * (1 + 1e-12)
+def test_eval_count_formula():
+    """Entries evaluated per superblock = LU init r(R + C) + per addition: samples +
+    (R + C) per rook round + the final column/row when the rook search did not end on them
+    (the GPU path's counter is compared with the same per-sweep totals)."""
+    prob = make_problem(FAMILY_C, 5, 9, 3.0, 7, ns=8, rook=2)
+    st = X.sweep(prob, X.sweep(prob, X.initial_state(prob)))
+    new = X.sweep(prob, st)
+    total = 0
+    for k in range(4):
+        info = new.log[-1][1][k]
+        R = (st.ranks[k - 1] if k > 0 else 1) * 9
+        C = (st.ranks[k + 1] if k < 3 else 1) * 9
+        assert info["evals"] >= st.ranks[k] * (R + C) + info["added"] * prob.n_samples
+        total += info["evals"]
+    assert new.n_evals - st.n_evals == total
 
 
 # ---------------------------------------------------------------- TT formula / quadrature
@@ -186,11 +188,15 @@ class AsymProblem(X.Problem):
         return 1.0 / (1.0 + np.sum(U * (1.0 + np.arange(self.d)), axis=-1))
 
 
-def test_interpolation_theorem1_on_nested_init():
-    """Theorem 1: nested crosses interpolate their fibers."""
+def test_interpolation_theorem1_after_parallel_sweeps():
+    """Theorem 1: the crosses produced by dimension-parallel sweeps
+    stay nested, so eq. (3) interpolates every fiber entry A(I_{<=m-1}, i_m, I_{>m})."""
     u, w = ising_grid(4, 6, 3.0)
-    prob = AsymProblem(FAMILY_C, u, w, 3, 1e-12, 4, 1e-2, 0, 7)
-    st = X.initial_state(prob)  # nested by construction
+    prob = AsymProblem(FAMILY_C, u, w, 4, 1e-12, 8, 4, 7)
+    st = X.initial_state(prob)
+    for _ in range(4):
+        st = X.sweep(prob, st)
+    assert max(st.ranks) > 1
     for m in range(4):
         Lt = st.piv[m - 1] if m > 0 else np.zeros((1, 4), np.int64)
         Rt = st.piv[m] if m < 3 else np.zeros((1, 4), np.int64)
@@ -215,7 +221,8 @@ def test_integrate_equals_full_sum_of_tt_reconstruction():
     """§4.1 (lines 689-693): the (2d-1)-matrix product equals the quadrature of A~."""
     prob = make_problem(FAMILY_D, 3, 6, 3.0, 4)
     st = X.initial_state(prob)
-    st = X.sweep(prob, st)
+    for _ in range(3):
+        st = X.sweep(prob, st)
     val, log10, sign, _ = X.integrate(prob, st)
     ref = brute_tt_integral(prob, st)
     assert abs(val - ref) <= 1e-11 * abs(ref)
@@ -232,10 +239,11 @@ class ExactRankProblem(X.Problem):
 def test_exact_recovery_theorem2():
     """Theorem 2 (lines 344-350): exact-rank tensors are recovered exactly."""
     u, w = ising_grid(4, 7, 2.0)
-    prob = ExactRankProblem(FAMILY_C, u, w, 4, 1e-13, 4, 1e-2, 0, 5)
+    prob = ExactRankProblem(FAMILY_C, u, w, 4, 1e-11, 16, 4, 5)
     st = X.initial_state(prob)
-    st = X.sweep(prob, st)
-    assert max(st.ranks) <= 2  # truncation finds the exact rank
+    for _ in range(4):
+        st = X.sweep(prob, st)
+    assert max(st.ranks) == 2  # additions stop at the exact rank
     val, *_ = X.integrate(prob, st)
     d, n = 4, 7
     tot = 0.0
@@ -245,57 +253,21 @@ def test_exact_recovery_theorem2():
     assert abs(val - tot * ig.prefactor(d)) <= 1e-12 * abs(val)
 
 
-def test_half_sweep_invariants():
-    prob = make_problem(FAMILY_D, 5, 17, 6.0, 6, tol=1e-11, p=3)
-    st = X.initial_state(prob)
-    for s in range(2):
-        for direction in (X.DIR_LR, X.DIR_RL):
-            new = X.half_sweep(prob, st, direction)
-            for i, P in enumerate(new.piv):
-                assert 1 <= len(P) <= prob.rank_cap
-                assert len({tuple(r[:i + 1]) for r in P}) == len(P)
-                assert len({tuple(r[i + 1:]) for r in P}) == len(P)
-                M = X.intersection(prob, new, i)
-                assert abs(np.linalg.det(M)) > 0
-                if direction == X.DIR_LR and i > 0:
-                    # new left parts come from the OLD I_{<=i-1} x [n]   (§3.4 relaxation)
-                    old = {tuple(r[:i]) for r in st.piv[i - 1]}
-                    assert all(tuple(r[:i]) in old for r in P)
-                if direction == X.DIR_RL and i < prob.d - 2:
-                    old = {tuple(r[i + 2:]) for r in st.piv[i + 1]}
-                    assert all(tuple(r[i + 2:]) in old for r in P)
-            st = new
-        st.sweep += 1
-
-
-def test_parallel_partition_equals_all_at_once():
-    """Alg. 6: updating disjoint interface chunks separately and merging equals one
-    half-sweep over all interfaces (each interface only reads the previous state)."""
-    prob = make_problem(FAMILY_C, 7, 9, 4.0, 5)
-    st = X.initial_state(prob)
-    full = X.half_sweep(prob, st, X.DIR_LR)
-    merged = st.copy()
-    for chunk in ([0, 1], [2, 3, 4], [5]):
-        part = X.half_sweep(prob, st, X.DIR_LR, chunk)
-        for i in chunk:
-            merged.piv[i] = part.piv[i]
-    for a, b in zip(full.piv, merged.piv):
-        assert np.array_equal(a, b)
-
-
 def test_c4_converges_toward_brute_force():
     """Sanity of the whole pipeline: C_4 at rank cap 16 approaches the full-grid sum."""
-    prob = make_problem(FAMILY_C, 4, 33, 8.0, 16, tol=1e-13)
-    st, val, _ = X.run(prob, 4)
+    prob = make_problem(FAMILY_C, 4, 33, 8.0, 20, tol=1e-13, ns=32)
+    st, val, _ = X.run(prob, 20)
     ref = ig.brute_force(FAMILY_C, prob.u, prob.w)
-    assert abs(val - ref) < 1e-6 * ref
+    assert abs(val - ref) < 1e-7 * ref
 
 
 def test_integrate_exact_agrees_with_fp64_when_well_conditioned():
     """R9: the near-exact contraction equals the fp64 one to rounding on a well-conditioned
     cross, and equals the full-grid sum of the TT reconstruction (eq. (3))."""
     prob = make_problem(FAMILY_D, 3, 6, 3.0, 4)
-    st = X.sweep(prob, X.initial_state(prob))
+    st = X.initial_state(prob)
+    for _ in range(3):
+        st = X.sweep(prob, st)
     v64, l64, s64, _ = X.integrate(prob, st)
     vex, lex, sex = X.integrate_exact(prob, st)
     assert s64 == sex and abs(v64 - vex) <= 1e-13 * abs(vex)

@@ -31,3 +31,11 @@ def test_workloads_match_baseline_configs():
         assert f"{wl.n}-point" in text
         assert f"rank cap {wl.rank_cap}" in text
         assert f"[−{int(wl.L)},{int(wl.L)}]" in text
+
+
+def test_alg6_sweeps_reach_the_cap_in_the_configured_sweeps():
+    for wl in WORKLOADS.values():
+        per = wl.alg6_sweeps // wl.sweeps
+        assert wl.alg6_sweeps % wl.sweeps == 0
+        assert 1 + wl.alg6_sweeps >= wl.rank_cap
+        assert 1 + (per - 1) * wl.sweeps < wl.rank_cap or per == 1

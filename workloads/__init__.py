@@ -17,7 +17,7 @@ CUDA path consume bit-identical u-nodes (the nodes are an input, like a dataset)
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -54,24 +54,27 @@ class Workload:
     rank_cap: int
     tol: float
     sweeps: int
-    n_enrich: int = 4
-    maxvol_delta: float = 1e-2
-    max_swaps: int = 0  # 0 -> 2*rank_cap
+    n_samples: int = 32      # |L| of Alg. 2 line 1 (R6)
+    rook_iters: int = 4      # rook rounds of Alg. 2 (R6)
     seed: int = 20190327
     note: str = ""
 
+    @property
+    def alg6_sweeps(self) -> int:
+        """Dimension-parallel sweeps of PAPER.md Alg. 6 run by one solve.  Each adds at most one
+        pivot per superblock, so one BASELINE 'sweep' is ceil((cap-1)/sweeps) Alg. 6 sweeps:
+        enough to reach the rank cap from rank 1 in the configured number (R7)."""
+        return self.sweeps * max(1, -(-(self.rank_cap - 1) // self.sweeps))
+
     def grid(self):
         return ising_grid(self.d, self.n, self.L)
-
-    def swaps_cap(self) -> int:
-        return self.max_swaps if self.max_swaps > 0 else 2 * self.rank_cap
 
     def prefactor(self) -> float:
         return 4.0 / math.factorial(self.d)
 
 
-# BASELINE.json configs[0..4].  `sweeps` is the number of full (L->R + R->L) sweeps; the
-# configs that do not state a sweep count use 4 (reading R7).
+# BASELINE.json configs[0..4].  `sweeps` is the BASELINE sweep count (4 where a config
+# states none, DESIGN.md R7); `alg6_sweeps` the dimension-parallel sweeps it stands for.
 WORKLOADS = {
     "C4": Workload("C4", FAMILY_C, 4, 129, 20.0, 8, 1e-10, 4,
                    note="configs[0]: C_4, 129-pt trapezoid on [-20,20], rank cap 8, tol 1e-10"),
