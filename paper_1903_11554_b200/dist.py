@@ -31,6 +31,37 @@ def owned_interfaces(d: int, rank: int, world: int):
     return kb, ke, chunk
 
 
+def record_stride(d: int, cap: int) -> int:
+    """int32 per pivot record: [r, PIV[cap][d], PAR[cap][2]] (include/ttcross.h)."""
+    return 1 + cap * d + 2 * cap
+
+
+def pack_records(piv, par, d: int, cap: int, nrec: int):
+    """Host encoding of pivot sets in the exchange-buffer layout (int32, -1 padded)."""
+    rs = record_stride(d, cap)
+    out = torch.full((nrec * rs,), -1, dtype=torch.int32)
+    for k, (P, Q) in enumerate(zip(piv, par)):
+        r = len(P)
+        base = k * rs
+        out[base] = r
+        out[base + 1: base + 1 + r * d] = torch.as_tensor(P, dtype=torch.int32).reshape(-1)
+        out[base + 1 + cap * d: base + 1 + cap * d + 2 * r] = torch.as_tensor(Q, dtype=torch.int32).reshape(-1)
+    return out
+
+
+def unpack_records(buf, d: int, cap: int, n_interfaces: int):
+    """Inverse of pack_records: ([PIV[k] (r_k, d)], [PAR[k] (r_k, 2)]) as int64 tensors."""
+    rs = record_stride(d, cap)
+    buf = torch.as_tensor(buf).to(torch.int64).cpu()
+    piv, par = [], []
+    for k in range(n_interfaces):
+        base = k * rs
+        r = int(buf[base])
+        piv.append(buf[base + 1: base + 1 + r * d].reshape(r, d).clone())
+        par.append(buf[base + 1 + cap * d: base + 1 + cap * d + 2 * r].reshape(r, 2).clone())
+    return piv, par
+
+
 def allgather_slices(buf: torch.Tensor, per_rank: int, group=None):
     """In-place all-gather: rank p's elements buf[p*per_rank:(p+1)*per_rank] are copied to
     every rank.  ``buf`` must hold world*per_rank elements (1-D)."""
