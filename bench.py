@@ -133,13 +133,8 @@ def roofline(kt, stats, family, peaks, peak_src):
     avg_s = ms / max(1, launches) / 1e3
     out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
     fpe = FLOPS_PER_ENTRY[family]
-    if name in ("k_sb_extend_rows", "k_sb_extend_cols"):
-        # the two extension kernels split the entries about evenly; report their mean
-        l2 = kt["k_sb_extend_rows"][0] + kt["k_sb_extend_cols"][0]
-        ms2 = kt["k_sb_extend_rows"][1] + kt["k_sb_extend_cols"][1]
-        avg_s = ms2 / max(1, l2) / 1e3
-        ent, upd = stats["ext_entries"] / max(1, l2), stats["ext_updates"] / max(1, l2)
-        out.update({"kernel": "k_sb_extend_rows+cols", "avg_us": avg_s * 1e6, "launches": l2})
+    if name == "k_sb_extend":
+        ent, upd = stats["ext_entries"] / max(1, launches), stats["ext_updates"] / max(1, launches)
     elif name == "k_greedy":
         ent = (stats["sb_entries"] - stats["ext_entries"]) / max(1, launches)
         upd = (stats["sb_updates"] - stats["ext_updates"]) / max(1, launches)

@@ -71,11 +71,11 @@ typedef struct ttc_stats {
   double  ms_quad;         /* device time: quadrature contraction kernels                  */
   double  ms_other;        /* device time: init kernels                                    */
   int64_t fiber_entries;   /* entries written by k_fiber (quadrature fibers)               */
-  int64_t sb_entries;      /* superblock entries evaluated by k_sb_extend_* and k_greedy   */
+  int64_t sb_entries;      /* superblock entries evaluated by k_sb_extend and k_greedy     */
   int64_t sb_updates;      /* multiply-subtract terms u_t(x) v_t(y) of those kernels        */
   int64_t rook_steps;      /* column+row rounds of the rook searches                        */
-  int64_t ext_entries;     /* superblock entries evaluated by k_sb_extend_* only            */
-  int64_t ext_updates;     /* multiply-subtract terms of k_sb_extend_* only                 */
+  int64_t ext_entries;     /* superblock entries evaluated by k_sb_extend only              */
+  int64_t ext_updates;     /* multiply-subtract terms of k_sb_extend only                   */
 } ttc_stats;
 
 /*
@@ -189,10 +189,10 @@ int tt_cross_get_fiber(ttc_ctx* ctx, int32_t mode, double* out, int64_t capacity
 int tt_cross_get_stats(ttc_ctx* ctx, ttc_stats* out);
 
 /* tt_cross_get_kernel_time -- per-kernel launch count and accumulated device time (ms,
- * timing enabled) since the last reset, for kernel id kid in [0, 17): 0 k_prep_nodes,
- * 1 k_init_pivot, 2 k_init_records, 3 k_sb_sides, 4 k_sb_cx, 5 k_sb_extend_rows,
- * 6 k_sb_extend_cols, 7 k_greedy, 8 k_frozen_sides, 9 k_frozen_q, 10 k_frozen_lr,
- * 11 k_fiber, 12 k_wsum, 13 k_intersection, 14 k_solve, 15 k_chain, 16 k_finish.
+ * timing enabled) since the last reset, for kernel id kid in [0, 15): 0 k_prep_nodes,
+ * 1 k_init_pivot, 2 k_init_records, 3 k_sb_tables, 4 k_sb_extend, 5 k_greedy,
+ * 6 k_frozen_sides, 7 k_frozen_q, 8 k_frozen_lr, 9 k_fiber, 10 k_wsum, 11 k_intersection,
+ * 12 k_solve, 13 k_chain, 14 k_finish.
  * *name is a static string.  Errors: TTC_ERR_ARG for kid out of range. */
 int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64_t* launches, double* ms);
 

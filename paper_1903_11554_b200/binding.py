@@ -28,7 +28,7 @@ EXPORTS = [
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
     "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info",
 ]
-N_KERNELS = 17
+N_KERNELS = 15
 
 
 class TtcConfig(ctypes.Structure):

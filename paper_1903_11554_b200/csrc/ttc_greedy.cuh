@@ -7,10 +7,10 @@
 // incomplete-LU form A~(x, y) = sum_t u_t(x) v_t(y) (oracle/cross.py).
 //
 //   k_init_pivot / k_init_records : the rank-1 start (first argmax |A| over seeded samples)
-//   k_sb_sides / k_sb_cx          : factor tables of the superblock entries for the rows /
+//   k_sb_tables                   : factor tables of the superblock entries for the rows /
 //                                   columns that are new this sweep (the frozen left/right
 //                                   pivot coordinates, staged once per sweep)
-//   k_sb_extend_rows / _cols      : u_s(x) / v_s(y) of the existing pivots on the new rows /
+//   k_sb_extend                   : u_s(x) / v_s(y) of the existing pivots on the new rows /
 //                                   columns -- the batched fiber evaluation of the sweep
 //   k_greedy                      : one thread-block cluster per superblock: random samples
 //                                   (Alg. 2 line 1), rook search (lines 2-5), append the new
@@ -28,7 +28,6 @@ namespace cg = cooperative_groups;
 namespace ttc {
 
 #define N_INIT 64
-#define GREEDY_THREADS 512
 #define TTC_MAX_SAMPLES 1024
 
 // ---------------------------------------------------------------------------------------
@@ -58,16 +57,18 @@ __device__ double init_entry(const DevCtx& c, int q) {
 
 // one block of N_INIT threads: t0 = first argmax |A| over the seeded samples -> t0buf[d]
 __global__ void __launch_bounds__(N_INIT) k_init_pivot(DevCtx c, int* t0buf) {
-  __shared__ double sv[N_INIT];
+  __shared__ double sv[N_INIT], sgn[N_INIT];
   __shared__ int best;
   const int q = threadIdx.x;
-  sv[q] = fabs(init_entry(c, q));
+  sgn[q] = init_entry(c, q);
+  sv[q] = fabs(sgn[q]);
   __syncthreads();
   if (q == 0) {
     int b = 0;
     for (int t = 1; t < N_INIT; ++t)
       if (sv[t] > sv[b]) b = t;
     best = b;
+    *c.p0val = sgn[b];  // A(t0): u_0(x_0) of every superblock at the first sweep
     if (c.counters) atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)N_INIT);
   }
   __syncthreads();
@@ -100,13 +101,15 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 // ---------------------------------------------------------------------------------------
 // superblock factor tables (eq. (9)-(10) integrands split over the frozen parts)
 // ---------------------------------------------------------------------------------------
-// grid: x = node chunk, y = slot (alpha or beta), z = job*2 + side; block 128.
-// side 0 (alpha >= rows_done): SA = S_L + c_k[a], PA = P_LL * prod_{i<k} rho(u_k[a], X_i),
-//                              QL1 = prod_{i<k} rho(u_{k+1}[b], X_i)
-// side 1 (beta >= cols_done):  SB = c_{k+1}[b] + S_R, PB = P_RR * prod_{j>k+1} rho(u_{k+1}[b], Y_j),
-//                              QR0 = prod_{j>k+1} rho(u_k[a], Y_j)
-__global__ void __launch_bounds__(128) k_sb_sides(DevCtx c) {
-  const int job = blockIdx.z >> 1, side = blockIdx.z & 1, slot = blockIdx.y;
+// One launch, block 128.  blockIdx.z < 2*jobs: side tables, z = job*2 + side, x = node chunk,
+// y = slot (alpha or beta):
+//   side 0 (alpha >= rows_done): SA = S_L + c_k[a], PA = P_LL * prod_{i<k} rho(u_k[a], X_i),
+//                                QL1 = prod_{i<k} rho(u_{k+1}[b], X_i)
+//   side 1 (beta >= cols_done):  SB = c_{k+1}[b] + S_R, PB = P_RR * prod_{j>k+1} rho(u_{k+1}[b], Y_j),
+//                                QR0 = prod_{j>k+1} rho(u_k[a], Y_j)
+// blockIdx.z >= 2*jobs (family D): CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j)
+// for the new (alpha, beta) pairs, z = 2*jobs + job, y = alpha, x*128 + tid = beta.
+__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
   __shared__ ESum sS;
@@ -162,11 +165,7 @@ __global__ void __launch_bounds__(128) k_sb_sides(DevCtx c) {
   }
 }
 
-// CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j) for the new pairs;
-// grid: x = beta chunk (64), y = alpha, z = job
-__global__ void __launch_bounds__(64) k_sb_cx(DevCtx c) {
-  const int job = blockIdx.z, al = blockIdx.y;
-  const int be = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void sb_cx_table(const DevCtx& c, int job, int al, int be) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
   const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
@@ -182,6 +181,26 @@ __global__ void __launch_bounds__(64) k_sb_cx(DevCtx c) {
     }
   }
   c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
+}
+
+// grid: x = node chunk (sides) / beta chunk (CX), y = alpha (CX only), z = 2*jobs (+ jobs
+// for CX); only the rows/columns that are new since the previous sweep (at most one slot
+// per side after the first sweep) are computed
+__global__ void __launch_bounds__(128) k_sb_tables(DevCtx c, int njobs) {
+  const int d = c.d;
+  if ((int)blockIdx.z < 2 * njobs) {
+    if (blockIdx.y != 0) return;
+    const int job = blockIdx.z >> 1, side = blockIdx.z & 1, k = c.kb + job;
+    const int lim = side == 0 ? (k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1)
+                              : (k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1);
+    for (int slot = c.sbstate[job * 4 + side]; slot < lim; ++slot) {
+      sb_side_tables(c, job, side, slot);
+      __syncthreads();
+    }
+  } else {
+    const int be = blockIdx.x * blockDim.x + threadIdx.x;
+    if (be < c.cap) sb_cx_table(c, blockIdx.z - 2 * njobs, blockIdx.y, be);
+  }
 }
 
 // A_k(alpha, a; beta, b) from the tables (single rounding, R3)
@@ -213,95 +232,114 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 }
 
 // ---------------------------------------------------------------------------------------
-// u_s(x) on the new rows:  u_s(x) = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s)
-// grid: x = row chunk (256), y = job
+// k_sb_extend: u/v of the existing pivots on the rows / columns that are new this sweep
+// (the batched fiber evaluation).  One launch: z = side (0 rows, 1 columns), y = job,
+// x = tile of 32 rows (columns).  A warp owns one row at a time; lane s evaluates the raw
+// entries A(x, y_s) (A(x_s, y)) for s = lane, lane + 32, then the triangular recurrence runs
+// column-oriented with shuffles:  for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s] (s > t)
+// -- per s the same operations in the same order as the oracle's row-oriented
+// u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s) (t ascending), hence the same bits.
+// Columns: v_t = acc_t / u_t(x_t) final; acc_s -= U[t][x_s] * v_t.
 // ---------------------------------------------------------------------------------------
-template <int FAMILY>
-__global__ void __launch_bounds__(256) k_sb_extend_rows(DevCtx c) {
-  const int job = blockIdx.y, k = c.kb + job, n = c.n;
-  __shared__ int syb[TTC_MAX_RANK_DEV], sbb[TTC_MAX_RANK_DEV];
-  const int r = rec_rank(c.rec_cur, c.RS, k);
-  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
-  const long long x0 = (long long)c.sbstate[job * 4 + 0] * n;
-  const long long x = x0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (x0 + blockIdx.x * (long long)blockDim.x >= (long long)rl * n) return;
-  if (threadIdx.x < r) {
-    int px, py;
-    pivot_pos(c, k, threadIdx.x, px, py);
-    syb[threadIdx.x] = py / n;
-    sbb[threadIdx.x] = py - (py / n) * n;
-  }
-  __syncthreads();
-  if (x >= (long long)rl * n) return;
-  const int al = (int)(x / n), a = (int)(x - (long long)al * n);
-  const long long sbn = c.sbn;
-  const double* V = c.V + (long long)job * c.cap * sbn;
-  double* U = c.U + (long long)job * c.cap * sbn;
-  for (int s = 0; s < r; ++s) {
-    const long long ys = (long long)syb[s] * n + sbb[s];
-    double acc = sb_entry<FAMILY>(c, job, k, al, a, syb[s], sbb[s]);
-    for (int t = 0; t < s; ++t) acc = __dsub_rn(acc, __dmul_rn(U[t * sbn + x], V[t * sbn + ys]));
-    U[s * sbn + x] = acc;
-  }
-  if (c.counters) {
-    // one atomic per warp
-    const unsigned mask = __activemask();
-    const int cnt = __popc(mask);
-    if ((threadIdx.x & 31) == __ffs(mask) - 1) {
-      atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_SB_ENTRIES], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_EXT_ENTRIES], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_SB_UPDATES], (unsigned long long)cnt * r * (r - 1) / 2);
-      atomicAdd(&c.counters[CNT_EXT_UPDATES], (unsigned long long)cnt * r * (r - 1) / 2);
-    }
-  }
+#define EXT_TILE 64   // maximum rows per block; the launch picks tile = 16 or 64
+#define EXT_THREADS 256
+
+__host__ __device__ __forceinline__ size_t ext_smem_bytes(int cap) {
+  return (size_t)cap * cap * sizeof(double) + (size_t)cap * (EXT_TILE + 1) * sizeof(double);
 }
 
-// v_s(y) on the new columns:  v_s(y) = (A(x_s, y) - sum_{t<s} u_t(x_s) v_t(y)) / u_s(x_s)
 template <int FAMILY>
-__global__ void __launch_bounds__(256) k_sb_extend_cols(DevCtx c) {
-  const int job = blockIdx.y, k = c.kb + job, d = c.d, n = c.n;
-  __shared__ int sal[TTC_MAX_RANK_DEV], sa[TTC_MAX_RANK_DEV];
-  __shared__ long long sx[TTC_MAX_RANK_DEV];
+__global__ void __launch_bounds__(EXT_THREADS) k_sb_extend(DevCtx c, int tile_rows) {
+  const int side = blockIdx.z, job = blockIdx.y, k = c.kb + job, d = c.d, n = c.n, cap = c.cap;
+  extern __shared__ double ext_dyn[];
+  double* coef = ext_dyn;                       // [t][s], stride cap
+  double* tile = ext_dyn + (long long)cap * cap;  // [s][EXT_TILE + 1]
+  __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
+  __shared__ double pdiag[TTC_MAX_RANK_DEV];
   const int r = rec_rank(c.rec_cur, c.RS, k);
+  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
   const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
-  const long long y0 = (long long)c.sbstate[job * 4 + 1] * n;
-  const long long y = y0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (y0 + blockIdx.x * (long long)blockDim.x >= (long long)rr * n) return;
+  const int done = c.sbstate[job * 4 + side];
+  const long long lim = (long long)(side == 0 ? rl : rr) * n;
+  const long long first_new = (long long)done * n;
+  if (first_new + (long long)blockIdx.x * tile_rows >= lim) return;
+  const long long sbn = c.sbn;
+  double* U = c.U + (long long)job * cap * sbn;
+  double* V = c.V + (long long)job * cap * sbn;
+  const bool first = (c.sbstate[job * 4 + 0] == 0 && c.sbstate[job * 4 + 1] == 0);
+  // pivot coordinates (the fixed index of every raw entry) and the recurrence coefficients
   if (threadIdx.x < r) {
     int px, py;
     pivot_pos(c, k, threadIdx.x, px, py);
-    sal[threadIdx.x] = px / n;
-    sa[threadIdx.x] = px - (px / n) * n;
-    sx[threadIdx.x] = px;
+    const int q = side == 0 ? py : px;
+    p_al[threadIdx.x] = q / n;
+    p_a[threadIdx.x] = q - (q / n) * n;
+    if (side == 1) pdiag[threadIdx.x] = first ? *c.p0val : U[(long long)threadIdx.x * sbn + px];
   }
   __syncthreads();
-  if (y >= (long long)rr * n) return;
-  const int be = (int)(y / n), b = (int)(y - (long long)be * n);
-  const long long sbn = c.sbn;
-  const double* U = c.U + (long long)job * c.cap * sbn;
-  double* V = c.V + (long long)job * c.cap * sbn;
-  for (int s = 0; s < r; ++s) {
-    double acc = sb_entry<FAMILY>(c, job, k, sal[s], sa[s], be, b);
-    for (int t = 0; t < s; ++t) acc = __dsub_rn(acc, __dmul_rn(U[t * sbn + sx[s]], V[t * sbn + y]));
-    V[s * sbn + y] = __ddiv_rn(acc, U[s * sbn + sx[s]]);
-  }
-  if (c.counters) {
-    const unsigned mask = __activemask();
-    const int cnt = __popc(mask);
-    if ((threadIdx.x & 31) == __ffs(mask) - 1) {
-      atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_SB_ENTRIES], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_EXT_ENTRIES], (unsigned long long)cnt * r);
-      atomicAdd(&c.counters[CNT_SB_UPDATES], (unsigned long long)cnt * r * (r - 1) / 2);
-      atomicAdd(&c.counters[CNT_EXT_UPDATES], (unsigned long long)cnt * r * (r - 1) / 2);
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int t = e / r, s = e - t * r;
+    double v = 0.0;
+    if (t < s) {
+      const long long q = (long long)p_al[s] * n + p_a[s];
+      v = side == 0 ? V[(long long)t * sbn + q] : U[(long long)t * sbn + q];
     }
+    coef[t * cap + s] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double* dst = side == 0 ? U : V;
+  unsigned long long rows_done_here = 0;
+  for (long long x0 = first_new + (long long)blockIdx.x * tile_rows; x0 < lim;
+       x0 += (long long)gridDim.x * tile_rows) {
+    const int nrow = (int)min((long long)tile_rows, lim - x0);
+    for (int j = warp; j < nrow; j += nw) {
+      const long long x = x0 + j;
+      const int al = (int)(x / n), a = (int)(x - (long long)al * n);
+      double acc0 = 0.0, acc1 = 0.0;
+      if (lane < r)
+        acc0 = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[lane], p_a[lane])
+                         : sb_entry<FAMILY>(c, job, k, p_al[lane], p_a[lane], al, a);
+      if (lane + 32 < r)
+        acc1 = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[lane + 32], p_a[lane + 32])
+                         : sb_entry<FAMILY>(c, job, k, p_al[lane + 32], p_a[lane + 32], al, a);
+      for (int t = 0; t < r; ++t) {
+        double f = __shfl_sync(0xffffffffu, t < 32 ? acc0 : acc1, t & 31);
+        if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t final
+        if (t < 32 && lane == t) acc0 = f;
+        if (t >= 32 && lane == t - 32) acc1 = f;
+        if (lane > t) acc0 = __dsub_rn(acc0, __dmul_rn(f, coef[t * cap + lane]));
+        if (lane + 32 > t && lane + 32 < r) acc1 = __dsub_rn(acc1, __dmul_rn(f, coef[t * cap + lane + 32]));
+      }
+      if (lane < r) tile[lane * (EXT_TILE + 1) + j] = acc0;
+      if (lane + 32 < r) tile[(lane + 32) * (EXT_TILE + 1) + j] = acc1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * tile_rows; e += blockDim.x) {
+      const int s = e / tile_rows, j = e - s * tile_rows;
+      if (j < nrow) dst[(long long)s * sbn + x0 + j] = tile[s * (EXT_TILE + 1) + j];
+    }
+    __syncthreads();
+    rows_done_here += nrow;
+  }
+  if (c.counters && threadIdx.x == 0) {
+    const unsigned long long ent = rows_done_here * r;
+    const unsigned long long upd = rows_done_here * r * (r - 1) / 2;
+    atomicAdd(&c.counters[CNT_EVALS], ent);
+    atomicAdd(&c.counters[CNT_SB_ENTRIES], ent);
+    atomicAdd(&c.counters[CNT_EXT_ENTRIES], ent);
+    atomicAdd(&c.counters[CNT_SB_UPDATES], upd);
+    atomicAdd(&c.counters[CNT_EXT_UPDATES], upd);
   }
 }
 
 // ---------------------------------------------------------------------------------------
 // k_greedy: one cluster of G CTAs per superblock
 // ---------------------------------------------------------------------------------------
+#define GREEDY_MAX_THREADS 512
+#define STAGE_N 1024  // n up to which the n-indexed factor of a step is staged in shared memory
+
 struct Cand {
   double val;
   long long idx;
@@ -322,11 +360,16 @@ __device__ __forceinline__ void warp_argmax(double& v, long long& f) {
 
 struct GreedySmem {
   Cand cand[2];                      // published CTA candidate (double-buffered per step)
-  Cand red[GREEDY_THREADS / 32];
+  Cand red[GREEDY_MAX_THREADS / 32];
   Cand best;                         // CTA argmax / cluster winner
   int xs[TTC_MAX_RANK_DEV];          // pivot rows
   int ys[TTC_MAX_RANK_DEV];          // pivot columns
   double vec[TTC_MAX_RANK_DEV];      // V[t][y*] (column step) or U[t][x*] (row step)
+  // factors of the fixed column (row) of a step
+  DDE f_slot[TTC_MAX_RANK_DEV];      // column step: CX[alpha][beta]*QL1[alpha][b]; row step: CX*QR0
+  DDE f_node[STAGE_N];               // column step: QR0[beta][a]; row step: QL1[alpha][b]
+  ESum fs;                           // SB[beta][b] (column step) or SA[alpha][a] (row step)
+  DDE fp;                            // PB[beta][b] or PA[alpha][a]
 };
 
 // CTA-wide argmax of (v, f) -> S.best (all threads call)
@@ -348,8 +391,18 @@ __device__ __forceinline__ void cta_argmax(GreedySmem& S, double v, long long f)
 // cluster-wide argmax: every CTA publishes S.best in cand[ph]; after the barrier every CTA
 // reduces all G candidates (DSMEM) in cluster-rank order -> S.best
 __device__ __forceinline__ void cluster_argmax(GreedySmem& S, cg::cluster_group& cl, int G, int& ph) {
-  if (threadIdx.x == 0) S.cand[ph] = S.best;
-  cl.sync();
+  if (G == 1) {
+    ph ^= 1;
+    return;
+  }
+  // only thread 0 publishes, so only it needs release semantics: fence, then a relaxed arrive
+  // by every thread and the (acquiring) wait
+  if (threadIdx.x == 0) {
+    S.cand[ph] = S.best;
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double bv = -1.0;
@@ -366,8 +419,15 @@ __device__ __forceinline__ void cluster_argmax(GreedySmem& S, cg::cluster_group&
   __syncthreads();
 }
 
-template <int FAMILY>
-__global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int sweep) {
+// dynamic shared memory of the CACHED variant: own rows' U[t][x], SA, PA and own columns'
+// V[t][y], SB, PB stay on chip for the whole launch, plus the E / raw values of the last steps
+__host__ __device__ __forceinline__ long long greedy_cache_doubles(long long rpcap, int cap) {
+  // U[cap-1] Ecol Acol SA(2) PA(3) | V[cap-1] Erow SB(2) PB(3)
+  return rpcap * ((cap - 1) + 1 + 1 + 2 + 3 + (cap - 1) + 1 + 2 + 3);
+}
+
+template <int FAMILY, bool CACHED, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_greedy(DevCtx c, int sweep) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
@@ -375,12 +435,16 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
   const int k = c.kb + job, d = c.d, n = c.n, cap = c.cap;
   const int tid = threadIdx.x, T = blockDim.x;
   __shared__ GreedySmem S;
+  extern __shared__ double dyn[];
 
   const int r = rec_rank(c.rec_cur, c.RS, k);
   const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
   const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
   const long long R = (long long)rl * n, C = (long long)rr * n;
+  // rows / columns of this CTA (contiguous blocks); the cached variant's shared-memory
+  // stride is the capacity block rpcap >= rpc, cpc
   const long long rpc = (R + G - 1) / G, cpc = (C + G - 1) / G;
+  const long long rpcap = (c.sbn + G - 1) / G;
   const long long xb = cr * rpc, xe = min(R, xb + rpc);
   const long long yb = cr * cpc, ye = min(C, yb + cpc);
   const long long sbn = c.sbn;
@@ -389,6 +453,20 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
   double* Araw = c.Araw + (long long)job * sbn;
   int* Rn = c.rec_next + (long long)k * c.RS;
   const int* Rc = c.rec_cur + (long long)k * c.RS;
+  const long long jo = (long long)job * cap * n;   // table offset of this job
+  const long long jcx = (long long)job * cap * cap;
+  const double* uk = c.u + (long long)k * n;
+  const double* uk1 = c.u + (long long)(k + 1) * n;
+  // cached layout (rpcap rows / columns per CTA)
+  double* Uc = dyn;                                  // [t][rpcap]
+  double* Ecol = Uc + (long long)(cap - 1) * rpcap;  // [rpcap]
+  double* Acol = Ecol + rpcap;                       // [rpcap]
+  ESum* SAc = reinterpret_cast<ESum*>(Acol + rpcap);  // [rpcap]
+  DDE* PAc = reinterpret_cast<DDE*>(SAc + rpcap);     // [rpcap]
+  double* Vc = reinterpret_cast<double*>(PAc + rpcap);  // [t][rpcap]
+  double* Erow = Vc + (long long)(cap - 1) * rpcap;  // [rpcap]
+  ESum* SBc = reinterpret_cast<ESum*>(Erow + rpcap);  // [rpcap]
+  DDE* PBc = reinterpret_cast<DDE*>(SBc + rpcap);     // [rpcap]
 
   if (cr == 0)
     for (int t = tid; t < c.RS; t += T) Rn[t] = Rc[t];
@@ -405,13 +483,34 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
   if (p0 == 0.0) active = false;  // singular first pivot: leave the interface (R8)
   double scale = c.praw_max[job];
   if (scale < 0.0) scale = fabs(p0);
-  unsigned long long evals = 0, steps = 0, upd = 0;
+  unsigned long long evals = 0, upd = 0;
+  int steps = 0;
   int ph = 0;
   int xst = 0, yst = 0;
   bool added = false;
   double raw_star = 0.0;
+  const bool stage_n = n <= STAGE_N;
 
   if (active) {
+    if (CACHED) {
+      for (long long e = tid; e < (long long)r * rpcap; e += T) {
+        const int t = (int)(e / rpcap);
+        const long long j = e - (long long)t * rpcap;
+        if (xb + j < xe) Uc[t * rpcap + j] = U[t * sbn + xb + j];
+        if (yb + j < ye) Vc[t * rpcap + j] = V[t * sbn + yb + j];
+      }
+      for (long long j = tid; j < rpcap; j += T) {
+        if (xb + j < xe) {
+          SAc[j] = c.SA[jo + xb + j];
+          if (FAMILY == 1) PAc[j] = c.PA[jo + xb + j];
+        }
+        if (yb + j < ye) {
+          SBc[j] = c.SB[jo + yb + j];
+          if (FAMILY == 1) PBc[j] = c.PB[jo + yb + j];
+        }
+      }
+      // visibility of the cache is provided by the __syncthreads of the first step
+    }
     // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically)
     {
       const uint64_t tag = 1ULL + (uint64_t)sweep;
@@ -438,22 +537,61 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
         upd += (unsigned long long)c.ns * r;
       }
     }
-    // column step E(:, y) -> U[r][:], Araw; returns the cluster argmax row when `search`
+    // column step E(:, y) on this CTA's rows; returns the cluster argmax row when `search`.
+    // The factors that depend on the fixed column are staged once per step:
+    //   S.fs = SB[beta][b], S.fp = PB[beta][b], f_slot[alpha] = CX[alpha][beta]*QL1[alpha][b],
+    //   f_node[a] = QR0[beta][a]
     auto column = [&](int y, bool search) -> int {
-      if (tid < r) S.vec[tid] = V[tid * sbn + y];
-      __syncthreads();
       const int be = y / n, b = y - (y / n) * n;
+      if (tid < r) S.vec[tid] = V[tid * sbn + y];
+      if (tid == 0) {
+        S.fs = c.SB[jo + (long long)be * n + b];
+        if (FAMILY == 1) S.fp = c.PB[jo + (long long)be * n + b];
+      }
+      if (FAMILY == 1) {
+        for (int al = tid; al < rl; al += T) {
+          DDE f = c.CX[jcx + (long long)al * cap + be];
+          dde_mul(f, c.QL1[jo + (long long)al * n + b]);
+          S.f_slot[al] = f;
+        }
+        if (stage_n)
+          for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + (long long)be * n + a];
+      }
+      __syncthreads();
+      const double ub = uk1[b];
       double bv = -1.0;
       long long bf = LLONG_MAX;
       for (long long x = xb + tid; x < xe; x += T) {
         const int al = (int)(x / n), a = (int)(x - (long long)al * n);
-        const double raw = sb_entry<FAMILY>(c, job, k, al, a, be, b);
+        ESum s = CACHED ? SAc[x - xb] : c.SA[jo + x];
+        esum_add(s, S.fs);
+        const double Sd = esum_round(s);
+        const double SS = __dmul_rn(Sd, Sd);
+        double raw;
+        if (FAMILY == 0) {
+          raw = __drcp_rn(SS);
+        } else {
+          DDE p = CACHED ? PAc[x - xb] : c.PA[jo + x];
+          dde_mul(p, S.fp);
+          dde_mul(p, S.f_slot[al]);
+          dde_mul(p, stage_n ? S.f_node[a] : c.QR0[jo + (long long)be * n + a]);
+          dde_mul_d(p, rho(uk[a], ub));
+          raw = __ddiv_rn(dde_round(p), SS);
+        }
         double e = raw;
-        for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + x], S.vec[t]));
+        if (CACHED)
+          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(Uc[t * rpcap + (x - xb)], S.vec[t]));
+        else
+          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + x], S.vec[t]));
         for (int t = 0; t < r; ++t)
           if (S.xs[t] == x) e = 0.0;
-        Araw[x] = raw;
-        U[r * sbn + x] = e;
+        if (CACHED) {
+          Acol[x - xb] = raw;
+          Ecol[x - xb] = e;
+        } else {
+          Araw[x] = raw;
+          U[r * sbn + x] = e;
+        }
         if (cand_better(fabs(e), x, bv, bf)) { bv = fabs(e); bf = x; }
       }
       if (tid == 0) {
@@ -470,19 +608,53 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
       }
       return win;
     };
+    // row step E(x, :) on this CTA's columns; staged: S.fs = SA[alpha][a], S.fp = PA[alpha][a],
+    //   f_slot[beta] = CX[alpha][beta]*QR0[beta][a], f_node[b] = QL1[alpha][b]
     auto row = [&](int x, bool search) -> int {
-      if (tid < r) S.vec[tid] = U[tid * sbn + x];
-      __syncthreads();
       const int al = x / n, a = x - (x / n) * n;
+      if (tid < r) S.vec[tid] = U[tid * sbn + x];
+      if (tid == 0) {
+        S.fs = c.SA[jo + x];
+        if (FAMILY == 1) S.fp = c.PA[jo + x];
+      }
+      if (FAMILY == 1) {
+        for (int be = tid; be < rr; be += T) {
+          DDE f = c.CX[jcx + (long long)al * cap + be];
+          dde_mul(f, c.QR0[jo + (long long)be * n + a]);
+          S.f_slot[be] = f;
+        }
+        if (stage_n)
+          for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + (long long)al * n + b];
+      }
+      __syncthreads();
+      const double ua = uk[a];
       double bv = -1.0;
       long long bf = LLONG_MAX;
       for (long long y = yb + tid; y < ye; y += T) {
         const int be = (int)(y / n), b = (int)(y - (long long)be * n);
-        double e = sb_entry<FAMILY>(c, job, k, al, a, be, b);
-        for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], V[t * sbn + y]));
+        ESum s = CACHED ? SBc[y - yb] : c.SB[jo + y];
+        esum_add(s, S.fs);
+        const double Sd = esum_round(s);
+        const double SS = __dmul_rn(Sd, Sd);
+        double e;
+        if (FAMILY == 0) {
+          e = __drcp_rn(SS);
+        } else {
+          DDE p = CACHED ? PBc[y - yb] : c.PB[jo + y];
+          dde_mul(p, S.fp);
+          dde_mul(p, S.f_slot[be]);
+          dde_mul(p, stage_n ? S.f_node[b] : c.QL1[jo + (long long)al * n + b]);
+          dde_mul_d(p, rho(ua, uk1[b]));
+          e = __ddiv_rn(dde_round(p), SS);
+        }
+        if (CACHED)
+          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], Vc[t * rpcap + (y - yb)]));
+        else
+          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], V[t * sbn + y]));
         for (int t = 0; t < r; ++t)
           if (S.ys[t] == y) e = 0.0;
-        V[r * sbn + y] = e;
+        if (CACHED) Erow[y - yb] = e;
+        else V[r * sbn + y] = e;
         if (cand_better(fabs(e), y, bv, bf)) { bv = fabs(e); bf = y; }
       }
       if (tid == 0) {
@@ -514,7 +686,15 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
     }
     if (c_at != yst) column(yst, false);
     if (g_at != xst) row(xst, false);
-    cl.sync();  // U[r][:], V[r][:], Araw visible to the whole cluster
+    if (CACHED) {   // the final column / row leave the chip once
+      for (long long x = xb + tid; x < xe; x += T) {
+        U[r * sbn + x] = Ecol[x - xb];
+        Araw[x] = Acol[x - xb];
+      }
+      for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
+    }
+    if (G > 1) cl.sync();  // U[r][:], V[r][:], Araw visible to the whole cluster
+    else __syncthreads();
     const double pv = V[r * sbn + yst];
     raw_star = Araw[xst];
     if (fabs(pv) > c.tol * scale) {
@@ -543,16 +723,15 @@ __global__ void __launch_bounds__(GREEDY_THREADS, 1) k_greedy(DevCtx c, int swee
     c.sbstate[job * 4 + 0] = rl;
     c.sbstate[job * 4 + 1] = rr;
   }
-  if (c.counters) {
-    // per-thread tallies reduced by one atomic per thread with nonzero work
+  if (c.counters && tid == 0) {
     if (evals) {
       atomicAdd(&c.counters[CNT_EVALS], evals);
       atomicAdd(&c.counters[CNT_SB_ENTRIES], evals);
     }
     if (upd) atomicAdd(&c.counters[CNT_SB_UPDATES], upd);
-    if (cr == 0 && tid == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], steps);
+    if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
-  cl.sync();  // no CTA may exit while another can still read its shared memory
+  if (G > 1) cl.sync();  // no CTA may exit while another can still read its shared memory
 }
 
 }  // namespace ttc

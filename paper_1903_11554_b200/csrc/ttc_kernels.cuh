@@ -217,44 +217,47 @@ __global__ void k_wsum(DevCtx c, int mode_base) {
 }
 
 // H_i = M_i^{-1} W_{i+1}: LU with partial pivoting in double-double (shared memory),
-// one CTA per owned interface.
+// one CTA per owned interface.  Per elimination step: warp-0 argmax of |A[row][k].hi| (first
+// index on ties), row swap, multipliers l[row] = A[row][k] / A[k][k] once per row, then the
+// rank-1 update of the trailing block of [A | B] by all threads; back substitution is
+// column-oriented (x_k = B[k] / A[k][k], then B[q] -= A[q][k] x_k for q < k).
 __global__ void __launch_bounds__(256) k_solve(DevCtx c) {
   const int i = blockIdx.x + c.kb;
   const int cap = c.cap, d = c.d;
   extern __shared__ DD smd[];
   DD* A = smd;                 // [cap][cap]
   DD* Bm = smd + cap * cap;    // [cap][cap]
+  __shared__ DD l[TTC_MAX_RANK_DEV];
   __shared__ int piv_row;
-  __shared__ double piv_abs[256];
-  __shared__ int piv_idx[256];
   const int r = rec_rank(c.rec_cur, c.RS, i);
   const int nc = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
   for (int t = threadIdx.x; t < r * r; t += blockDim.x) {
-    int a = t / r, b = t % r;
+    const int a = t / r, b = t % r;
     A[a * cap + b] = dd_make(c.M[((long long)i * cap + a) * cap + b]);
   }
   for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
-    int a = t / nc, b = t % nc;
+    const int a = t / nc, b = t % nc;
     Bm[a * cap + b] = c.W[((long long)(i + 1) * cap + a) * cap + b];
   }
   __syncthreads();
   for (int k = 0; k < r; ++k) {
-    double best = -1.0;
-    int bi = k;
-    for (int row = k + threadIdx.x; row < r; row += blockDim.x) {
-      double v = fabs(A[row * cap + k].hi);
-      if (v > best) { best = v; bi = row; }
-    }
-    piv_abs[threadIdx.x] = best;
-    piv_idx[threadIdx.x] = bi;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double bb = -1.0;
-      int bj = k;
-      for (int t = 0; t < blockDim.x; ++t)
-        if (piv_abs[t] > bb || (piv_abs[t] == bb && piv_idx[t] < bj)) { bb = piv_abs[t]; bj = piv_idx[t]; }
-      piv_row = bj;
-      if (!(bb > 0.0)) atomicOr(&c.flags[0], 1);
+    if (threadIdx.x < 32) {
+      double bv = -1.0;
+      int bi = k;
+      for (int row = k + threadIdx.x; row < r; row += 32) {
+        const double v = fabs(A[row * cap + k].hi);
+        if (v > bv) { bv = v; bi = row; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (threadIdx.x == 0) {
+        piv_row = bi;
+        if (!(bv > 0.0)) atomicOr(&c.flags[0], 1);
+      }
     }
     __syncthreads();
     const int pr = piv_row;
@@ -263,34 +266,36 @@ __global__ void __launch_bounds__(256) k_solve(DevCtx c) {
         if (t < r) { DD x = A[k * cap + t]; A[k * cap + t] = A[pr * cap + t]; A[pr * cap + t] = x; }
         if (t < nc) { DD y = Bm[k * cap + t]; Bm[k * cap + t] = Bm[pr * cap + t]; Bm[pr * cap + t] = y; }
       }
+      __syncthreads();
     }
-    __syncthreads();
     const DD akk = A[k * cap + k];
+    for (int row = k + 1 + threadIdx.x; row < r; row += blockDim.x) l[row] = dd_div(A[row * cap + k], akk);
+    __syncthreads();
     const int width = (r - k - 1) + nc;
     for (int t = threadIdx.x; t < (r - k - 1) * width; t += blockDim.x) {
       const int row = k + 1 + t / width;
       const int colx = t % width;
-      const DD l = dd_div(A[row * cap + k], akk);
       if (colx < r - k - 1) {
         const int col = k + 1 + colx;
-        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l, A[k * cap + col]));
+        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l[row], A[k * cap + col]));
       } else {
         const int col = colx - (r - k - 1);
-        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l, Bm[k * cap + col]));
+        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l[row], Bm[k * cap + col]));
       }
     }
     __syncthreads();
   }
   for (int k = r - 1; k >= 0; --k) {
-    for (int col = threadIdx.x; col < nc; col += blockDim.x) {
-      DD acc = Bm[k * cap + col];
-      for (int q = k + 1; q < r; ++q) acc = dd_sub(acc, dd_mul(A[k * cap + q], Bm[q * cap + col]));
-      Bm[k * cap + col] = dd_div(acc, A[k * cap + k]);
+    for (int col = threadIdx.x; col < nc; col += blockDim.x) Bm[k * cap + col] = dd_div(Bm[k * cap + col], A[k * cap + k]);
+    __syncthreads();
+    for (int t = threadIdx.x; t < k * nc; t += blockDim.x) {
+      const int q = t / nc, col = t % nc;
+      Bm[q * cap + col] = dd_sub(Bm[q * cap + col], dd_mul(A[q * cap + k], Bm[k * cap + col]));
     }
     __syncthreads();
   }
   for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
-    int a = t / nc, b = t % nc;
+    const int a = t / nc, b = t % nc;
     c.H[((long long)i * cap + a) * cap + b] = Bm[a * cap + b];
   }
 }
