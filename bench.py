@@ -133,12 +133,11 @@ def roofline(kt, stats, family, peaks, peak_src):
     avg_s = ms / max(1, launches) / 1e3
     out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
     fpe = FLOPS_PER_ENTRY[family]
-    if name == "k_sb_extend":
-        ent, upd = stats["ext_entries"] / max(1, launches), stats["ext_updates"] / max(1, launches)
-    elif name == "k_greedy":
-        ent = (stats["sb_entries"] - stats["ext_entries"]) / max(1, launches)
-        upd = (stats["sb_updates"] - stats["ext_updates"]) / max(1, launches)
+    if name == "k_sweep":
+        ent = stats["sb_entries"] / max(1, launches)
+        upd = stats["sb_updates"] / max(1, launches)
         out["rook_steps_per_launch"] = stats["rook_steps"] / max(1, launches)
+        out["extension_share_of_entries"] = stats["ext_entries"] / max(1, stats["sb_entries"])
     elif name == "k_fiber":
         ent, upd = stats["fiber_entries"] / max(1, launches), 0
     else:
@@ -391,6 +390,7 @@ def main():
             "evals_per_step": evals_total, "sweep_ms": ms_max / args.steps,
             "integral": {"value": val[0], "log10_abs": val[1], "sign": val[2]},
             "graph": use_graph, "gpu_launches": int(launches_step) * args.steps,
+            "launch_shape": core.launch_shape(),
             "roofline": roof, "kernel_ms_per_solve": kernel_ms, "clocks": clocks, "e2e": e2e,
             "cpu_baseline": cpu,
         }

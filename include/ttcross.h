@@ -66,16 +66,16 @@ typedef struct ttc_stats {
   int64_t launches;        /* kernels launched since the last reset                        */
   int32_t sweeps;          /* Alg. 6 sweeps committed since the last reset                 */
   int32_t pad;
-  double  ms_fiber;        /* device time: superblock tables/extension + quadrature fibers */
-  double  ms_cross;        /* device time: k_greedy (samples + rook search)                */
+  double  ms_fiber;        /* device time: quadrature fibers (k_frozen_*, k_fiber)          */
+  double  ms_cross;        /* device time: k_sweep (tables, u/v extension, Alg. 2 search)   */
   double  ms_quad;         /* device time: quadrature contraction kernels                  */
   double  ms_other;        /* device time: init kernels                                    */
   int64_t fiber_entries;   /* entries written by k_fiber (quadrature fibers)               */
-  int64_t sb_entries;      /* superblock entries evaluated by k_sb_extend and k_greedy     */
+  int64_t sb_entries;      /* superblock entries evaluated by k_sweep                      */
   int64_t sb_updates;      /* multiply-subtract terms u_t(x) v_t(y) of those kernels        */
   int64_t rook_steps;      /* column+row rounds of the rook searches                        */
-  int64_t ext_entries;     /* superblock entries evaluated by k_sb_extend only              */
-  int64_t ext_updates;     /* multiply-subtract terms of k_sb_extend only                   */
+  int64_t ext_entries;     /* ... of which by the u/v extension phase (batched fibers)      */
+  int64_t ext_updates;     /* multiply-subtract terms of the extension phase                */
 } ttc_stats;
 
 /*
@@ -189,12 +189,17 @@ int tt_cross_get_fiber(ttc_ctx* ctx, int32_t mode, double* out, int64_t capacity
 int tt_cross_get_stats(ttc_ctx* ctx, ttc_stats* out);
 
 /* tt_cross_get_kernel_time -- per-kernel launch count and accumulated device time (ms,
- * timing enabled) since the last reset, for kernel id kid in [0, 15): 0 k_prep_nodes,
- * 1 k_init_pivot, 2 k_init_records, 3 k_sb_tables, 4 k_sb_extend, 5 k_greedy,
- * 6 k_frozen_sides, 7 k_frozen_q, 8 k_frozen_lr, 9 k_fiber, 10 k_wsum, 11 k_intersection,
- * 12 k_solve, 13 k_chain, 14 k_finish.
+ * timing enabled) since the last reset, for kernel id kid in [0, 13): 0 k_prep_nodes,
+ * 1 k_init_pivot, 2 k_init_records, 3 k_sweep, 4 k_frozen_sides, 5 k_frozen_q,
+ * 6 k_frozen_lr, 7 k_fiber, 8 k_wsum, 9 k_intersection, 10 k_solve, 11 k_chain, 12 k_finish.
  * *name is a static string.  Errors: TTC_ERR_ARG for kid out of range. */
 int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64_t* launches, double* ms);
+
+/* tt_cross_get_launch_shape -- the k_sweep launch chosen at init: CTAs per superblock cluster,
+ * threads per CTA, whether the rook search keeps its rows/columns in shared memory, and the
+ * dynamic shared memory per CTA (bytes).  Any pointer may be NULL. */
+int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, int32_t* cached,
+                              int64_t* smem_bytes);
 
 /* tt_cross_set_timing -- 1: bracket every kernel launch with CUDA events on the context
  * stream and accumulate per-kernel device time; 0: off (default).  Ignored while a CUDA

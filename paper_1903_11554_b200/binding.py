@@ -26,9 +26,9 @@ EXPORTS = [
     "tt_cross_commit", "tt_cross_exchange_buffer", "tt_solve_launch", "tt_integrate", "tt_integrate_launch",
     "tt_integrate_read", "tt_integrate_local", "tt_integrate_partials_buffer", "tt_integrate_finish",
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
-    "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info",
+    "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info", "tt_cross_get_launch_shape",
 ]
-N_KERNELS = 15
+N_KERNELS = 13
 
 
 class TtcConfig(ctypes.Structure):
@@ -79,6 +79,8 @@ def load(path: str = LIB_PATH):
         "tt_cross_set_timing": (i32, [P, i32]),
         "tt_cross_destroy": (None, [P]),
         "tt_cross_load_grid": (i32, [P, P, P, i32]),
+        "tt_cross_get_launch_shape": (i32, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                            ctypes.POINTER(i64)]),
         "tt_cross_get_kernel_time": (i32, [P, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64),
                                            ctypes.POINTER(f64)]),
         "tt_solve_launch": (i32, [P, i32, i32]),
@@ -249,6 +251,12 @@ class TTCross:
         _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
         return {f: getattr(s, f) for f, _ in TtcStats._fields_ if f != "pad"}
 
+
+    def launch_shape(self):
+        g, t, ca, sm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _check(self.lib, self.lib.tt_cross_get_launch_shape(self._h, ctypes.byref(g), ctypes.byref(t), ctypes.byref(ca),
+                                                            ctypes.byref(sm)), "tt_cross_get_launch_shape")
+        return {"cluster": g.value, "threads": t.value, "cached": bool(ca.value), "smem_bytes": sm.value}
 
     def kernel_times(self):
         """{kernel name: (launches, ms)} since the last reset (ms only with timing on)."""

@@ -37,16 +37,14 @@ enum KClass { KC_FIBER = 0, KC_CROSS = 1, KC_QUAD = 2, KC_OTHER = 3 };
 
 // per-kernel identifiers for tt_cross_get_kernel_time (class = accounting bucket of ttc_stats)
 enum KId {
-  K_PREP = 0, K_INIT_PIVOT, K_INIT_RECORDS, K_SB_TABLES, K_SB_EXTEND, K_GREEDY, K_FROZEN_SIDES, K_FROZEN_Q,
-  K_FROZEN_LR, K_FIBER, K_WSUM, K_INTERSECTION, K_SOLVE, K_CHAIN, K_FINISH, K_COUNT
+  K_PREP = 0, K_INIT_PIVOT, K_INIT_RECORDS, K_SWEEP, K_FROZEN_SIDES, K_FROZEN_Q, K_FROZEN_LR, K_FIBER,
+  K_WSUM, K_INTERSECTION, K_SOLVE, K_CHAIN, K_FINISH, K_COUNT
 };
 const char* const kKernelName[K_COUNT] = {
-    "k_prep_nodes", "k_init_pivot", "k_init_records", "k_sb_tables", "k_sb_extend", "k_greedy",
-    "k_frozen_sides", "k_frozen_q", "k_frozen_lr", "k_fiber", "k_wsum", "k_intersection", "k_solve",
-    "k_chain", "k_finish"};
-const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_OTHER, KC_FIBER, KC_FIBER, KC_CROSS, KC_FIBER,
-                                   KC_FIBER, KC_FIBER, KC_FIBER, KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,
-                                   KC_QUAD};
+    "k_prep_nodes", "k_init_pivot", "k_init_records", "k_sweep", "k_frozen_sides", "k_frozen_q",
+    "k_frozen_lr", "k_fiber", "k_wsum", "k_intersection", "k_solve", "k_chain", "k_finish"};
+const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_OTHER, KC_CROSS, KC_FIBER, KC_FIBER, KC_FIBER,
+                                   KC_FIBER, KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD};
 
 struct EvRec {
   cudaEvent_t a, b;
@@ -70,9 +68,9 @@ struct ttc_ctx {
   int pending = 0;  // a local sweep waits for commit
   int* t0buf = nullptr;
   int sms = 148;               // multiprocessors of the device
-  bool greedy_cached = false;  // k_greedy keeps its rows' u / columns' v in shared memory
-  size_t greedy_smem = 0;      // dynamic shared memory of k_greedy
-  int greedy_threads = 256;    // CTA size of k_greedy (256: two CTAs per SM, 512: one)
+  bool greedy_cached = false;  // k_sweep keeps its rows' u / columns' v in shared memory
+  size_t greedy_smem = 0;      // dynamic shared memory of k_sweep
+  int greedy_threads = 256;    // CTA size of k_sweep (256: two CTAs per SM, 512: one)
   const void* greedy_fn = nullptr;
   // buffers
   std::vector<void*> allocs;
@@ -180,28 +178,7 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
 int do_sweep_local(ttc_ctx* c) {
   if (c->n_owned > 0) {
     DevCtx& dc = c->dc;
-    const int nj = c->n_owned, cap = dc.cap, n = dc.n;
-    {
-      Timed t(c, K_SB_TABLES);
-      const int gx = std::max((cap + 127) / 128, std::min(4, (n + 127) / 128));
-      const int gy = dc.family == TTC_FAMILY_D ? cap : 1;
-      const int gz = 2 * nj + (dc.family == TTC_FAMILY_D ? nj : 0);
-      k_sb_tables<<<dim3(gx, gy, gz), 128, 0, c->ls>>>(dc, nj);
-    }
-    if (int e = check_launch("k_sb_tables")) return e;
-    {
-      // new rows (columns) per sweep: at most one neighbour slot = n, except never more
-      Timed t(c, K_SB_EXTEND);
-      // small launches are latency-bound: 16-row tiles (2 rows per warp) unless that makes
-      // more than 4 blocks per SM, then 64-row tiles amortise the coefficient loads
-      int tile_rows = 16;
-      if ((long long)nj * 2 * ((n + 15) / 16) > 4LL * c->sms) tile_rows = EXT_TILE;
-      const dim3 g((unsigned)((n + tile_rows - 1) / tile_rows), nj, 2);
-      const size_t sm = ext_smem_bytes(cap);
-      if (dc.family == TTC_FAMILY_C) k_sb_extend<0><<<g, EXT_THREADS, sm, c->ls>>>(dc, tile_rows);
-      else k_sb_extend<1><<<g, EXT_THREADS, sm, c->ls>>>(dc, tile_rows);
-    }
-    if (int e = check_launch("k_sb_extend")) return e;
+    const int nj = c->n_owned;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(nj * dc.G);
     lc.blockDim = dim3(c->greedy_threads);
@@ -216,12 +193,12 @@ int do_sweep_local(ttc_ctx* c) {
     lc.numAttrs = 1;
     cudaError_t e;
     {
-      Timed t(c, K_GREEDY);
+      Timed t(c, K_SWEEP);
       lc.dynamicSmemBytes = c->greedy_smem;
       e = cudaLaunchKernelEx(&lc, (void (*)(DevCtx, int))c->greedy_fn, dc, c->sweeps);
     }
-    if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_greedy launch: ") + cudaGetErrorString(e));
-    if (int e2 = check_launch("k_greedy")) return e2;
+    if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweep launch: ") + cudaGetErrorString(e));
+    if (int e2 = check_launch("k_sweep")) return e2;
   }
   c->pending = 1;
   return TTC_OK;
@@ -462,7 +439,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.ke = c->ke;
   dc.RS = 1 + cap * d + 2 * cap;
   dc.sbn = (long long)cap * n;
-  dc.G = 1;  // cluster size of k_greedy, chosen below once the device is known
+  dc.G = 1;  // cluster size of k_sweep, chosen below once the device is known
   c->slots = d;
   c->nrec = k.world * c->chunk;
   c->rec_ints = (long long)c->nrec * dc.RS;
@@ -516,25 +493,21 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     };
-    if (ce == cudaSuccess)
-      ce = cudaFuncSetAttribute(k_sb_extend<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ext_smem_bytes(cap));
-    if (ce == cudaSuccess)
-      ce = cudaFuncSetAttribute(k_sb_extend<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ext_smem_bytes(cap));
-    allow((const void*)k_greedy<0, false, 256>, 0);
-    allow((const void*)k_greedy<1, false, 256>, 0);
-    allow((const void*)k_greedy<0, true, 256>, 80 * 1024);
-    allow((const void*)k_greedy<1, true, 256>, 80 * 1024);
-    allow((const void*)k_greedy<0, false, 512>, 0);
-    allow((const void*)k_greedy<1, false, 512>, 0);
-    allow((const void*)k_greedy<0, true, 512>, 180 * 1024);
-    allow((const void*)k_greedy<1, true, 512>, 180 * 1024);
+    allow((const void*)k_sweep<0, false, 256>, 180 * 1024);
+    allow((const void*)k_sweep<1, false, 256>, 180 * 1024);
+    allow((const void*)k_sweep<0, true, 256>, 180 * 1024);
+    allow((const void*)k_sweep<1, true, 256>, 180 * 1024);
+    allow((const void*)k_sweep<0, false, 512>, 180 * 1024);
+    allow((const void*)k_sweep<1, false, 512>, 180 * 1024);
+    allow((const void*)k_sweep<0, true, 512>, 180 * 1024);
+    allow((const void*)k_sweep<1, true, 512>, 180 * 1024);
     const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   }
   {
-    // k_greedy shape: G CTAs (a power of two <= 16, at least 128 superblock rows each) per
+    // k_sweep shape: G CTAs (a power of two <= 16, at least 128 superblock rows each) per
     // owned superblock, all resident at once.  512-thread CTAs (one per SM) when that gives
     // at least as many threads per superblock as 256-thread CTAs (two per SM); the CACHED
     // variant when the CTA's rows/columns fit in shared memory.
@@ -549,53 +522,66 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       while (G > 1 && (G * (long long)nj > slots || G > by_rows)) G >>= 1;
       return G;
     };
-    const int g512 = pick_g(sms), g256 = pick_g(2LL * sms);
-    int T = (g512 > 0 && 512LL * g512 >= 256LL * g256) ? 512 : 256;
-    int G = T == 512 ? g512 : std::max(1, g256);
+    // 256-thread CTAs measured faster than 512 at equal cluster size (profiles/r01d_probe_*)
+    int T = 256;
+    int G = std::max(1, pick_g(2LL * sms));
     // tuning overrides (benchmarks / experiments): TTC_GREEDY_T in {256, 512}, TTC_GREEDY_G
     if (const char* e = std::getenv("TTC_GREEDY_T")) {
       const int t = std::atoi(e);
-      if (t == 256 || t == 512) { T = t; G = std::max(1, t == 512 ? g512 : g256); }
+      if (t == 256 || t == 512) { T = t; G = std::max(1, pick_g(t == 512 ? sms : 2LL * sms)); }
     }
     if (const char* e = std::getenv("TTC_GREEDY_G")) {
       const int g = std::atoi(e);
       if (g >= 1 && g <= 16 && (g & (g - 1)) == 0) G = g;
     }
-    auto smem_for = [&](int g) -> size_t {
+    auto cache_for = [&](int g) -> size_t {
       const long long rpcap = (dc.sbn + g - 1) / g;
       return (size_t)greedy_cache_doubles(rpcap, cap) * sizeof(double);
     };
-    const size_t smem_lim = T == 512 ? 180 * 1024 : 80 * 1024;
+    const size_t ext_bytes = (size_t)extend_smem_doubles(cap) * sizeof(double);
+    const size_t smem_lim = 180 * 1024;
+    auto smem_for = [&](int g, bool cached) -> size_t {
+      return std::max(ext_bytes, cached ? cache_for(g) : (size_t)0);
+    };
     auto fn_for = [&](bool cached) -> const void* {
       if (k.family == TTC_FAMILY_C)
-        return T == 512 ? (cached ? (const void*)k_greedy<0, true, 512> : (const void*)k_greedy<0, false, 512>)
-                        : (cached ? (const void*)k_greedy<0, true, 256> : (const void*)k_greedy<0, false, 256>);
-      return T == 512 ? (cached ? (const void*)k_greedy<1, true, 512> : (const void*)k_greedy<1, false, 512>)
-                      : (cached ? (const void*)k_greedy<1, true, 256> : (const void*)k_greedy<1, false, 256>);
+        return T == 512 ? (cached ? (const void*)k_sweep<0, true, 512> : (const void*)k_sweep<0, false, 512>)
+                        : (cached ? (const void*)k_sweep<0, true, 256> : (const void*)k_sweep<0, false, 256>);
+      return T == 512 ? (cached ? (const void*)k_sweep<1, true, 512> : (const void*)k_sweep<1, false, 512>)
+                      : (cached ? (const void*)k_sweep<1, true, 256> : (const void*)k_sweep<1, false, 256>);
     };
-    while (G > 1) {
+    // resident clusters for (G, cached)
+    auto resident = [&](int g, bool cached) -> int {
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(G);
+      lc.gridDim = dim3(g);
       lc.blockDim = dim3(T);
-      const bool cached = smem_for(G) <= smem_lim;
-      lc.dynamicSmemBytes = cached ? smem_for(G) : 0;
+      lc.dynamicSmemBytes = smem_for(g, cached);
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.x = g;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
       int nclus = 0;
-      cudaError_t ce = cudaOccupancyMaxActiveClusters(&nclus, fn_for(cached), &lc);
-      if (ce == cudaSuccess && nclus >= 1) break;
-      cudaGetLastError();
-      G >>= 1;
+      if (cudaOccupancyMaxActiveClusters(&nclus, fn_for(cached), &lc) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      return nclus;
+    };
+    // prefer: all nj clusters resident; cached rows when they fit; then the largest G
+    bool cached = false;
+    for (;; G >>= 1) {
+      const bool can_cache = cache_for(G) <= smem_lim;
+      if (can_cache && resident(G, true) >= std::min(nj, 1 << 30)) { cached = true; break; }
+      if (resident(G, false) >= nj) { cached = false; break; }
+      if (G == 1) { cached = false; break; }
     }
     dc.G = G;
     c->greedy_threads = T;
-    c->greedy_cached = smem_for(G) <= smem_lim;
-    c->greedy_smem = c->greedy_cached ? smem_for(G) : 0;
+    c->greedy_cached = cached;
+    c->greedy_smem = smem_for(G, cached);
     c->greedy_fn = fn_for(c->greedy_cached);
   }
   int rc = tt_cross_load_grid(c, nodes_u, weights, mem_kind);
@@ -790,6 +776,16 @@ int tt_cross_get_kernel_time(ttc_ctx* c, int32_t kid, const char** name, int64_t
   if (name) *name = kKernelName[kid];
   if (launches) *launches = c->klaunch[kid];
   if (ms) *ms = c->kms[kid];
+  return TTC_OK;
+}
+
+int tt_cross_get_launch_shape(ttc_ctx* c, int32_t* cluster, int32_t* threads, int32_t* cached,
+                              int64_t* smem_bytes) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (cluster) *cluster = c->dc.G;
+  if (threads) *threads = c->greedy_threads;
+  if (cached) *cached = c->greedy_cached ? 1 : 0;
+  if (smem_bytes) *smem_bytes = (int64_t)c->greedy_smem;
   return TTC_OK;
 }
 

@@ -7,14 +7,14 @@
 // incomplete-LU form A~(x, y) = sum_t u_t(x) v_t(y) (oracle/cross.py).
 //
 //   k_init_pivot / k_init_records : the rank-1 start (first argmax |A| over seeded samples)
-//   k_sb_tables                   : factor tables of the superblock entries for the rows /
-//                                   columns that are new this sweep (the frozen left/right
-//                                   pivot coordinates, staged once per sweep)
-//   k_sb_extend                   : u_s(x) / v_s(y) of the existing pivots on the new rows /
-//                                   columns -- the batched fiber evaluation of the sweep
-//   k_greedy                      : one thread-block cluster per superblock: random samples
-//                                   (Alg. 2 line 1), rook search (lines 2-5), append the new
-//                                   pivot (Alg. 6 line 4) to the next record buffer.
+//   k_sweep                       : one thread-block cluster per superblock, three phases
+//                                   separated by cluster barriers:
+//     1. factor tables of the superblock entries for the rows / columns that are new this
+//        sweep (the frozen left/right pivot coordinates, staged once per sweep);
+//     2. u_s(x) / v_s(y) of the existing pivots on the new rows / columns -- the batched
+//        fiber evaluation of the sweep;
+//     3. Alg. 2: random samples (line 1), rook search (lines 2-5), append the new pivot
+//        (Alg. 6 line 4) to the next record buffer.
 //
 // Arithmetic is bit-identical to the oracle (R3, R4): entries are exactly rounded
 // functions of the coordinate multiset (any factorisation gives the same bits), every sum
@@ -109,7 +109,7 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 //                                QR0 = prod_{j>k+1} rho(u_k[a], Y_j)
 // blockIdx.z >= 2*jobs (family D): CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j)
 // for the new (alpha, beta) pairs, z = 2*jobs + job, y = alpha, x*128 + tid = beta.
-__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot) {
+__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
   __shared__ ESum sS;
@@ -146,7 +146,7 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot) {
   const long long o = ((long long)job * c.cap + slot) * n;
   const int mode_own = side == 0 ? k : k + 1;    // mode summed into SA / SB
   const int mode_oth = side == 0 ? k + 1 : k;    // mode of QL1 / QR0
-  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+  for (int a = a0 + threadIdx.x; a < n; a += astride) {
     ESum s = sS;
     esum_add(s, c.chi[mode_own * n + a], c.clo[mode_own * n + a]);
     if (side == 0) c.SA[o + a] = s;
@@ -183,26 +183,6 @@ __device__ void sb_cx_table(const DevCtx& c, int job, int al, int be) {
   c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
 }
 
-// grid: x = node chunk (sides) / beta chunk (CX), y = alpha (CX only), z = 2*jobs (+ jobs
-// for CX); only the rows/columns that are new since the previous sweep (at most one slot
-// per side after the first sweep) are computed
-__global__ void __launch_bounds__(128) k_sb_tables(DevCtx c, int njobs) {
-  const int d = c.d;
-  if ((int)blockIdx.z < 2 * njobs) {
-    if (blockIdx.y != 0) return;
-    const int job = blockIdx.z >> 1, side = blockIdx.z & 1, k = c.kb + job;
-    const int lim = side == 0 ? (k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1)
-                              : (k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1);
-    for (int slot = c.sbstate[job * 4 + side]; slot < lim; ++slot) {
-      sb_side_tables(c, job, side, slot);
-      __syncthreads();
-    }
-  } else {
-    const int be = blockIdx.x * blockDim.x + threadIdx.x;
-    if (be < c.cap) sb_cx_table(c, blockIdx.z - 2 * njobs, blockIdx.y, be);
-  }
-}
-
 // A_k(alpha, a; beta, b) from the tables (single rounding, R3)
 template <int FAMILY>
 __device__ __forceinline__ double sb_entry(const DevCtx& c, int job, int k, int al, int a, int be, int b) {
@@ -232,51 +212,26 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 }
 
 // ---------------------------------------------------------------------------------------
-// k_sb_extend: u/v of the existing pivots on the rows / columns that are new this sweep
-// (the batched fiber evaluation).  One launch: z = side (0 rows, 1 columns), y = job,
-// x = tile of 32 rows (columns).  A warp owns one row at a time; lane s evaluates the raw
-// entries A(x, y_s) (A(x_s, y)) for s = lane, lane + 32, then the triangular recurrence runs
-// column-oriented with shuffles:  for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s] (s > t)
+// phase 2: u/v of the existing pivots on the rows / columns that are new this sweep.  A warp
+// owns one row at a time; lane s evaluates the raw entries A(x, y_s) (A(x_s, y)) for s = lane,
+// lane + 32, then the triangular recurrence runs column-oriented with shuffles:
+//   for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s]  (s > t)
 // -- per s the same operations in the same order as the oracle's row-oriented
 // u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s) (t ascending), hence the same bits.
 // Columns: v_t = acc_t / u_t(x_t) final; acc_s -= U[t][x_s] * v_t.
+// Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][EXT_TILE + 1].
 // ---------------------------------------------------------------------------------------
-#define EXT_TILE 64   // maximum rows per block; the launch picks tile = 16 or 64
-#define EXT_THREADS 256
-
-__host__ __device__ __forceinline__ size_t ext_smem_bytes(int cap) {
-  return (size_t)cap * cap * sizeof(double) + (size_t)cap * (EXT_TILE + 1) * sizeof(double);
-}
+#define EXT_TILE 16
 
 template <int FAMILY>
-__global__ void __launch_bounds__(EXT_THREADS) k_sb_extend(DevCtx c, int tile_rows) {
-  const int side = blockIdx.z, job = blockIdx.y, k = c.kb + job, d = c.d, n = c.n, cap = c.cap;
-  extern __shared__ double ext_dyn[];
-  double* coef = ext_dyn;                       // [t][s], stride cap
-  double* tile = ext_dyn + (long long)cap * cap;  // [s][EXT_TILE + 1]
-  __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
-  __shared__ double pdiag[TTC_MAX_RANK_DEV];
-  const int r = rec_rank(c.rec_cur, c.RS, k);
-  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
-  const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
-  const int done = c.sbstate[job * 4 + side];
-  const long long lim = (long long)(side == 0 ? rl : rr) * n;
-  const long long first_new = (long long)done * n;
-  if (first_new + (long long)blockIdx.x * tile_rows >= lim) return;
+__device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
+                            const int* p_al, const int* p_a, const double* pdiag, double* coef, double* tile,
+                            unsigned long long& ent, unsigned long long& upd) {
+  const int n = c.n, cap = c.cap;
   const long long sbn = c.sbn;
   double* U = c.U + (long long)job * cap * sbn;
   double* V = c.V + (long long)job * cap * sbn;
-  const bool first = (c.sbstate[job * 4 + 0] == 0 && c.sbstate[job * 4 + 1] == 0);
-  // pivot coordinates (the fixed index of every raw entry) and the recurrence coefficients
-  if (threadIdx.x < r) {
-    int px, py;
-    pivot_pos(c, k, threadIdx.x, px, py);
-    const int q = side == 0 ? py : px;
-    p_al[threadIdx.x] = q / n;
-    p_a[threadIdx.x] = q - (q / n) * n;
-    if (side == 1) pdiag[threadIdx.x] = first ? *c.p0val : U[(long long)threadIdx.x * sbn + px];
-  }
-  __syncthreads();
+  if (x_lo >= x_hi) return;
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
     const int t = e / r, s = e - t * r;
     double v = 0.0;
@@ -290,10 +245,8 @@ __global__ void __launch_bounds__(EXT_THREADS) k_sb_extend(DevCtx c, int tile_ro
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   double* dst = side == 0 ? U : V;
-  unsigned long long rows_done_here = 0;
-  for (long long x0 = first_new + (long long)blockIdx.x * tile_rows; x0 < lim;
-       x0 += (long long)gridDim.x * tile_rows) {
-    const int nrow = (int)min((long long)tile_rows, lim - x0);
+  for (long long x0 = x_lo; x0 < x_hi; x0 += EXT_TILE) {
+    const int nrow = (int)min((long long)EXT_TILE, x_hi - x0);
     for (int j = warp; j < nrow; j += nw) {
       const long long x = x0 + j;
       const int al = (int)(x / n), a = (int)(x - (long long)al * n);
@@ -316,26 +269,23 @@ __global__ void __launch_bounds__(EXT_THREADS) k_sb_extend(DevCtx c, int tile_ro
       if (lane + 32 < r) tile[(lane + 32) * (EXT_TILE + 1) + j] = acc1;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < r * tile_rows; e += blockDim.x) {
-      const int s = e / tile_rows, j = e - s * tile_rows;
+    for (int e = threadIdx.x; e < r * EXT_TILE; e += blockDim.x) {
+      const int s = e / EXT_TILE, j = e - s * EXT_TILE;
       if (j < nrow) dst[(long long)s * sbn + x0 + j] = tile[s * (EXT_TILE + 1) + j];
     }
     __syncthreads();
-    rows_done_here += nrow;
   }
-  if (c.counters && threadIdx.x == 0) {
-    const unsigned long long ent = rows_done_here * r;
-    const unsigned long long upd = rows_done_here * r * (r - 1) / 2;
-    atomicAdd(&c.counters[CNT_EVALS], ent);
-    atomicAdd(&c.counters[CNT_SB_ENTRIES], ent);
-    atomicAdd(&c.counters[CNT_EXT_ENTRIES], ent);
-    atomicAdd(&c.counters[CNT_SB_UPDATES], upd);
-    atomicAdd(&c.counters[CNT_EXT_UPDATES], upd);
-  }
+  ent += (unsigned long long)(x_hi - x_lo) * r;
+  upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
+}
+
+// dynamic shared memory of phase 2: coef [cap][cap] + tile [cap][EXT_TILE + 1]
+__host__ __device__ __forceinline__ long long extend_smem_doubles(int cap) {
+  return (long long)cap * cap + (long long)cap * (EXT_TILE + 1);
 }
 
 // ---------------------------------------------------------------------------------------
-// k_greedy: one cluster of G CTAs per superblock
+// k_sweep phase 3 (Alg. 2): helpers
 // ---------------------------------------------------------------------------------------
 #define GREEDY_MAX_THREADS 512
 #define STAGE_N 1024  // n up to which the n-indexed factor of a step is staged in shared memory
@@ -419,15 +369,16 @@ __device__ __forceinline__ void cluster_argmax(GreedySmem& S, cg::cluster_group&
   __syncthreads();
 }
 
-// dynamic shared memory of the CACHED variant: own rows' U[t][x], SA, PA and own columns'
-// V[t][y], SB, PB stay on chip for the whole launch, plus the E / raw values of the last steps
+// dynamic shared memory of the CACHED variant (phase 3): own rows' U[t][x], SA, PA and own
+// columns' V[t][y], SB, PB stay on chip for the whole rook search, plus the E / raw values of
+// the last steps.  Phase 2 uses the same buffer first.
 __host__ __device__ __forceinline__ long long greedy_cache_doubles(long long rpcap, int cap) {
   // U[cap-1] Ecol Acol SA(2) PA(3) | V[cap-1] Erow SB(2) PB(3)
   return rpcap * ((cap - 1) + 1 + 1 + 2 + 3 + (cap - 1) + 1 + 2 + 3);
 }
 
 template <int FAMILY, bool CACHED, int THREADS>
-__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_greedy(DevCtx c, int sweep) {
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int sweep) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
@@ -476,7 +427,67 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_greedy(DevCtx c, int
     S.xs[tid] = px;
     S.ys[tid] = py;
   }
+  const int rows_done = c.sbstate[job * 4 + 0], cols_done = c.sbstate[job * 4 + 1];
+  const bool first = rows_done == 0 && cols_done == 0;
   __syncthreads();
+  unsigned long long ext_ent = 0, ext_upd = 0;
+
+  // ---- phase 1: factor tables of the new left slots [rows_done, rl) and right slots
+  // [cols_done, rr); every CTA of the cluster takes a strided share of the nodes a
+  for (int slot = rows_done; slot < rl; ++slot) {
+    sb_side_tables(c, job, 0, slot, cr * T, G * T);
+    __syncthreads();
+  }
+  for (int slot = cols_done; slot < rr; ++slot) {
+    sb_side_tables(c, job, 1, slot, cr * T, G * T);
+    __syncthreads();
+  }
+  if (FAMILY == 1) {
+    // CX for the new pairs: new alpha x all beta, then old alpha x new beta
+    const long long na = (long long)(rl - rows_done) * rr, nb = (long long)rows_done * (rr - cols_done);
+    for (long long e = (long long)cr * T + tid; e < na + nb; e += (long long)G * T) {
+      int al, be;
+      if (e < na) { al = rows_done + (int)(e / rr); be = (int)(e % rr); }
+      else { const long long f = e - na; al = (int)(f / (rr - cols_done)); be = cols_done + (int)(f % (rr - cols_done)); }
+      sb_cx_table(c, job, al, be);
+    }
+  }
+  cl.sync();  // tables visible to the whole cluster
+
+  // ---- phase 2: u / v of the existing pivots on the new rows and columns
+  {
+    __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
+    __shared__ double pdiag[TTC_MAX_RANK_DEV];
+    double* coef = dyn;
+    double* tile = dyn + (long long)cap * cap;
+    const long long nr_new = (long long)(rl - rows_done) * n, nc_new = (long long)(rr - cols_done) * n;
+    const long long rchunk = (nr_new + G - 1) / G, cchunk = (nc_new + G - 1) / G;
+    // rows: fixed index = pivot columns y_s
+    if (tid < r) {
+      p_al[tid] = S.ys[tid] / n;
+      p_a[tid] = S.ys[tid] - (S.ys[tid] / n) * n;
+    }
+    __syncthreads();
+    {
+      const long long lo = (long long)rows_done * n + (long long)cr * rchunk;
+      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, (long long)rl * n), p_al, p_a, pdiag, coef, tile,
+                          ext_ent, ext_upd);
+    }
+    __syncthreads();
+    // columns: fixed index = pivot rows x_s, divisors u_s(x_s) (A(t0) at the first sweep)
+    if (tid < r) {
+      p_al[tid] = S.xs[tid] / n;
+      p_a[tid] = S.xs[tid] - (S.xs[tid] / n) * n;
+      pdiag[tid] = first ? *c.p0val : U[(long long)tid * sbn + S.xs[tid]];
+    }
+    __syncthreads();
+    {
+      const long long lo = (long long)cols_done * n + (long long)cr * cchunk;
+      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, (long long)rr * n), p_al, p_a, pdiag, coef, tile,
+                          ext_ent, ext_upd);
+    }
+  }
+  cl.sync();  // u / v of the new rows and columns visible to the whole cluster
 
   bool active = r < cap;
   const double p0 = U[S.xs[0]];  // u_0(x_0) = A(x_0, y_0)
@@ -724,11 +735,15 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_greedy(DevCtx c, int
     c.sbstate[job * 4 + 1] = rr;
   }
   if (c.counters && tid == 0) {
+    evals += ext_ent;
+    upd += ext_upd;
     if (evals) {
       atomicAdd(&c.counters[CNT_EVALS], evals);
       atomicAdd(&c.counters[CNT_SB_ENTRIES], evals);
     }
     if (upd) atomicAdd(&c.counters[CNT_SB_UPDATES], upd);
+    if (ext_ent) atomicAdd(&c.counters[CNT_EXT_ENTRIES], ext_ent);
+    if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
   if (G > 1) cl.sync();  // no CTA may exit while another can still read its shared memory
