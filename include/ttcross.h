@@ -127,6 +127,9 @@ int tt_cross_commit(ttc_ctx* ctx);
  * PAR[k][0..cap)[0..2)]), where chunk = ceil((d-1)/world) interfaces are owned by each rank,
  * rank p owning records [p*chunk, (p+1)*chunk).  *bytes_per_rank = chunk*(1+cap*d+2*cap)*4.
  * An in-place all-gather of this buffer completes a sweep (Alg. 6 lines 6-8).
+ * For world > 1 the buffer stays at the same address for the life of the context
+ * (tt_cross_commit copies it into the current records); for world == 1 commit swaps the
+ * two record buffers, so re-query the pointer after every commit.
  */
 int tt_cross_exchange_buffer(ttc_ctx* ctx, void** dev_ptr, int64_t* bytes_total,
                              int64_t* bytes_per_rank);

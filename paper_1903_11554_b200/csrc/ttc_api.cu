@@ -206,7 +206,13 @@ int do_sweep_local(ttc_ctx* c) {
 
 int do_commit(ttc_ctx* c) {
   if (!c->pending) return fail(TTC_ERR_STATE, "tt_cross_commit without a pending local sweep");
-  std::swap(c->dc.rec_cur, c->dc.rec_next);
+  if (c->cfg.world == 1) {
+    std::swap(c->dc.rec_cur, c->dc.rec_next);
+  } else {
+    // keep the exchange buffer at a fixed address for the caller's collectives
+    CK(cudaMemcpyAsync(c->dc.rec_cur, c->dc.rec_next, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice,
+                       c->ls));
+  }
   c->pending = 0;
   c->sweeps++;
   return TTC_OK;

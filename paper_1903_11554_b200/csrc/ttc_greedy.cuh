@@ -461,28 +461,32 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     double* coef = dyn;
     double* tile = dyn + (long long)cap * cap;
     const long long nr_new = (long long)(rl - rows_done) * n, nc_new = (long long)(rr - cols_done) * n;
-    const long long rchunk = (nr_new + G - 1) / G, cchunk = (nc_new + G - 1) / G;
-    // rows: fixed index = pivot columns y_s
-    if (tid < r) {
-      p_al[tid] = S.ys[tid] / n;
-      p_a[tid] = S.ys[tid] - (S.ys[tid] / n) * n;
-    }
-    __syncthreads();
-    {
-      const long long lo = (long long)rows_done * n + (long long)cr * rchunk;
+    // with G >= 2 the first half of the cluster extends the rows, the second half the columns
+    // (independent: the column recurrence reads u only at old pivot rows, or A(t0) at the
+    // first sweep), so the two latency chains overlap
+    const int gr = G >= 2 ? G / 2 : 1, gc = G >= 2 ? G - gr : 1;
+    const bool do_rows = G == 1 || cr < gr, do_cols = G == 1 || cr >= gr;
+    const int rr_i = G == 1 ? 0 : cr, cc_i = G == 1 ? 0 : cr - gr;
+    const long long rchunk = (nr_new + gr - 1) / gr, cchunk = (nc_new + gc - 1) / gc;
+    if (do_rows) {   // rows: fixed index = pivot columns y_s
+      if (tid < r) {
+        p_al[tid] = S.ys[tid] / n;
+        p_a[tid] = S.ys[tid] - (S.ys[tid] / n) * n;
+      }
+      __syncthreads();
+      const long long lo = (long long)rows_done * n + (long long)rr_i * rchunk;
       extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, (long long)rl * n), p_al, p_a, pdiag, coef, tile,
                           ext_ent, ext_upd);
+      __syncthreads();
     }
-    __syncthreads();
-    // columns: fixed index = pivot rows x_s, divisors u_s(x_s) (A(t0) at the first sweep)
-    if (tid < r) {
-      p_al[tid] = S.xs[tid] / n;
-      p_a[tid] = S.xs[tid] - (S.xs[tid] / n) * n;
-      pdiag[tid] = first ? *c.p0val : U[(long long)tid * sbn + S.xs[tid]];
-    }
-    __syncthreads();
-    {
-      const long long lo = (long long)cols_done * n + (long long)cr * cchunk;
+    if (do_cols) {   // columns: fixed index = pivot rows x_s, divisors u_s(x_s) (A(t0) at first)
+      if (tid < r) {
+        p_al[tid] = S.xs[tid] / n;
+        p_a[tid] = S.xs[tid] - (S.xs[tid] / n) * n;
+        pdiag[tid] = first ? *c.p0val : U[(long long)tid * sbn + S.xs[tid]];
+      }
+      __syncthreads();
+      const long long lo = (long long)cols_done * n + (long long)cc_i * cchunk;
       extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, (long long)rr * n), p_al, p_a, pdiag, coef, tile,
                           ext_ent, ext_upd);
     }
