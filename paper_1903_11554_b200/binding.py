@@ -27,6 +27,7 @@ EXPORTS = [
     "tt_integrate_read", "tt_integrate_local", "tt_integrate_partials_buffer", "tt_integrate_finish",
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
     "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info", "tt_cross_get_launch_shape",
+    "tt_cross_get_phase_times",
 ]
 N_KERNELS = 13
 
@@ -79,6 +80,7 @@ def load(path: str = LIB_PATH):
         "tt_cross_set_timing": (i32, [P, i32]),
         "tt_cross_destroy": (None, [P]),
         "tt_cross_load_grid": (i32, [P, P, P, i32]),
+        "tt_cross_get_phase_times": (i32, [P, P, i32]),
         "tt_cross_get_launch_shape": (i32, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                                             ctypes.POINTER(i64)]),
         "tt_cross_get_kernel_time": (i32, [P, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64),
@@ -251,6 +253,14 @@ class TTCross:
         _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
         return {f: getattr(s, f) for f, _ in TtcStats._fields_ if f != "pad"}
 
+
+    def phase_times(self):
+        """k_sweep phase clocks (us, first superblock's CTA 0) accumulated while timing is on."""
+        out = np.zeros(8)
+        _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), 8),
+               "tt_cross_get_phase_times")
+        names = ["prologue", "tables", "extend", "samples", "rook", "final", "exit", "launches"]
+        return dict(zip(names, out.tolist()))
 
     def launch_shape(self):
         g, t, ca, sm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()

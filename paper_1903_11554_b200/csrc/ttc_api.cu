@@ -67,6 +67,7 @@ struct ttc_ctx {
   int sweeps = 0;
   int pending = 0;  // a local sweep waits for commit
   int* t0buf = nullptr;
+  unsigned long long* phase_buf = nullptr;  // k_sweep phase timer (enabled with timing)
   int sms = 148;               // multiprocessors of the device
   bool greedy_cached = false;  // k_sweep keeps its rows' u / columns' v in shared memory
   size_t greedy_smem = 0;      // dynamic shared memory of k_sweep
@@ -480,7 +481,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.pf, (size_t)c->slots * cap * cap)) ||
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
-      (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) ||
+      (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_NPHASES)) ||
       (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)))
     return bail(e);
   if (k.family == TTC_FAMILY_D) {
@@ -549,12 +550,14 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     auto smem_for = [&](int g, bool cached) -> size_t {
       return std::max(ext_bytes, cached ? cache_for(g) : (size_t)0);
     };
+    // T = threads per CTA; kernels are compiled for 256 (two CTAs per SM) and 512 (one)
     auto fn_for = [&](bool cached) -> const void* {
+      const bool big = T > 256;
       if (k.family == TTC_FAMILY_C)
-        return T == 512 ? (cached ? (const void*)k_sweep<0, true, 512> : (const void*)k_sweep<0, false, 512>)
-                        : (cached ? (const void*)k_sweep<0, true, 256> : (const void*)k_sweep<0, false, 256>);
-      return T == 512 ? (cached ? (const void*)k_sweep<1, true, 512> : (const void*)k_sweep<1, false, 512>)
-                      : (cached ? (const void*)k_sweep<1, true, 256> : (const void*)k_sweep<1, false, 256>);
+        return big ? (cached ? (const void*)k_sweep<0, true, 512> : (const void*)k_sweep<0, false, 512>)
+                   : (cached ? (const void*)k_sweep<0, true, 256> : (const void*)k_sweep<0, false, 256>);
+      return big ? (cached ? (const void*)k_sweep<1, true, 512> : (const void*)k_sweep<1, false, 512>)
+                 : (cached ? (const void*)k_sweep<1, true, 256> : (const void*)k_sweep<1, false, 256>);
     };
     // resident clusters for (G, cached)
     auto resident = [&](int g, bool cached) -> int {
@@ -585,6 +588,17 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       if (G == 1) { cached = false; break; }
     }
     dc.G = G;
+    // the block size covers a CTA's rows/columns at full rank in one pass when that takes at
+    // most 512 threads (the 512-thread variant is launched with fewer threads then)
+    {
+      const long long per = (dc.sbn + G - 1) / G;
+      const int want = (int)std::min<long long>(512, ((per + 31) / 32) * 32);
+      if (!std::getenv("TTC_GREEDY_T") && want > T) {
+        const int Tsave = T;
+        T = want;
+        if (resident(G, cached) < nj) T = Tsave;
+      }
+    }
     c->greedy_threads = T;
     c->greedy_cached = cached;
     c->greedy_smem = smem_for(G, cached);
@@ -798,6 +812,19 @@ int tt_cross_get_launch_shape(ttc_ctx* c, int32_t* cluster, int32_t* threads, in
 int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   c->timing = enable != 0;
+  c->dc.phase_ns = c->timing ? c->phase_buf : nullptr;
+  if (c->timing) CK(cudaMemsetAsync(c->phase_buf, 0, TTC_NPHASES * sizeof(unsigned long long), c->stream));
+  return TTC_OK;
+}
+
+int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
+  if (!c || !us_out) return fail(TTC_ERR_ARG, "null argument");
+  if (count < TTC_NPHASES) return fail(TTC_ERR_ARG, "need 8 slots");
+  unsigned long long v[TTC_NPHASES] = {};
+  CK(cudaMemcpyAsync(v, c->phase_buf, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < TTC_NPHASES - 1; ++i) us_out[i] = v[i] * 1e-3;
+  us_out[TTC_NPHASES - 1] = (double)v[TTC_NPHASES - 1];
   return TTC_OK;
 }
 

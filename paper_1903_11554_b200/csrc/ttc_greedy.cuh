@@ -212,16 +212,17 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 }
 
 // ---------------------------------------------------------------------------------------
-// phase 2: u/v of the existing pivots on the rows / columns that are new this sweep.  A warp
-// owns one row at a time; lane s evaluates the raw entries A(x, y_s) (A(x_s, y)) for s = lane,
-// lane + 32, then the triangular recurrence runs column-oriented with shuffles:
+// phase 2: u/v of the existing pivots on the rows / columns that are new this sweep, in tiles
+// of EXT_TILE rows: (1) all raw entries A(x, y_s) (A(x_s, y)) of the tile at once, one per
+// thread, into shared memory -- the batched fiber evaluation; (2) a warp per row runs the
+// triangular recurrence column-oriented with shuffles:
 //   for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s]  (s > t)
 // -- per s the same operations in the same order as the oracle's row-oriented
 // u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s) (t ascending), hence the same bits.
 // Columns: v_t = acc_t / u_t(x_t) final; acc_s -= U[t][x_s] * v_t.
 // Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][EXT_TILE + 1].
 // ---------------------------------------------------------------------------------------
-#define EXT_TILE 16
+#define EXT_TILE 64
 
 template <int FAMILY>
 __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
@@ -241,22 +242,25 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
     }
     coef[t * cap + s] = v;
   }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
+  constexpr int TS = EXT_TILE + 1;
   double* dst = side == 0 ? U : V;
   for (long long x0 = x_lo; x0 < x_hi; x0 += EXT_TILE) {
     const int nrow = (int)min((long long)EXT_TILE, x_hi - x0);
-    for (int j = warp; j < nrow; j += nw) {
+    // (1) raw entries of the tile, one per thread
+    for (int e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+      const int s = e / nrow, j = e - s * nrow;
       const long long x = x0 + j;
       const int al = (int)(x / n), a = (int)(x - (long long)al * n);
-      double acc0 = 0.0, acc1 = 0.0;
-      if (lane < r)
-        acc0 = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[lane], p_a[lane])
-                         : sb_entry<FAMILY>(c, job, k, p_al[lane], p_a[lane], al, a);
-      if (lane + 32 < r)
-        acc1 = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[lane + 32], p_a[lane + 32])
-                         : sb_entry<FAMILY>(c, job, k, p_al[lane + 32], p_a[lane + 32], al, a);
+      tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                                   : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+    }
+    __syncthreads();
+    // (2) the recurrence, a warp per row
+    for (int j = warp; j < nrow; j += nw) {
+      double acc0 = lane < r ? tile[lane * TS + j] : 0.0;
+      double acc1 = lane + 32 < r ? tile[(lane + 32) * TS + j] : 0.0;
       for (int t = 0; t < r; ++t) {
         double f = __shfl_sync(0xffffffffu, t < 32 ? acc0 : acc1, t & 31);
         if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t final
@@ -265,13 +269,13 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
         if (lane > t) acc0 = __dsub_rn(acc0, __dmul_rn(f, coef[t * cap + lane]));
         if (lane + 32 > t && lane + 32 < r) acc1 = __dsub_rn(acc1, __dmul_rn(f, coef[t * cap + lane + 32]));
       }
-      if (lane < r) tile[lane * (EXT_TILE + 1) + j] = acc0;
-      if (lane + 32 < r) tile[(lane + 32) * (EXT_TILE + 1) + j] = acc1;
+      if (lane < r) tile[lane * TS + j] = acc0;
+      if (lane + 32 < r) tile[(lane + 32) * TS + j] = acc1;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < r * EXT_TILE; e += blockDim.x) {
-      const int s = e / EXT_TILE, j = e - s * EXT_TILE;
-      if (j < nrow) dst[(long long)s * sbn + x0 + j] = tile[s * (EXT_TILE + 1) + j];
+    for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
+      const int s = e / nrow, j = e - s * nrow;
+      dst[(long long)s * sbn + x0 + j] = tile[s * TS + j];
     }
     __syncthreads();
   }
@@ -369,12 +373,161 @@ __device__ __forceinline__ void cluster_argmax(GreedySmem& S, cg::cluster_group&
   __syncthreads();
 }
 
+// asynchronous global -> shared copies (LDGSTS): the whole cache fill is one round trip
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // dynamic shared memory of the CACHED variant (phase 3): own rows' U[t][x], SA, PA and own
 // columns' V[t][y], SB, PB stay on chip for the whole rook search, plus the E / raw values of
 // the last steps.  Phase 2 uses the same buffer first.
 __host__ __device__ __forceinline__ long long greedy_cache_doubles(long long rpcap, int cap) {
   // U[cap-1] Ecol Acol SA(2) PA(3) | V[cap-1] Erow SB(2) PB(3)
   return rpcap * ((cap - 1) + 1 + 1 + 2 + 3 + (cap - 1) + 1 + 2 + 3);
+}
+
+// everything a rook step needs (one per CTA, built once per launch)
+struct StepCtx {
+  const DevCtx* c;
+  GreedySmem* S;
+  int job, k, n, cap, r, rl, rr, tid, T;
+  long long xb, xe, yb, ye, sbn, rpcap, jo, jcx;
+  double *U, *V, *Araw, *Uc, *Ecol, *Acol, *Vc, *Erow;
+  ESum* SAc;
+  DDE* PAc;
+  ESum* SBc;
+  DDE* PBc;
+  const double *uk, *uk1;
+  bool stage_n;
+};
+
+// column step E(:, y) on this CTA's rows -> U[r][:] (or the row cache), raw values; returns
+// the thread's (|E|, row) candidate.  The factors that depend on the fixed column are staged
+// once per step: S.fs = SB[beta][b], S.fp = PB[beta][b], f_slot[alpha] = CX[alpha][beta] *
+// QL1[alpha][b], f_node[a] = QR0[beta][a].
+template <int FAMILY, bool CACHED>
+__device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_out, long long& bf_out) {
+  const DevCtx& c = *X.c;
+  GreedySmem& S = *X.S;
+  const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
+  const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, xb = X.xb, xe = X.xe, rpcap = X.rpcap;
+  const int be = y / n, b = y - (y / n) * n;
+  if (tid < r) S.vec[tid] = X.V[tid * sbn + y];
+  if (tid == 0) {
+    S.fs = c.SB[jo + (long long)be * n + b];
+    if (FAMILY == 1) S.fp = c.PB[jo + (long long)be * n + b];
+  }
+  if (FAMILY == 1) {
+    for (int al = tid; al < X.rl; al += T) {
+      DDE f = c.CX[jcx + (long long)al * cap + be];
+      dde_mul(f, c.QL1[jo + (long long)al * n + b]);
+      S.f_slot[al] = f;
+    }
+    if (X.stage_n)
+      for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + (long long)be * n + a];
+  }
+  __syncthreads();
+  const double ub = X.uk1[b];
+  double bv = -1.0;
+  long long bf = LLONG_MAX;
+  for (long long x = xb + tid; x < xe; x += T) {
+    const int al = (int)(x / n), a = (int)(x - (long long)al * n);
+    ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
+    esum_add(s, S.fs);
+    const double Sd = esum_round(s);
+    const double SS = __dmul_rn(Sd, Sd);
+    double raw;
+    if (FAMILY == 0) {
+      raw = __drcp_rn(SS);
+    } else {
+      DDE p = CACHED ? X.PAc[x - xb] : c.PA[jo + x];
+      dde_mul(p, S.fp);
+      dde_mul(p, S.f_slot[al]);
+      dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + (long long)be * n + a]);
+      dde_mul_d(p, rho(X.uk[a], ub));
+      raw = __ddiv_rn(dde_round(p), SS);
+    }
+    double e = raw;
+    if (CACHED)
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.Uc[t * rpcap + (x - xb)], S.vec[t]));
+    else
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.U[t * sbn + x], S.vec[t]));
+#pragma unroll 1
+    for (int t = 0; t < r; ++t)
+      if (S.xs[t] == x) e = 0.0;
+    if (CACHED) {
+      X.Acol[x - xb] = raw;
+      X.Ecol[x - xb] = e;
+    } else {
+      X.Araw[x] = raw;
+      X.U[r * sbn + x] = e;
+    }
+    if (cand_better(fabs(e), x, bv, bf)) { bv = fabs(e); bf = x; }
+  }
+  bv_out = bv;
+  bf_out = bf;
+}
+
+// row step E(x, :) on this CTA's columns -> V[r][:] (or the column cache); staged:
+// S.fs = SA[alpha][a], S.fp = PA[alpha][a], f_slot[beta] = CX[alpha][beta] * QR0[beta][a],
+// f_node[b] = QL1[alpha][b]
+template <int FAMILY, bool CACHED>
+__device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out, long long& bf_out) {
+  const DevCtx& c = *X.c;
+  GreedySmem& S = *X.S;
+  const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
+  const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, yb = X.yb, ye = X.ye, rpcap = X.rpcap;
+  const int al = x / n, a = x - (x / n) * n;
+  if (tid < r) S.vec[tid] = X.U[tid * sbn + x];
+  if (tid == 0) {
+    S.fs = c.SA[jo + x];
+    if (FAMILY == 1) S.fp = c.PA[jo + x];
+  }
+  if (FAMILY == 1) {
+    for (int be = tid; be < X.rr; be += T) {
+      DDE f = c.CX[jcx + (long long)al * cap + be];
+      dde_mul(f, c.QR0[jo + (long long)be * n + a]);
+      S.f_slot[be] = f;
+    }
+    if (X.stage_n)
+      for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + (long long)al * n + b];
+  }
+  __syncthreads();
+  const double ua = X.uk[a];
+  double bv = -1.0;
+  long long bf = LLONG_MAX;
+  for (long long y = yb + tid; y < ye; y += T) {
+    const int be = (int)(y / n), b = (int)(y - (long long)be * n);
+    ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
+    esum_add(s, S.fs);
+    const double Sd = esum_round(s);
+    const double SS = __dmul_rn(Sd, Sd);
+    double e;
+    if (FAMILY == 0) {
+      e = __drcp_rn(SS);
+    } else {
+      DDE p = CACHED ? X.PBc[y - yb] : c.PB[jo + y];
+      dde_mul(p, S.fp);
+      dde_mul(p, S.f_slot[be]);
+      dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + (long long)al * n + b]);
+      dde_mul_d(p, rho(ua, X.uk1[b]));
+      e = __ddiv_rn(dde_round(p), SS);
+    }
+    if (CACHED)
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));
+    else
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.V[t * sbn + y]));
+#pragma unroll 1
+    for (int t = 0; t < r; ++t)
+      if (S.ys[t] == y) e = 0.0;
+    if (CACHED) X.Erow[y - yb] = e;
+    else X.V[r * sbn + y] = e;
+    if (cand_better(fabs(e), y, bv, bf)) { bv = fabs(e); bf = y; }
+  }
+  bv_out = bv;
+  bf_out = bf;
 }
 
 template <int FAMILY, bool CACHED, int THREADS>
@@ -419,6 +572,15 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   ESum* SBc = reinterpret_cast<ESum*>(Erow + rpcap);  // [rpcap]
   DDE* PBc = reinterpret_cast<DDE*>(SBc + rpcap);     // [rpcap]
 
+  const bool timer = c.phase_ns && job == 0 && cr == 0 && tid == 0;
+  unsigned long long t_last = timer ? gtimer() : 0;
+  auto phase = [&](int ph) {
+    if (timer) {
+      const unsigned long long t = gtimer();
+      atomicAdd(&c.phase_ns[ph], t - t_last);
+      t_last = t;
+    }
+  };
   if (cr == 0)
     for (int t = tid; t < c.RS; t += T) Rn[t] = Rc[t];
   if (tid < r) {
@@ -434,13 +596,22 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
 
   // ---- phase 1: factor tables of the new left slots [rows_done, rl) and right slots
   // [cols_done, rr); every CTA of the cluster takes a strided share of the nodes a
-  for (int slot = rows_done; slot < rl; ++slot) {
-    sb_side_tables(c, job, 0, slot, cr * T, G * T);
-    __syncthreads();
-  }
-  for (int slot = cols_done; slot < rr; ++slot) {
-    sb_side_tables(c, job, 1, slot, cr * T, G * T);
-    __syncthreads();
+  {
+    // with G >= 2 the first half of the cluster builds the left tables, the second half the
+    // right ones; each CTA takes a strided share of the nodes a
+    const int gl = G >= 2 ? G / 2 : 1;
+    const bool do_l = G == 1 || cr < gl, do_r = G == 1 || cr >= gl;
+    const int il = G == 1 ? 0 : cr, ir = G == 1 ? 0 : cr - gl;
+    if (do_l)
+      for (int slot = rows_done; slot < rl; ++slot) {
+        sb_side_tables(c, job, 0, slot, il * T, gl * T);
+        __syncthreads();
+      }
+    if (do_r)
+      for (int slot = cols_done; slot < rr; ++slot) {
+        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T);
+        __syncthreads();
+      }
   }
   if (FAMILY == 1) {
     // CX for the new pairs: new alpha x all beta, then old alpha x new beta
@@ -453,6 +624,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     }
   }
   cl.sync();  // tables visible to the whole cluster
+  phase(PH_TABLES);
 
   // ---- phase 2: u / v of the existing pivots on the new rows and columns
   {
@@ -492,6 +664,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     }
   }
   cl.sync();  // u / v of the new rows and columns visible to the whole cluster
+  phase(PH_EXTEND);
 
   bool active = r < cap;
   const double p0 = U[S.xs[0]];  // u_0(x_0) = A(x_0, y_0)
@@ -508,23 +681,44 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
 
   if (active) {
     if (CACHED) {
+#pragma unroll 1
       for (long long e = tid; e < (long long)r * rpcap; e += T) {
         const int t = (int)(e / rpcap);
         const long long j = e - (long long)t * rpcap;
-        if (xb + j < xe) Uc[t * rpcap + j] = U[t * sbn + xb + j];
-        if (yb + j < ye) Vc[t * rpcap + j] = V[t * sbn + yb + j];
+        if (xb + j < xe) cp_async8(&Uc[t * rpcap + j], &U[t * sbn + xb + j]);
+        if (yb + j < ye) cp_async8(&Vc[t * rpcap + j], &V[t * sbn + yb + j]);
       }
+#pragma unroll 1
       for (long long j = tid; j < rpcap; j += T) {
         if (xb + j < xe) {
-          SAc[j] = c.SA[jo + xb + j];
-          if (FAMILY == 1) PAc[j] = c.PA[jo + xb + j];
+          const double* sa = reinterpret_cast<const double*>(&c.SA[jo + xb + j]);
+          double* da = reinterpret_cast<double*>(&SAc[j]);
+          cp_async8(da, sa);
+          cp_async8(da + 1, sa + 1);
+          if (FAMILY == 1) {
+            const double* pa = reinterpret_cast<const double*>(&c.PA[jo + xb + j]);
+            double* dp = reinterpret_cast<double*>(&PAc[j]);
+            cp_async8(dp, pa);
+            cp_async8(dp + 1, pa + 1);
+            cp_async8(dp + 2, pa + 2);
+          }
         }
         if (yb + j < ye) {
-          SBc[j] = c.SB[jo + yb + j];
-          if (FAMILY == 1) PBc[j] = c.PB[jo + yb + j];
+          const double* sb = reinterpret_cast<const double*>(&c.SB[jo + yb + j]);
+          double* db = reinterpret_cast<double*>(&SBc[j]);
+          cp_async8(db, sb);
+          cp_async8(db + 1, sb + 1);
+          if (FAMILY == 1) {
+            const double* pb = reinterpret_cast<const double*>(&c.PB[jo + yb + j]);
+            double* dp = reinterpret_cast<double*>(&PBc[j]);
+            cp_async8(dp, pb);
+            cp_async8(dp + 1, pb + 1);
+            cp_async8(dp + 2, pb + 2);
+          }
         }
       }
-      // visibility of the cache is provided by the __syncthreads of the first step
+      cp_async_wait_all();
+      // visibility of the cache to the other threads: the __syncthreads of the first step
     }
     // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically)
     {
@@ -539,6 +733,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         double e = sb_entry<FAMILY>(c, job, k, al, a, be, b);
         for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + sx], V[t * sbn + sy]));
         bool masked = false;
+#pragma unroll 1
         for (int t = 0; t < r; ++t) masked |= (S.xs[t] == sx) | (S.ys[t] == sy);
         if (masked) e = 0.0;
         if (cand_better(fabs(e), q, bv, bf)) { bv = fabs(e); bf = q; }
@@ -551,140 +746,45 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         evals += c.ns;
         upd += (unsigned long long)c.ns * r;
       }
+      phase(PH_SAMPLES);
     }
     // column step E(:, y) on this CTA's rows; returns the cluster argmax row when `search`.
     // The factors that depend on the fixed column are staged once per step:
     //   S.fs = SB[beta][b], S.fp = PB[beta][b], f_slot[alpha] = CX[alpha][beta]*QL1[alpha][b],
     //   f_node[a] = QR0[beta][a]
+    StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
+              U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n};
     auto column = [&](int y, bool search) -> int {
-      const int be = y / n, b = y - (y / n) * n;
-      if (tid < r) S.vec[tid] = V[tid * sbn + y];
-      if (tid == 0) {
-        S.fs = c.SB[jo + (long long)be * n + b];
-        if (FAMILY == 1) S.fp = c.PB[jo + (long long)be * n + b];
-      }
-      if (FAMILY == 1) {
-        for (int al = tid; al < rl; al += T) {
-          DDE f = c.CX[jcx + (long long)al * cap + be];
-          dde_mul(f, c.QL1[jo + (long long)al * n + b]);
-          S.f_slot[al] = f;
-        }
-        if (stage_n)
-          for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + (long long)be * n + a];
-      }
-      __syncthreads();
-      const double ub = uk1[b];
-      double bv = -1.0;
-      long long bf = LLONG_MAX;
-      for (long long x = xb + tid; x < xe; x += T) {
-        const int al = (int)(x / n), a = (int)(x - (long long)al * n);
-        ESum s = CACHED ? SAc[x - xb] : c.SA[jo + x];
-        esum_add(s, S.fs);
-        const double Sd = esum_round(s);
-        const double SS = __dmul_rn(Sd, Sd);
-        double raw;
-        if (FAMILY == 0) {
-          raw = __drcp_rn(SS);
-        } else {
-          DDE p = CACHED ? PAc[x - xb] : c.PA[jo + x];
-          dde_mul(p, S.fp);
-          dde_mul(p, S.f_slot[al]);
-          dde_mul(p, stage_n ? S.f_node[a] : c.QR0[jo + (long long)be * n + a]);
-          dde_mul_d(p, rho(uk[a], ub));
-          raw = __ddiv_rn(dde_round(p), SS);
-        }
-        double e = raw;
-        if (CACHED)
-          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(Uc[t * rpcap + (x - xb)], S.vec[t]));
-        else
-          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + x], S.vec[t]));
-        for (int t = 0; t < r; ++t)
-          if (S.xs[t] == x) e = 0.0;
-        if (CACHED) {
-          Acol[x - xb] = raw;
-          Ecol[x - xb] = e;
-        } else {
-          Araw[x] = raw;
-          U[r * sbn + x] = e;
-        }
-        if (cand_better(fabs(e), x, bv, bf)) { bv = fabs(e); bf = x; }
-      }
+      double bv;
+      long long bf;
+      column_eval<FAMILY, CACHED>(X, y, bv, bf);
       if (tid == 0) {
         evals += (unsigned long long)max(0LL, xe - xb);
         upd += (unsigned long long)max(0LL, xe - xb) * r;
       }
-      int win = -1;
-      if (search) {
-        cta_argmax(S, bv, bf);
-        cluster_argmax(S, cl, G, ph);
-        win = (int)S.best.idx;
-      } else {
+      if (!search) {
         __syncthreads();
+        return -1;
       }
-      return win;
+      cta_argmax(S, bv, bf);
+      cluster_argmax(S, cl, G, ph);
+      return (int)S.best.idx;
     };
-    // row step E(x, :) on this CTA's columns; staged: S.fs = SA[alpha][a], S.fp = PA[alpha][a],
-    //   f_slot[beta] = CX[alpha][beta]*QR0[beta][a], f_node[b] = QL1[alpha][b]
     auto row = [&](int x, bool search) -> int {
-      const int al = x / n, a = x - (x / n) * n;
-      if (tid < r) S.vec[tid] = U[tid * sbn + x];
-      if (tid == 0) {
-        S.fs = c.SA[jo + x];
-        if (FAMILY == 1) S.fp = c.PA[jo + x];
-      }
-      if (FAMILY == 1) {
-        for (int be = tid; be < rr; be += T) {
-          DDE f = c.CX[jcx + (long long)al * cap + be];
-          dde_mul(f, c.QR0[jo + (long long)be * n + a]);
-          S.f_slot[be] = f;
-        }
-        if (stage_n)
-          for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + (long long)al * n + b];
-      }
-      __syncthreads();
-      const double ua = uk[a];
-      double bv = -1.0;
-      long long bf = LLONG_MAX;
-      for (long long y = yb + tid; y < ye; y += T) {
-        const int be = (int)(y / n), b = (int)(y - (long long)be * n);
-        ESum s = CACHED ? SBc[y - yb] : c.SB[jo + y];
-        esum_add(s, S.fs);
-        const double Sd = esum_round(s);
-        const double SS = __dmul_rn(Sd, Sd);
-        double e;
-        if (FAMILY == 0) {
-          e = __drcp_rn(SS);
-        } else {
-          DDE p = CACHED ? PBc[y - yb] : c.PB[jo + y];
-          dde_mul(p, S.fp);
-          dde_mul(p, S.f_slot[be]);
-          dde_mul(p, stage_n ? S.f_node[b] : c.QL1[jo + (long long)al * n + b]);
-          dde_mul_d(p, rho(ua, uk1[b]));
-          e = __ddiv_rn(dde_round(p), SS);
-        }
-        if (CACHED)
-          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], Vc[t * rpcap + (y - yb)]));
-        else
-          for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], V[t * sbn + y]));
-        for (int t = 0; t < r; ++t)
-          if (S.ys[t] == y) e = 0.0;
-        if (CACHED) Erow[y - yb] = e;
-        else V[r * sbn + y] = e;
-        if (cand_better(fabs(e), y, bv, bf)) { bv = fabs(e); bf = y; }
-      }
+      double bv;
+      long long bf;
+      row_eval<FAMILY, CACHED>(X, x, bv, bf);
       if (tid == 0) {
         evals += (unsigned long long)max(0LL, ye - yb);
         upd += (unsigned long long)max(0LL, ye - yb) * r;
       }
-      int win = -1;
-      if (search) {
-        cta_argmax(S, bv, bf);
-        cluster_argmax(S, cl, G, ph);
-        win = (int)S.best.idx;
-      } else {
+      if (!search) {
         __syncthreads();
+        return -1;
       }
-      return win;
+      cta_argmax(S, bv, bf);
+      cluster_argmax(S, cl, G, ph);
+      return (int)S.best.idx;
     };
     // ---- Alg. 2 lines 2-5: rook search
     int c_at = -1, g_at = -1;
@@ -699,6 +799,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
       yst = yn;
       if (conv) break;
     }
+    phase(PH_ROOK);
     if (c_at != yst) column(yst, false);
     if (g_at != xst) row(xst, false);
     if (CACHED) {   // the final column / row leave the chip once
@@ -706,6 +807,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         U[r * sbn + x] = Ecol[x - xb];
         Araw[x] = Acol[x - xb];
       }
+#pragma unroll 1
       for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
     }
     if (G > 1) cl.sync();  // U[r][:], V[r][:], Araw visible to the whole cluster
@@ -714,10 +816,12 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     raw_star = Araw[xst];
     if (fabs(pv) > c.tol * scale) {
       added = true;
+#pragma unroll 1
       for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = __ddiv_rn(V[r * sbn + y], pv);
     }
   }
 
+  phase(PH_FINAL);
   if (cr == 0 && tid == 0) {
     if (added) {
       const int al = xst / n, a = xst - al * n, be = yst / n, b = yst - be * n;
@@ -751,6 +855,8 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
   if (G > 1) cl.sync();  // no CTA may exit while another can still read its shared memory
+  phase(PH_END);
+  if (timer) atomicAdd(&c.phase_ns[PH_LAUNCHES], 1ULL);
 }
 
 }  // namespace ttc

@@ -1,0 +1,36 @@
+#!/usr/bin/env python
+"""Per-phase device time of k_sweep (globaltimer, first superblock's CTA 0) for workloads.
+Usage (GPU): python tools/probe_phases.py D5 C10 ..."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1903_11554_b200 import TTCross  # noqa: E402
+from workloads import WORKLOADS  # noqa: E402
+
+for name in sys.argv[1:] or ["D5"]:
+    wl = WORKLOADS[name]
+    u, w = wl.grid()
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    tt = TTCross(wl.family, torch.from_numpy(u).cuda(), torch.from_numpy(w).cuda(), wl.rank_cap, wl.tol,
+                 n_samples=wl.n_samples, rook_iters=wl.rook_iters, seed=wl.seed, stream=s.cuda_stream)
+    for _ in range(3):
+        tt.solve_launch(wl.alg6_sweeps, graph=True)
+        tt.integrate_read()
+    tt.set_timing(True)
+    tt.solve_launch(wl.alg6_sweeps, graph=False)
+    tt.integrate_read()
+    ph = tt.phase_times()
+    kt = tt.kernel_times()
+    tt.set_timing(False)
+    nl = max(1.0, ph.pop("launches"))
+    per = {k: round(v / nl, 2) for k, v in ph.items()}
+    print(json.dumps({"workload": name, "shape": tt.launch_shape(), "k_sweep_us": kt["k_sweep"][1] * 1e3 / kt["k_sweep"][0],
+                      "phase_us_per_launch": per, "rook_steps": tt.stats()["rook_steps"]}), flush=True)
+    tt.close()
