@@ -146,6 +146,12 @@ def roofline(kt, stats, family, peaks, peak_src):
         return out
     flops = ent * fpe + 2 * upd   # one multiply + one subtract per u_t(x) v_t(y) term
     tf = flops / avg_s / 1e12
+    if name == "k_sweep":
+        # memory side: every u_t(x) v_t(y) term reads one factor from memory (the other is
+        # staged), every entry writes its E (and the column its raw value) -- when the rook
+        # rows are not kept on chip this is HBM/L2 traffic
+        bytes_ = 8 * upd + 16 * ent
+        out["memory_GBs_if_uncached"] = bytes_ / avg_s / 1e9
     out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / FP64_PEAK_TFLOPS, "entries_per_launch": ent, "updates_per_launch": upd,
                 "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
