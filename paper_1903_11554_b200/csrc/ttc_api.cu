@@ -324,11 +324,6 @@ int resolve_timing(ttc_ctx* c) {
 int reset_device(ttc_ctx* c) {
   CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
   {
-    Timed t(c, K_INIT_PIVOT);
-    k_init_pivot<<<1, N_INIT, 0, c->ls>>>(c->dc, c->t0buf);
-  }
-  if (int e = check_launch("k_init_pivot")) return e;
-  {
     Timed t(c, K_INIT_RECORDS);
     k_init_records<<<std::max(c->nrec, c->n_owned), 128, 0, c->ls>>>(c->dc, c->t0buf, c->nrec, c->n_owned);
   }
@@ -627,6 +622,11 @@ int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights,
                                                              const_cast<long long*>(c->dc.clo), d * n);
   }
   if (int e = check_launch("k_prep_nodes")) return e;
+  {
+    Timed t(c, K_INIT_PIVOT);
+    k_init_pivot<<<1, N_INIT, 0, c->stream>>>(c->dc, c->t0buf);
+  }
+  if (int e = check_launch("k_init_pivot")) return e;
   return tt_cross_reset(c);
 }
 

@@ -55,7 +55,9 @@ __device__ double init_entry(const DevCtx& c, int q) {
   return __ddiv_rn(dde_round(p), SS);
 }
 
-// one block of N_INIT threads: t0 = first argmax |A| over the seeded samples -> t0buf[d]
+// one block of N_INIT threads: t0 = first argmax |A| over the seeded samples -> t0buf[d],
+// A(t0) -> p0val.  Part of loading a grid (tt_cross_init / tt_cross_load_grid): the start
+// depends only on the grid and the seed, so every solve of the same problem reuses it.
 __global__ void __launch_bounds__(N_INIT) k_init_pivot(DevCtx c, int* t0buf) {
   __shared__ double sv[N_INIT], sgn[N_INIT];
   __shared__ int best;
@@ -69,7 +71,6 @@ __global__ void __launch_bounds__(N_INIT) k_init_pivot(DevCtx c, int* t0buf) {
       if (sv[t] > sv[b]) b = t;
     best = b;
     *c.p0val = sgn[b];  // A(t0): u_0(x_0) of every superblock at the first sweep
-    if (c.counters) atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)N_INIT);
   }
   __syncthreads();
   for (int j = q; j < c.d; j += blockDim.x) t0buf[j] = init_coord(c, best, j);

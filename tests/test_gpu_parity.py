@@ -66,7 +66,7 @@ def quad_evals(prob, st):
 def check_run(tt, prob, sweeps, check_fibers=True, check_evals=True):
     st = X.initial_state(prob)
     assert_same_state(tt, st, "at init")
-    expect = X.N_INIT
+    expect = 0   # the rank-1 start (X.N_INIT evaluations) belongs to loading the grid
     prev_rows = [0] * (prob.d - 1)
     prev_cols = [0] * (prob.d - 1)
     for s in range(sweeps):
@@ -227,4 +227,18 @@ def test_large_configs_properties(lib, name):
             al, be, a = rng.integers(F.shape[0]), rng.integers(F.shape[1]), rng.integers(wl.n)
             idx = np.concatenate([L[al][:m], [a], R[be][m + 1:]])
             assert F[al, be, a] == ig.entries(wl.family, prob.u, idx[None, :])[0]
+    tt.close()
+
+
+@pytest.mark.parametrize("family,d,n,L,cap,sweeps", [
+    (FAMILY_C, 1000, 9, 4.0, 3, 2),      # d near the paper's largest (C_1024), C family
+    (FAMILY_D, 24, 1024, 30.0, 4, 2),    # 276 pairs per entry; n >> d^2 so that seeded samples avoid A = 0
+    (FAMILY_C, 3, 4096, 30.0, 2, 2),     # maximum n
+    (FAMILY_C, 2, 64, 8.0, 64, 3),       # rank cap = grid size along the single interface
+])
+def test_parity_extreme_sizes(lib, family, d, n, L, cap, sweeps):
+    """Size limits: pivots, parents and ranks bit-exact against the oracle after every sweep,
+    eval counter, and a nonsingular quadrature."""
+    tt, prob = make(family, d, n, L, cap, 1e-12, 8, 2, 17)
+    check_run(tt, prob, sweeps, check_fibers=(d <= 40))
     tt.close()
