@@ -208,7 +208,9 @@ int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, 
 /* tt_cross_get_phase_times -- with timing enabled, k_sweep's first CTA of the first owned
  * superblock accumulates its phases (globaltimer): us_out[0..6] = microseconds spent in
  * [prologue, tables, u/v extension, samples, rook search, final column/row + append, exit
- * barrier], us_out[7] = launches measured.  count >= 8.  Reset by tt_cross_set_timing(1). */
+ * barrier], us_out[7] = launches measured, us_out[8..11] = [column evaluation, column argmax
+ * (CTA + cluster), row evaluation, row argmax] summed over the search steps.  count >= 12.
+ * Reset by tt_cross_set_timing(1). */
 int tt_cross_get_phase_times(ttc_ctx* ctx, double* us_out, int32_t count);
 
 /* tt_cross_set_timing -- 1: bracket every kernel launch with CUDA events on the context

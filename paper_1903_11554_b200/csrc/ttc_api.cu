@@ -441,6 +441,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.ke = c->ke;
   dc.RS = 1 + cap * d + 2 * cap;
   dc.sbn = (long long)cap * n;
+  dc.ext_tile = extend_tile_rows(cap);
   dc.G = 1;  // cluster size of k_sweep, chosen below once the device is known
   c->slots = d;
   c->nrec = k.world * c->chunk;
@@ -819,12 +820,11 @@ int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
 
 int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
   if (!c || !us_out) return fail(TTC_ERR_ARG, "null argument");
-  if (count < TTC_NPHASES) return fail(TTC_ERR_ARG, "need 8 slots");
+  if (count < TTC_NPHASES) return fail(TTC_ERR_ARG, "need 12 slots");
   unsigned long long v[TTC_NPHASES] = {};
   CK(cudaMemcpyAsync(v, c->phase_buf, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (int i = 0; i < TTC_NPHASES - 1; ++i) us_out[i] = v[i] * 1e-3;
-  us_out[TTC_NPHASES - 1] = (double)v[TTC_NPHASES - 1];
+  for (int i = 0; i < TTC_NPHASES; ++i) us_out[i] = i == PH_LAUNCHES ? (double)v[i] : v[i] * 1e-3;
   return TTC_OK;
 }
 

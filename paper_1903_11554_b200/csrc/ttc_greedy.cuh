@@ -50,7 +50,7 @@ __device__ double init_entry(const DevCtx& c, int q) {
   DDE p = dde_one();
   for (int i = 0; i < d; ++i) {
     const double ui = c.u[i * n + init_coord(c, q, i)];
-    for (int j = i + 1; j < d; ++j) dde_mul_d(p, rho(ui, c.u[j * n + init_coord(c, q, j)]));
+    for (int j = i + 1; j < d; ++j) dde_mul_d(p, rho_ool(ui, c.u[j * n + init_coord(c, q, j)]));
   }
   return __ddiv_rn(dde_round(p), SS);
 }
@@ -138,7 +138,7 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int
     if (c.family == 1)
       for (int a = lo; a < hi; ++a) {
         const double ua = c.u[a * n + T[a]];
-        for (int b = a + 1; b < hi; ++b) dde_mul_d(p, rho(ua, c.u[b * n + T[b]]));
+        for (int b = a + 1; b < hi; ++b) dde_mul_d(p, rho_ool(ua, c.u[b * n + T[b]]));
       }
     sS = s;
     sP = p;
@@ -157,8 +157,8 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int
       DDE p = sP, q = dde_one();
       for (int t = lo; t < hi; ++t) {
         const double x = c.u[t * n + T[t]];
-        dde_mul_d(p, rho(uo, x));
-        dde_mul_d(q, rho(ux, x));
+        dde_mul_d(p, rho_ool(uo, x));
+        dde_mul_d(q, rho_ool(ux, x));
       }
       if (side == 0) { c.PA[o + a] = p; c.QL1[o + a] = q; }
       else { c.PB[o + a] = p; c.QR0[o + a] = q; }
@@ -178,7 +178,7 @@ __device__ void sb_cx_table(const DevCtx& c, int job, int al, int be) {
     const int* TY = rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d;
     for (int i = 0; i < k; ++i) {
       const double ui = c.u[i * n + TX[i]];
-      for (int j = k + 2; j < d; ++j) dde_mul_d(p, rho(ui, c.u[j * n + TY[j]]));
+      for (int j = k + 2; j < d; ++j) dde_mul_d(p, rho_ool(ui, c.u[j * n + TY[j]]));
     }
   }
   c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
@@ -215,15 +215,16 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // phase 2: u/v of the existing pivots on the rows / columns that are new this sweep, in tiles
 // of EXT_TILE rows: (1) all raw entries A(x, y_s) (A(x_s, y)) of the tile at once, one per
-// thread, into shared memory -- the batched fiber evaluation; (2) a warp per row runs the
-// triangular recurrence column-oriented with shuffles:
+// thread, into shared memory -- the batched fiber evaluation; (2) a thread per row runs the
+// triangular recurrence column-oriented:
 //   for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s]  (s > t)
 // -- per s the same operations in the same order as the oracle's row-oriented
 // u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s) (t ascending), hence the same bits.
 // Columns: v_t = acc_t / u_t(x_t) final; acc_s -= U[t][x_s] * v_t.
-// Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][EXT_TILE + 1].
+// Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][c.ext_tile + 1].
 // ---------------------------------------------------------------------------------------
-#define EXT_TILE 64
+// rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
+#define EXT_SMEM_DOUBLES 8192
 
 template <int FAMILY>
 __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
@@ -243,12 +244,10 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
     }
     coef[t * cap + s] = v;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  constexpr int TS = EXT_TILE + 1;
+  const int tile_rows = c.ext_tile, TS = c.ext_tile + 1;
   double* dst = side == 0 ? U : V;
-  for (long long x0 = x_lo; x0 < x_hi; x0 += EXT_TILE) {
-    const int nrow = (int)min((long long)EXT_TILE, x_hi - x0);
+  for (long long x0 = x_lo; x0 < x_hi; x0 += tile_rows) {
+    const int nrow = (int)min((long long)tile_rows, x_hi - x0);
     // (1) raw entries of the tile, one per thread
     for (int e = threadIdx.x; e < nrow * r; e += blockDim.x) {
       const int s = e / nrow, j = e - s * nrow;
@@ -258,20 +257,17 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
                                    : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
     }
     __syncthreads();
-    // (2) the recurrence, a warp per row
-    for (int j = warp; j < nrow; j += nw) {
-      double acc0 = lane < r ? tile[lane * TS + j] : 0.0;
-      double acc1 = lane + 32 < r ? tile[(lane + 32) * TS + j] : 0.0;
+    // (2) the recurrence, a thread per row, column-oriented (t outer, s > t inner): for every
+    // s the same subtractions in the same t order as the oracle's row-oriented sum
+    for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
       for (int t = 0; t < r; ++t) {
-        double f = __shfl_sync(0xffffffffu, t < 32 ? acc0 : acc1, t & 31);
-        if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t final
-        if (t < 32 && lane == t) acc0 = f;
-        if (t >= 32 && lane == t - 32) acc1 = f;
-        if (lane > t) acc0 = __dsub_rn(acc0, __dmul_rn(f, coef[t * cap + lane]));
-        if (lane + 32 > t && lane + 32 < r) acc1 = __dsub_rn(acc1, __dmul_rn(f, coef[t * cap + lane + 32]));
+        double f = tile[t * TS + j];
+        if (side == 1) {
+          f = __ddiv_rn(f, pdiag[t]);  // v_t final
+          tile[t * TS + j] = f;
+        }
+        for (int q = t + 1; q < r; ++q) tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
       }
-      if (lane < r) tile[lane * TS + j] = acc0;
-      if (lane + 32 < r) tile[(lane + 32) * TS + j] = acc1;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
@@ -284,9 +280,13 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
   upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
 }
 
-// dynamic shared memory of phase 2: coef [cap][cap] + tile [cap][EXT_TILE + 1]
+// phase-2 tile rows and dynamic shared memory: coef [cap][cap] + tile [cap][rows + 1]
+__host__ __device__ __forceinline__ int extend_tile_rows(int cap) {
+  const long long rows = (EXT_SMEM_DOUBLES - (long long)cap * cap) / cap - 1;
+  return (int)(rows < 32 ? 32 : (rows > 256 ? 256 : rows));
+}
 __host__ __device__ __forceinline__ long long extend_smem_doubles(int cap) {
-  return (long long)cap * cap + (long long)cap * (EXT_TILE + 1);
+  return (long long)cap * cap + (long long)cap * (extend_tile_rows(cap) + 1);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -402,6 +402,8 @@ struct StepCtx {
   DDE* PBc;
   const double *uk, *uk1;
   bool stage_n;
+  unsigned long long rowmask, colmask;  // bit j: this thread's j-th row / column is a pivot's
+  bool timer;                           // phase clock owner (tt_cross_get_phase_times)
 };
 
 // column step E(:, y) on this CTA's rows -> U[r][:] (or the row cache), raw values; returns
@@ -433,8 +435,10 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   const double ub = X.uk1[b];
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  for (long long x = xb + tid; x < xe; x += T) {
+  int jrow = 0;
+  for (long long x = xb + tid; x < xe; x += T, ++jrow) {
     const int al = (int)(x / n), a = (int)(x - (long long)al * n);
+    const double ua = X.uk[a];
     ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
     esum_add(s, S.fs);
     const double Sd = esum_round(s);
@@ -447,7 +451,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[al]);
       dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + (long long)be * n + a]);
-      dde_mul_d(p, rho(X.uk[a], ub));
+      dde_mul_d(p, rho(ua, ub));
       raw = __ddiv_rn(dde_round(p), SS);
     }
     double e = raw;
@@ -455,9 +459,10 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.Uc[t * rpcap + (x - xb)], S.vec[t]));
     else
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.U[t * sbn + x], S.vec[t]));
-#pragma unroll 1
-    for (int t = 0; t < r; ++t)
-      if (S.xs[t] == x) e = 0.0;
+    bool piv = jrow < 64 && ((X.rowmask >> jrow) & 1ULL);   // a pivot row (E is exactly 0 there)
+    if (jrow >= 64)
+      for (int t = 0; t < r; ++t) piv |= (S.xs[t] == x);
+    if (piv) e = 0.0;
     if (CACHED) {
       X.Acol[x - xb] = raw;
       X.Ecol[x - xb] = e;
@@ -499,8 +504,10 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   const double ua = X.uk[a];
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  for (long long y = yb + tid; y < ye; y += T) {
+  int jcol = 0;
+  for (long long y = yb + tid; y < ye; y += T, ++jcol) {
     const int be = (int)(y / n), b = (int)(y - (long long)be * n);
+    const double ub = X.uk1[b];
     ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
     esum_add(s, S.fs);
     const double Sd = esum_round(s);
@@ -513,22 +520,64 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[be]);
       dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + (long long)al * n + b]);
-      dde_mul_d(p, rho(ua, X.uk1[b]));
+      dde_mul_d(p, rho(ua, ub));
       e = __ddiv_rn(dde_round(p), SS);
     }
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));
     else
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.V[t * sbn + y]));
-#pragma unroll 1
-    for (int t = 0; t < r; ++t)
-      if (S.ys[t] == y) e = 0.0;
+    bool piv = jcol < 64 && ((X.colmask >> jcol) & 1ULL);   // a pivot column
+    if (jcol >= 64)
+      for (int t = 0; t < r; ++t) piv |= (S.ys[t] == y);
+    if (piv) e = 0.0;
     if (CACHED) X.Erow[y - yb] = e;
     else X.V[r * sbn + y] = e;
     if (cand_better(fabs(e), y, bv, bf)) { bv = fabs(e); bf = y; }
   }
   bv_out = bv;
   bf_out = bf;
+}
+
+// CTA argmax + cluster argmax of (v, f) -> S->best, out of line (one copy of the shuffle
+// trees for all steps: the sweep kernel is instruction-cache bound).  ph alternates the
+// published candidate buffer between steps.
+__device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, int G, int ph) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_argmax(v, f);
+  if (lane == 0) S->red[warp] = {v, f};
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    double bv = lane < nw ? S->red[lane].val : -1.0;
+    long long bf = lane < nw ? S->red[lane].idx : LLONG_MAX;
+    warp_argmax(bv, bf);
+    if (lane == 0) {
+      S->best = {bv, bf};
+      if (G > 1) {
+        S->cand[ph] = {bv, bf};
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      }
+    }
+  }
+  if (G == 1) {
+    __syncthreads();
+    return;
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (warp == 0) {
+    double bv = -1.0;
+    long long bf = LLONG_MAX;
+    if (lane < G) {
+      const Cand* rc = cg::this_cluster().map_shared_rank(&S->cand[ph], lane);
+      bv = rc->val;
+      bf = rc->idx;
+    }
+    warp_argmax(bv, bf);
+    if (lane == 0) S->best = {bv, bf};
+  }
+  __syncthreads();
 }
 
 template <int FAMILY, bool CACHED, int THREADS>
@@ -739,7 +788,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         if (masked) e = 0.0;
         if (cand_better(fabs(e), q, bv, bf)) { bv = fabs(e); bf = q; }
       }
-      cta_argmax(S, bv, bf);
+      argmax_step(&S, bv, bf, 1, 0);   // CTA-local: every CTA drew the same samples
       const int q = (int)S.best.idx;
       xst = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
       yst = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
@@ -753,12 +802,22 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     // The factors that depend on the fixed column are staged once per step:
     //   S.fs = SB[beta][b], S.fp = PB[beta][b], f_slot[alpha] = CX[alpha][beta]*QL1[alpha][b],
     //   f_node[a] = QR0[beta][a]
+    // pivot rows / columns among this thread's first 64 rows / columns (a search beyond)
+    unsigned long long rowmask = 0, colmask = 0;
+    for (int t = 0; t < r; ++t) {
+      const long long x = S.xs[t], y = S.ys[t];
+      if (x >= xb && x < xe && (x - xb) % T == tid && (x - xb) / T < 64) rowmask |= 1ULL << ((x - xb) / T);
+      if (y >= yb && y < ye && (y - yb) % T == tid && (y - yb) / T < 64) colmask |= 1ULL << ((y - yb) / T);
+    }
     StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
-              U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n};
+              U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
+              timer};
     auto column = [&](int y, bool search) -> int {
       double bv;
       long long bf;
+      const unsigned long long t0 = timer ? gtimer() : 0;
       column_eval<FAMILY, CACHED>(X, y, bv, bf);
+      const unsigned long long t1 = timer ? gtimer() : 0;
       if (tid == 0) {
         evals += (unsigned long long)max(0LL, xe - xb);
         upd += (unsigned long long)max(0LL, xe - xb) * r;
@@ -767,14 +826,20 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         __syncthreads();
         return -1;
       }
-      cta_argmax(S, bv, bf);
-      cluster_argmax(S, cl, G, ph);
+      argmax_step(&S, bv, bf, G, ph);
+      if (timer) {
+        atomicAdd(&c.phase_ns[PH_COL_EVAL], t1 - t0);
+        atomicAdd(&c.phase_ns[PH_COL_ARGMAX], gtimer() - t1);
+      }
+      ph ^= 1;
       return (int)S.best.idx;
     };
     auto row = [&](int x, bool search) -> int {
       double bv;
       long long bf;
+      const unsigned long long t0 = timer ? gtimer() : 0;
       row_eval<FAMILY, CACHED>(X, x, bv, bf);
+      const unsigned long long t1 = timer ? gtimer() : 0;
       if (tid == 0) {
         evals += (unsigned long long)max(0LL, ye - yb);
         upd += (unsigned long long)max(0LL, ye - yb) * r;
@@ -783,26 +848,48 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
         __syncthreads();
         return -1;
       }
-      cta_argmax(S, bv, bf);
-      cluster_argmax(S, cl, G, ph);
+      argmax_step(&S, bv, bf, G, ph);
+      if (timer) {
+        atomicAdd(&c.phase_ns[PH_ROW_EVAL], t1 - t0);
+        atomicAdd(&c.phase_ns[PH_ROW_ARGMAX], gtimer() - t1);
+      }
+      ph ^= 1;
       return (int)S.best.idx;
     };
     // ---- Alg. 2 lines 2-5: rook search
+    // one call site per step kind (the kernel is instruction-cache bound): the loop runs
+    // the rook rounds, then at most one extra column and one extra row for the final pivot
     int c_at = -1, g_at = -1;
-    for (int it = 0; it < c.rook; ++it) {
-      const int xn = column(yst, true);
-      c_at = yst;
-      const int yn = row(xn, true);
-      g_at = xn;
-      steps += 1;
-      const bool conv = (yn == yst);
-      xst = xn;
-      yst = yn;
-      if (conv) break;
+    int it = 0;
+    bool done = c.rook == 0;
+    int stage = 0;  // 0: column, 1: row
+    while (true) {
+      if (stage == 0) {
+        const bool search = !done;
+        if (!search && c_at == yst) { stage = 1; continue; }
+        const int xn = column(yst, search);
+        c_at = yst;
+        if (search) xst = xn;
+        stage = 1;
+      } else {
+        const bool search = !done;
+        if (!search) {
+          if (g_at != xst) row(xst, false);
+          break;
+        }
+        const int yn = row(xst, true);
+        g_at = xst;
+        steps += 1;
+        const bool conv = (yn == yst);
+        yst = yn;
+        ++it;
+        if (conv || it >= c.rook) {
+          done = true;
+          phase(PH_ROOK);
+        }
+        stage = 0;
+      }
     }
-    phase(PH_ROOK);
-    if (c_at != yst) column(yst, false);
-    if (g_at != xst) row(xst, false);
     if (CACHED) {   // the final column / row leave the chip once
       for (long long x = xb + tid; x < xe; x += T) {
         U[r * sbn + x] = Ecol[x - xb];
