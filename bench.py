@@ -154,6 +154,8 @@ def roofline(kt, stats, family, peaks, peak_src):
         out["memory_GBs_if_uncached"] = bytes_ / avg_s / 1e9
     out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": tf / FP64_PEAK_TFLOPS, "entries_per_launch": ent, "updates_per_launch": upd,
+                "limiter": "latency: the dependent argmax chain of Alg. 2 (DESIGN.md 5b)" if name == "k_sweep"
+                else "throughput",
                 "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
                 "peak_source": "derived fp64 FMA peak: 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §6)"})
     return out

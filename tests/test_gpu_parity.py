@@ -242,3 +242,45 @@ def test_parity_extreme_sizes(lib, family, d, n, L, cap, sweeps):
     tt, prob = make(family, d, n, L, cap, 1e-12, 8, 2, 17)
     check_run(tt, prob, sweeps, check_fibers=(d <= 40))
     tt.close()
+
+
+@pytest.mark.parametrize("name,modes", [("D5", [0, 2, 4]), ("C10", [0, 5, 9]), ("D20", [1, 10, 19])])
+def test_theorem1_interpolation_of_gpu_cross(lib, name, modes):
+    """Theorem 1 on the CUDA path's own cross after the full bench
+    solve: eq. (3) built from the returned fibers and the intersection matrices (entries
+    from the oracle's integrand) reproduces sampled fiber entries A(I_{<=m-1}, i_m, I_{>m}).
+    Holds because every sweep kept the index sets nested; relative tolerance scales with
+    cond(M_k) (numpy fp64 solves)."""
+    wl = WORKLOADS[name]
+    tt, prob = make_wl(wl)
+    tt.solve_launch(wl.alg6_sweeps, graph=True)
+    tt.integrate_read()
+    ranks, piv = tt.state()
+    d = wl.d
+    st = X.State(piv, [np.zeros((len(p), 2), np.int64) for p in piv])
+    Ms = [X.intersection(prob, st, k) for k in range(d - 1)]
+    Fs = {}
+
+    def fib(m):
+        if m not in Fs:
+            Fs[m] = tt.fiber(m)
+        return Fs[m]
+
+    rng = np.random.default_rng(1)
+    for m in modes:
+        F = fib(m)
+        for _ in range(3):
+            al, be, a = rng.integers(F.shape[0]), rng.integers(F.shape[1]), rng.integers(wl.n)
+            L = piv[m - 1][al] if m > 0 else None
+            Rr = piv[m][be] if m < d - 1 else None
+            idx = np.concatenate([L[:m] if L is not None else [], [a], Rr[m + 1:] if Rr is not None else []]).astype(int)
+            # eq. (3) left to right: F_0[:, i_0, :] M_0^{-1} F_1[:, i_1, :] ... at idx
+            v = fib(0)[0, :, idx[0]]
+            for q in range(1, d):
+                v = np.linalg.solve(Ms[q - 1].T, v)
+                v = v @ fib(q)[:, :, idx[q]]
+            exact = F[al, be, a]
+            conds = max(np.linalg.cond(M) for M in Ms)
+            assert abs(float(v[0]) - exact) <= max(1e-10, 1e-15 * conds * d) * max(abs(exact), 1e-300) \
+                or abs(float(v[0]) - exact) <= 1e-13 * np.max(np.abs(F)), (m, float(v[0]), exact)
+    tt.close()
