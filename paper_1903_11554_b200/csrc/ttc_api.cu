@@ -76,7 +76,9 @@ struct ttc_ctx {
   // buffers
   std::vector<void*> allocs;
   long long rec_ints = 0;
-  double* partials = nullptr;  // [world][3 + 2*cap*cap] (see k_chain)
+  double* partials = nullptr;  // [world][3 + 2*cap*cap] (see k_chain_level)
+  DD *chainA = nullptr, *chainB = nullptr;  // tree-chain ping-pong items [d][cap][cap]
+  int *chainAd = nullptr, *chainBd = nullptr;  // their dims [d][3]
   double* out_dev = nullptr;   // [4]
   double* out_host = nullptr;  // pinned [8]
   // accounting
@@ -249,11 +251,39 @@ int do_integrate_local(ttc_ctx* c) {
     if (int e = check_launch("k_solve")) return e;
   }
   double* rec = c->partials + (long long)rank * chain_record_size(cap);
+  const int with_head = rank == 0 ? 1 : 0;
+  const int items = c->n_owned + with_head;
+  if (items == 0) {  // a rank without superblocks contributes an empty record
+    CK(cudaMemsetAsync(rec, 0, 3 * sizeof(double), c->ls));
+    return TTC_OK;
+  }
   {
     Timed t(c, K_CHAIN);
-    k_chain<<<1, 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc, c->kb, c->ke, rank == 0 ? 1 : 0, rec);
+    k_chain_init<<<items, 256, 0, c->ls>>>(dc, c->kb, c->ke, with_head, c->chainA, c->chainAd);
   }
-  return check_launch("k_chain");
+  if (int e = check_launch("k_chain_init")) return e;
+  DD* src = c->chainA;
+  int* sd = c->chainAd;
+  DD* dst = c->chainB;
+  int* dd_ = c->chainBd;
+  int count = items;
+  if (count == 1) {  // a single item: one level that only copies and emits the record
+    Timed t(c, K_CHAIN);
+    k_chain_level<<<1, 256, 0, c->ls>>>(cap, src, sd, 1, dst, dd_, rec, 1);
+    return check_launch("k_chain_level");
+  }
+  while (count > 1) {
+    const int out = (count + 1) / 2;
+    {
+      Timed t(c, K_CHAIN);
+      k_chain_level<<<out, 256, 0, c->ls>>>(cap, src, sd, count, dst, dd_, rec, out == 1 ? 1 : 0);
+    }
+    if (int e = check_launch("k_chain_level")) return e;
+    std::swap(src, dst);
+    std::swap(sd, dd_);
+    count = out;
+  }
+  return TTC_OK;
 }
 
 // enqueue k_finish and the D2H copy of the result into pinned host memory (no sync)
@@ -478,7 +508,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
       (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_NPHASES)) ||
-      (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)))
+      (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)) ||
+      (e = dalloc(c, &c->chainA, (size_t)(nj + 1) * cap * cap)) || (e = dalloc(c, &c->chainB, (size_t)(nj + 1) * cap * cap)) ||
+      (e = dalloc(c, &c->chainAd, (size_t)(nj + 1) * 3)) || (e = dalloc(c, &c->chainBd, (size_t)(nj + 1) * 3)))
     return bail(e);
   if (k.family == TTC_FAMILY_D) {
     if ((e = dalloc(c, &dc.ql, (size_t)c->slots * cap * n)) || (e = dalloc(c, &dc.qr, (size_t)c->slots * cap * n)) ||
@@ -506,7 +538,6 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     allow((const void*)k_sweep<1, true, 512>, 180 * 1024);
     const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
-    if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
   }
   {

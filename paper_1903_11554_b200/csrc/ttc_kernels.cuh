@@ -315,61 +315,93 @@ __device__ double block_absmax(double v, double* red) {
   return m;
 }
 
-// Partial product of the quadrature chain over interfaces [i_begin, i_end) (one CTA):
-//   with_head: V = W_0 (1 x r_0), else V = identity (r_{i_begin} x r_{i_begin});
-//   V <- V H_i for every i (double-double), renormalised by an exact power of two.
-// rows = 0 marks an empty record (a rank that owns no interface).
-__global__ void __launch_bounds__(256) k_chain(DevCtx c, int i_begin, int i_end, int with_head, double* rec) {
+// ---------------------------------------------------------------------------------------
+// tree-reduced chain: the rank's partial product W_0 H_kb ... H_{ke-1} (rank 0) or
+// H_kb ... H_{ke-1} (others) as a balanced binary tree of double-double matrix products,
+// ceil(log2(items)) launches instead of d sequential vector-matrix steps.  Each item carries
+// its dimensions and a power-of-two scale (exact), renormalised after every product so that
+// d = 200 neither overflows nor underflows.  The §4.1 product is associative; the tree only
+// changes the double-double rounding (R9).
+// item layout: DD [cap][cap] (row-major, stride cap) + int dims [3] = rows, cols, log2scale
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_chain_init(DevCtx c, int i_begin, int i_end, int with_head, DD* dst,
+                                                      int* ddim) {
   const int cap = c.cap, d = c.d;
-  extern __shared__ DD smc[];
-  DD* V = smc;               // [cap][cap]
-  DD* V2 = smc + cap * cap;  // [cap][cap]
-  __shared__ double red[256];
-  __shared__ long long lg2;
-  int rows, len;
-  if (!with_head && i_begin >= i_end) {
-    if (threadIdx.x == 0) { rec[0] = 0; rec[1] = 0; rec[2] = 0; }
-    return;
-  }
-  if (with_head) {
+  const int item = blockIdx.x;  // 0..count-1
+  int i;
+  int rows, cols;
+  const DD* src;
+  long long src_stride = cap;
+  if (with_head && item == 0) {
     rows = 1;
-    len = (d > 1) ? rec_rank(c.rec_cur, c.RS, 0) : 1;
-    for (int t = threadIdx.x; t < len; t += blockDim.x) V[t] = c.W[t];  // W_0, row 0
+    cols = (d > 1) ? rec_rank(c.rec_cur, c.RS, 0) : 1;
+    src = c.W;  // W_0, row 0
   } else {
-    rows = rec_rank(c.rec_cur, c.RS, i_begin);
-    len = rows;
-    for (int t = threadIdx.x; t < rows * rows; t += blockDim.x)
-      V[(t / rows) * cap + t % rows] = dd_make((t / rows == t % rows) ? 1.0 : 0.0);
+    i = i_begin + item - (with_head ? 1 : 0);
+    rows = rec_rank(c.rec_cur, c.RS, i);
+    cols = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+    src = c.H + (long long)i * cap * cap;
   }
-  if (threadIdx.x == 0) lg2 = 0;
-  __syncthreads();
-  for (int i = i_begin; i < i_end; ++i) {
-    const int nc = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
-    const DD* Hi = c.H + (long long)i * cap * cap;
+  DD* D = dst + (long long)item * cap * cap;
+  for (int t = threadIdx.x; t < rows * cols; t += blockDim.x) {
+    const int a = t / cols, b = t % cols;
+    D[a * cap + b] = src[a * src_stride + b];
+  }
+  if (threadIdx.x == 0) {
+    ddim[item * 3 + 0] = rows;
+    ddim[item * 3 + 1] = cols;
+    ddim[item * 3 + 2] = 0;
+  }
+}
+
+// dst[j] = src[2j] * src[2j+1] (or src[2j] if it has no partner); when `final` (one output
+// item), also write the chain record [rows, cols, log2scale, hi, lo]
+__global__ void __launch_bounds__(256) k_chain_level(int cap, const DD* src, const int* sdim, int count, DD* dst,
+                                                       int* ddim, double* rec, int final) {
+  __shared__ double red[256];
+  const int j = blockIdx.x, ia = 2 * j, ib = 2 * j + 1;
+  const DD* A = src + (long long)ia * cap * cap;
+  DD* C = dst + (long long)j * cap * cap;
+  const int p = sdim[ia * 3 + 0], q = sdim[ia * 3 + 1];
+  int s_, ex = 0;
+  long long lg = sdim[ia * 3 + 2];
+  if (ib >= count) {
+    s_ = q;
+    for (int t = threadIdx.x; t < p * q; t += blockDim.x) C[(t / q) * cap + t % q] = A[(t / q) * cap + t % q];
+  } else {
+    const DD* B = src + (long long)ib * cap * cap;
+    s_ = sdim[ib * 3 + 1];
+    lg += sdim[ib * 3 + 2];
     double mx = 0.0;
-    for (int t = threadIdx.x; t < rows * nc; t += blockDim.x) {
-      const int a = t / nc, col = t % nc;
+    for (int t = threadIdx.x; t < p * s_; t += blockDim.x) {
+      const int a = t / s_, col = t % s_;
       DD acc = dd_make(0.0);
-      for (int k = 0; k < len; ++k) acc = dd_add(acc, dd_mul(V[a * cap + k], Hi[k * cap + col]));
-      V2[a * cap + col] = acc;
+      for (int k = 0; k < q; ++k) acc = dd_add(acc, dd_mul(A[a * cap + k], B[k * cap + col]));
+      C[a * cap + col] = acc;
       mx = fmax(mx, fabs(acc.hi));
     }
     mx = block_absmax(mx, red);
-    int ex = 0;
     if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
-    for (int t = threadIdx.x; t < rows * nc; t += blockDim.x) {
-      const int a = t / nc, col = t % nc;
-      V[a * cap + col] = dd_ldexp(V2[a * cap + col], -ex);
-    }
-    if (threadIdx.x == 0) lg2 += ex;
-    len = nc;
     __syncthreads();
+    for (int t = threadIdx.x; t < p * s_; t += blockDim.x) {
+      const int a = t / s_, col = t % s_;
+      C[a * cap + col] = dd_ldexp(C[a * cap + col], -ex);
+    }
+    lg += ex;
   }
-  if (threadIdx.x == 0) { rec[0] = rows; rec[1] = len; rec[2] = (double)lg2; }
-  for (int t = threadIdx.x; t < rows * len; t += blockDim.x) {
-    const int a = t / len, col = t % len;
-    rec[3 + a * cap + col] = V[a * cap + col].hi;
-    rec[3 + (long long)cap * cap + a * cap + col] = V[a * cap + col].lo;
+  if (threadIdx.x == 0) {
+    ddim[j * 3 + 0] = p;
+    ddim[j * 3 + 1] = s_;
+    ddim[j * 3 + 2] = (int)lg;
+  }
+  if (final) {
+    __syncthreads();
+    if (threadIdx.x == 0) { rec[0] = p; rec[1] = s_; rec[2] = (double)lg; }
+    for (int t = threadIdx.x; t < p * s_; t += blockDim.x) {
+      const int a = t / s_, col = t % s_;
+      rec[3 + a * cap + col] = C[a * cap + col].hi;
+      rec[3 + (long long)cap * cap + a * cap + col] = C[a * cap + col].lo;
+    }
   }
 }
 
