@@ -72,7 +72,9 @@ struct ttc_ctx {
   bool greedy_cached = false;  // k_sweep keeps its rows' u / columns' v in shared memory
   size_t greedy_smem = 0;      // dynamic shared memory of k_sweep
   int greedy_threads = 256;    // CTA size of k_sweep (256: two CTAs per SM, 512: one)
-  const void* greedy_fn = nullptr;
+  const void* greedy_fn = nullptr;   // k_sweep variant (one sweep)
+  const void* sweeps_fn = nullptr;   // k_sweeps variant (persistent, world == 1)
+  bool persistent = false;           // k_sweeps usable (all clusters resident)
   // buffers
   std::vector<void*> allocs;
   long long rec_ints = 0;
@@ -207,6 +209,33 @@ int do_sweep_local(ttc_ctx* c) {
   return TTC_OK;
 }
 
+// n sweeps [c->sweeps, c->sweeps + n) in one persistent launch (world == 1)
+int do_sweeps_persistent(ttc_ctx* c, int n) {
+  if (n <= 0) return TTC_OK;
+  DevCtx& dc = c->dc;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(c->n_owned * dc.G);
+  lc.blockDim = dim3(c->greedy_threads);
+  lc.dynamicSmemBytes = c->greedy_smem;
+  lc.stream = c->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = dc.G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e;
+  {
+    Timed t(c, K_SWEEP);
+    e = cudaLaunchKernelEx(&lc, (void (*)(DevCtx, int, int))c->sweeps_fn, dc, c->sweeps, n);
+  }
+  if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweeps launch: ") + cudaGetErrorString(e));
+  if (int e2 = check_launch("k_sweeps")) return e2;
+  c->sweeps += n;
+  return TTC_OK;
+}
+
 int do_commit(ttc_ctx* c) {
   if (!c->pending) return fail(TTC_ERR_STATE, "tt_cross_commit without a pending local sweep");
   if (c->cfg.world == 1) {
@@ -237,7 +266,7 @@ int do_integrate_local(ttc_ctx* c) {
     }
     if (int e = check_launch("k_wsum")) return e;
   }
-  CK(cudaMemsetAsync(dc.flags, 0, 4 * sizeof(int), c->ls));
+  CK(cudaMemsetAsync(dc.flags, 0, sizeof(int), c->ls));  // flags[1] (sweep timeout) stays
   if (c->n_owned > 0) {
     {
       Timed t(c, K_INTERSECTION);
@@ -295,7 +324,7 @@ int do_integrate_finish_launch(ttc_ctx* c) {
   }
   if (int e = check_launch("k_finish")) return e;
   CK(cudaMemcpyAsync(c->out_host, c->out_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->ls));
-  CK(cudaMemcpyAsync(c->out_host + 2, c->dc.flags, sizeof(int), cudaMemcpyDeviceToHost, c->ls));
+  CK(cudaMemcpyAsync(c->out_host + 2, c->dc.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->ls));
   return TTC_OK;
 }
 
@@ -303,8 +332,10 @@ int do_integrate_finish_launch(ttc_ctx* c) {
 int do_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sign) {
   const int d = c->dc.d;
   CK(cudaStreamSynchronize(c->stream));
-  int flag = 0;
-  std::memcpy(&flag, c->out_host + 2, sizeof(int));
+  int flag = 0, flag2[2] = {0, 0};
+  std::memcpy(flag2, c->out_host + 2, 2 * sizeof(int));
+  flag = flag2[0];
+  if (flag2[1]) return fail(TTC_ERR_CUDA, "k_sweeps: a superblock waited > 2 s for a neighbour (clusters not co-resident)");
   if (flag) return fail(TTC_ERR_SINGULAR, "an intersection matrix A(I_{<=k}, I_{>k}) is singular");
   const double core = c->out_host[0];
   const double lg2 = c->out_host[1];
@@ -355,7 +386,8 @@ int reset_device(ttc_ctx* c) {
   CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
   {
     Timed t(c, K_INIT_RECORDS);
-    k_init_records<<<std::max(c->nrec, c->n_owned), 128, 0, c->ls>>>(c->dc, c->t0buf, c->nrec, c->n_owned);
+    k_init_records<<<std::max(std::max(c->nrec, c->n_owned), c->dc.d - 1), 128, 0, c->ls>>>(c->dc, c->t0buf, c->nrec,
+                                                                                      c->n_owned);
   }
   return check_launch("k_init_records");
 }
@@ -377,9 +409,13 @@ int do_reset(ttc_ctx* c) {
 
 // n_sweeps sweeps + the quadrature, enqueued on c->ls (world == 1)
 int enqueue_solve(ttc_ctx* c, int n_sweeps) {
-  for (int s = 0; s < n_sweeps; ++s) {
-    if (int e = do_sweep_local(c)) return e;
-    if (int e = do_commit(c)) return e;
+  if (c->persistent) {
+    if (int e = do_sweeps_persistent(c, n_sweeps)) return e;
+  } else {
+    for (int s = 0; s < n_sweeps; ++s) {
+      if (int e = do_sweep_local(c)) return e;
+      if (int e = do_commit(c)) return e;
+    }
   }
   if (int e = do_integrate_local(c)) return e;
   return do_integrate_finish_launch(c);
@@ -507,6 +543,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.pf, (size_t)c->slots * cap * cap)) ||
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
+      (e = dalloc(c, &dc.rank_ring, (size_t)2 * d)) || (e = dalloc(c, &dc.done, (size_t)d)) ||
       (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_NPHASES)) ||
       (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)) ||
       (e = dalloc(c, &c->chainA, (size_t)(nj + 1) * cap * cap)) || (e = dalloc(c, &c->chainB, (size_t)(nj + 1) * cap * cap)) ||
@@ -528,6 +565,14 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     };
+    allow((const void*)k_sweeps<0, false, 256>, 180 * 1024);
+    allow((const void*)k_sweeps<1, false, 256>, 180 * 1024);
+    allow((const void*)k_sweeps<0, true, 256>, 180 * 1024);
+    allow((const void*)k_sweeps<1, true, 256>, 180 * 1024);
+    allow((const void*)k_sweeps<0, false, 512>, 180 * 1024);
+    allow((const void*)k_sweeps<1, false, 512>, 180 * 1024);
+    allow((const void*)k_sweeps<0, true, 512>, 180 * 1024);
+    allow((const void*)k_sweeps<1, true, 512>, 180 * 1024);
     allow((const void*)k_sweep<0, false, 256>, 180 * 1024);
     allow((const void*)k_sweep<1, false, 256>, 180 * 1024);
     allow((const void*)k_sweep<0, true, 256>, 180 * 1024);
@@ -630,6 +675,17 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     c->greedy_cached = cached;
     c->greedy_smem = smem_for(G, cached);
     c->greedy_fn = fn_for(c->greedy_cached);
+    {
+      const bool big = T > 256;
+      if (k.family == TTC_FAMILY_C)
+        c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<0, true, 512> : (const void*)k_sweeps<0, false, 512>)
+                           : (cached ? (const void*)k_sweeps<0, true, 256> : (const void*)k_sweeps<0, false, 256>);
+      else
+        c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<1, true, 512> : (const void*)k_sweeps<1, false, 512>)
+                           : (cached ? (const void*)k_sweeps<1, true, 256> : (const void*)k_sweeps<1, false, 256>);
+      // the wavefront needs every cluster resident at once
+      c->persistent = k.world == 1 && resident(G, cached) >= nj && !std::getenv("TTC_NO_PERSISTENT");
+    }
   }
   int rc = tt_cross_load_grid(c, nodes_u, weights, mem_kind);
   if (rc) return bail(rc);
@@ -683,6 +739,7 @@ int tt_cross_sweep(ttc_ctx* c, int32_t n_sweeps) {
   if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_cross_sweep needs world == 1");
   if (n_sweeps < 0) return fail(TTC_ERR_ARG, "n_sweeps < 0");
   if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  if (c->persistent) return do_sweeps_persistent(c, n_sweeps);
   for (int s = 0; s < n_sweeps; ++s) {
     if (int e = do_sweep_local(c)) return e;
     if (int e = do_commit(c)) return e;

@@ -90,6 +90,11 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
       R[t] = v;
     }
   }
+  if (i < d - 1 && threadIdx.x == 0) {
+    c.rank_ring[2 * i] = 1;
+    c.rank_ring[2 * i + 1] = 1;
+    c.done[i] = 0;
+  }
   if (i < n_owned && threadIdx.x == 0) {
     c.sbstate[i * 4 + 0] = 0;
     c.sbstate[i * 4 + 1] = 0;
@@ -97,6 +102,7 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
     c.sbstate[i * 4 + 3] = 0;
     c.praw_max[i] = -1.0;
   }
+  if (i == 0 && threadIdx.x == 0) c.flags[1] = 0;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -110,7 +116,8 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 //                                QR0 = prod_{j>k+1} rho(u_k[a], Y_j)
 // blockIdx.z >= 2*jobs (family D): CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j)
 // for the new (alpha, beta) pairs, z = 2*jobs + job, y = alpha, x*128 + tid = beta.
-__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride) {
+__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride, int rl,
+                               int rr) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
   __shared__ ESum sS;
@@ -118,13 +125,11 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int
   const int* T;
   int lo, hi;  // coordinate range of the frozen tuple
   if (side == 0) {
-    const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
     if (slot < st[0] || slot >= rl) return;
     T = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)slot * d : nullptr;
     lo = 0;
     hi = k;
   } else {
-    const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
     if (slot < st[1] || slot >= rr) return;
     T = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)slot * d : nullptr;
     lo = k + 2;
@@ -166,11 +171,9 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int
   }
 }
 
-__device__ void sb_cx_table(const DevCtx& c, int job, int al, int be) {
+__device__ void sb_cx_table(const DevCtx& c, int job, int al, int be, int rl, int rr) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
-  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
-  const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
   if (al >= rl || be >= rr || (al < st[0] && be < st[1])) return;
   DDE p = dde_one();
   if (k > 0 && k < d - 2) {
@@ -580,20 +583,17 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
   __syncthreads();
 }
 
-template <int FAMILY, bool CACHED, int THREADS>
-__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int sweep) {
+// One Alg. 6 sweep of superblock `job` (all CTAs of its cluster): phases 1-3 with the ranks
+// r (own), rl / rr (neighbours, at the end of the previous sweep) given by the caller; the
+// new pivot (if any) is written to the record Rn (slot r and rank); returns the new rank.
+template <int FAMILY, bool CACHED>
+__device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
+                                          int rl, int rr, int* Rn) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
-  const int job = blockIdx.x / G;
   const int k = c.kb + job, d = c.d, n = c.n, cap = c.cap;
   const int tid = threadIdx.x, T = blockDim.x;
-  __shared__ GreedySmem S;
-  extern __shared__ double dyn[];
-
-  const int r = rec_rank(c.rec_cur, c.RS, k);
-  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
-  const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
   const long long R = (long long)rl * n, C = (long long)rr * n;
   // rows / columns of this CTA (contiguous blocks); the cached variant's shared-memory
   // stride is the capacity block rpcap >= rpc, cpc
@@ -605,8 +605,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   double* U = c.U + (long long)job * cap * sbn;
   double* V = c.V + (long long)job * cap * sbn;
   double* Araw = c.Araw + (long long)job * sbn;
-  int* Rn = c.rec_next + (long long)k * c.RS;
-  const int* Rc = c.rec_cur + (long long)k * c.RS;
   const long long jo = (long long)job * cap * n;   // table offset of this job
   const long long jcx = (long long)job * cap * cap;
   const double* uk = c.u + (long long)k * n;
@@ -631,8 +629,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
       t_last = t;
     }
   };
-  if (cr == 0)
-    for (int t = tid; t < c.RS; t += T) Rn[t] = Rc[t];
   if (tid < r) {
     int px, py;
     pivot_pos(c, k, tid, px, py);
@@ -654,12 +650,12 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     const int il = G == 1 ? 0 : cr, ir = G == 1 ? 0 : cr - gl;
     if (do_l)
       for (int slot = rows_done; slot < rl; ++slot) {
-        sb_side_tables(c, job, 0, slot, il * T, gl * T);
+        sb_side_tables(c, job, 0, slot, il * T, gl * T, rl, rr);
         __syncthreads();
       }
     if (do_r)
       for (int slot = cols_done; slot < rr; ++slot) {
-        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T);
+        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T, rl, rr);
         __syncthreads();
       }
   }
@@ -670,7 +666,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
       int al, be;
       if (e < na) { al = rows_done + (int)(e / rr); be = (int)(e % rr); }
       else { const long long f = e - na; al = (int)(f / (rr - cols_done)); be = cols_done + (int)(f % (rr - cols_done)); }
-      sb_cx_table(c, job, al, be);
+      sb_cx_table(c, job, al, be, rl, rr);
     }
   }
   cl.sync();  // tables visible to the whole cluster
@@ -942,9 +938,85 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
-  if (G > 1) cl.sync();  // no CTA may exit while another can still read its shared memory
+  if (G > 1) cl.sync();  // no CTA may leave while another can still read its shared memory
   phase(PH_END);
   if (timer) atomicAdd(&c.phase_ns[PH_LAUNCHES], 1ULL);
+  return added ? r + 1 : r;
+}
+
+// neighbour ranks published at the end of each sweep (a ring of two: a neighbour can be at
+// most one sweep ahead) and the sweeps each superblock has completed
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// single sweep (any world size): ranks from the current records, the updated record goes to
+// rec_next (the multi-process exchange buffer)
+template <int FAMILY, bool CACHED, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int sweep) {
+  __shared__ GreedySmem S;
+  extern __shared__ double dyn[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
+  const int r = rec_rank(c.rec_cur, c.RS, k);
+  const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
+  const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
+  int* Rn = c.rec_next + (long long)k * c.RS;
+  const int* Rc = c.rec_cur + (long long)k * c.RS;
+  if (cl.block_rank() == 0)
+    for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
+  __syncthreads();
+  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn);
+  if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    c.rank_ring[k * 2 + (sweep & 1)] = rn;
+    c.done[k] = sweep + 1;
+  }
+}
+
+// Sweeps [s0, s0 + nsweeps) in one launch (world == 1, all clusters resident): superblock k
+// starts sweep s as soon as its neighbours k-1 and k+1 have finished sweep s-1 -- the
+// neighbour-only pivot exchange of PAPER.md Alg. 6 lines 6-8, through release/acquire flags
+// in global memory instead of a grid-wide barrier.  Records are appended in place (slots
+// below a published rank never change).  A wait longer than ~2 s sets flags[1] and abandons
+// the launch (reported as an error), so a scheduling failure cannot hang the device.
+template <int FAMILY, bool CACHED, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
+  __shared__ GreedySmem S;
+  __shared__ int s_abort;
+  extern __shared__ double dyn[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
+  int* Rk = c.rec_cur + (long long)k * c.RS;
+  int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
+  for (int s = s0; s < s0 + nsweeps; ++s) {
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+      int abort = 0;
+      const long long t0 = clock64();
+      if (k > 0)
+        while (ld_acquire(&c.done[k - 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
+        }
+      if (!abort && k < d - 2)
+        while (ld_acquire(&c.done[k + 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
+        }
+      if (abort) atomicOr(&c.flags[1], 1);
+      s_abort = abort;
+    }
+    cl.sync();  // the acquire of thread 0 orders every CTA's reads of the neighbours' records
+    if (cl.map_shared_rank(&s_abort, 0)[0]) break;
+    cl.sync();
+    const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
+    const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
+    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk);
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+      c.rank_ring[k * 2 + (s & 1)] = r;
+      st_release(&c.done[k], s + 1);  // the record writes above happen-before this release
+    }
+  }
 }
 
 }  // namespace ttc
