@@ -40,7 +40,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from workloads import FAMILY_NAMES, WORKLOADS  # noqa: E402
+from workloads import FAMILY_NAMES, WORKLOADS, X_FAMILIES, X_WORKLOADS  # noqa: E402
+
+ALL_WORKLOADS = {**WORKLOADS, **X_WORKLOADS}
 
 DEFAULT_WORKLOAD = "D5"   # BASELINE.json configs[1]
 L2_FLUSH_BYTES = 256 << 20
@@ -53,7 +55,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(ALL_WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -122,17 +124,24 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # algorithmic fp64 flops per superblock entry: C: S = H + L*2^-52 (2), S*S (1),
 # 1/S^2 (1); D: + five double-double products (10 each), rho (4), dd * rho (8), rounding and
-# the division (2)
-FLOPS_PER_ENTRY = {0: 4, 1: 68}
+# the division (2).  x-form (m modes): prefix/suffix products and sums 4m, B 2; each of the
+# m(m+1)/2 pairs 6 (running product, 1-p, 1+p, division, q*q, accumulate).
+def flops_per_entry(family, m):
+    if family == 0:
+        return 4
+    if family == 1:
+        return 68
+    pairs = 3 * m * (m + 1)
+    return {2: 4 * m + 2, 3: 4 * m + 3 + pairs, 4: pairs}[family]
 
 
-def roofline(kt, stats, family, peaks, peak_src):
+def roofline(kt, stats, family, peaks, peak_src, modes=0):
     """kt: {name: (launches, ms)} of the profiling pass; stats: its summed counters."""
     name = max(kt, key=lambda k: kt[k][1])
     launches, ms = kt[name]
     avg_s = ms / max(1, launches) / 1e3
     out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
-    fpe = FLOPS_PER_ENTRY[family]
+    fpe = flops_per_entry(family, modes)
     if name == "k_sweep":
         ent = stats["sb_entries"] / max(1, launches)
         upd = stats["sb_updates"] / max(1, launches)
@@ -179,7 +188,7 @@ def oracle_sample(wl, budget_s):
     nsw = wl.alg6_sweeps
     evals, t0 = 0, time.perf_counter()
     with threadpool_limits(1):
-        if wl.d <= 5:
+        if wl.d <= 8:
             solves = 0
             while True:
                 st, val, _ = X.run(prob, nsw)
@@ -208,7 +217,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    wl = WORKLOADS[args.workload]
+    wl = ALL_WORKLOADS[args.workload]
     budget = max(0.5, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(wl, budget)
@@ -231,7 +240,8 @@ def run_reference(args):
 
 
 def workload_config(wl, n):
-    return {"workload": f"{FAMILY_NAMES[wl.family]}_{wl.d}", "d": wl.d, "n": wl.n, "L": wl.L,
+    return {"workload": f"{FAMILY_NAMES[wl.family]}_{wl.d}", "d": wl.d, "modes": wl.modes, "n": wl.n,
+            "rule": "gauss-legendre [0,1]" if wl.family in X_FAMILIES else f"trapezoid [-{wl.L:g},{wl.L:g}]",
             "rank_cap": wl.rank_cap, "tol": wl.tol, "sweeps": wl.sweeps, "alg6_sweeps": wl.alg6_sweeps,
             "n_samples": wl.n_samples, "rook_iters": wl.rook_iters, "seed": wl.seed,
             "parallelism": f"superblocks/{n}",
@@ -262,7 +272,7 @@ def main():
     from paper_1903_11554_b200 import TTCross
     from paper_1903_11554_b200.dist import DistTTCross
 
-    wl = WORKLOADS[args.workload]
+    wl = ALL_WORKLOADS[args.workload]
     u, w = wl.grid()
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
@@ -379,7 +389,7 @@ def main():
             st[k] = st.get(k, 0) + v
     core.set_timing(False)
     peaks, peak_src = measured_peaks()
-    roof = roofline(kt, st, wl.family, peaks, peak_src)
+    roof = roofline(kt, st, wl.family, peaks, peak_src, wl.modes)
     kernel_ms = {k: v[1] / nprof for k, v in kt.items() if v[0]}
 
     # ---- oracle on the host cores (rank 0, N = 1 only)

@@ -37,8 +37,14 @@ extern "C" {
 #define TTC_ERR_SINGULAR  3  /* an intersection matrix A(I_{<=k}, I_{>k}) is singular     */
 #define TTC_ERR_STATE     4  /* call order violated (e.g. commit without a local sweep)   */
 
+/* t-form (BASELINE.json configs): nodes are u = e^t, integral prefactor 4/d!              */
 #define TTC_FAMILY_C 0  /* C_d : f = 1/(sum_j (u_j + 1/u_j))^2                 (eq. (9))  */
 #define TTC_FAMILY_D 1  /* D_d : f = prod_{i<j} ((u_i-u_j)/(u_i+u_j))^2 / (...)^2 (eq. (10)) */
+/* x-form (eq. (9)-(11), lines 843-851): the d-1 variables x_2..x_d in (0,1) are the
+ * modes (cfg.d = d-1), nodes are x (e.g. Gauss-Legendre), integral prefactor 2              */
+#define TTC_FAMILY_CX 2 /* C_d = 2 int B_d                                                    */
+#define TTC_FAMILY_DX 3 /* D_d = 2 int A_d B_d                                                */
+#define TTC_FAMILY_EX 4 /* E_d = 2 int A_d                                                    */
 
 #define TTC_MEM_HOST   0
 #define TTC_MEM_DEVICE 1
@@ -49,8 +55,8 @@ extern "C" {
 typedef struct ttc_ctx ttc_ctx;
 
 typedef struct ttc_config {
-  int32_t  family;     /* TTC_FAMILY_C or TTC_FAMILY_D                                    */
-  int32_t  d;          /* number of modes, 2 <= d <= 2000                                 */
+  int32_t  family;     /* TTC_FAMILY_C, _D (t-form) or TTC_FAMILY_CX, _DX, _EX (x-form)     */
+  int32_t  d;          /* number of modes of the tensor, 2 <= d <= 2000                   */
   int32_t  n;          /* nodes per mode, 2 <= n <= 4096 (same for every mode)             */
   int32_t  rank_cap;   /* 1 <= rank_cap <= TTC_MAX_RANK                                    */
   int32_t  n_samples;  /* |L| of Alg. 2 line 1 (random superblock entries), 1..1024        */
@@ -84,7 +90,8 @@ typedef struct ttc_stats {
  * problem -- not counted in the per-solve statistics, which tt_cross_reset zeroes).
  *   out      : receives the context (owned by the caller; free with tt_cross_destroy)
  *   cfg      : problem configuration (copied)
- *   nodes_u  : d*n doubles, row-major [mode][node], u-nodes (u = e^t, R1), > 0
+ *   nodes_u  : d*n doubles, row-major [mode][node], > 0: u-nodes (u = e^t, R1) for
+ *              the t-form families, x-nodes in (0,1) for the x-form families
  *   weights  : d*n doubles, quadrature weights [mode][node]
  *   mem_kind : TTC_MEM_HOST (pageable/pinned host arrays, copied H2D on `stream`) or
  *              TTC_MEM_DEVICE (device arrays, copied D2D)

@@ -38,7 +38,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .integrand import entries, prefactor
+from .integrand import X_FAMILIES, entries, prefactor
 
 M64 = (1 << 64) - 1
 GOLDEN = 0x9E3779B97F4A7C15
@@ -339,13 +339,14 @@ def integrate(prob, state, fibers=None):
     sign = 1 if core > 0 else (-1 if core < 0 else 0)
     if core == 0.0 or not math.isfinite(core):
         return core, -math.inf if core == 0.0 else math.nan, sign, n_evals
-    lnpre = math.log(4.0) - math.lgamma(d + 1)
+    xform = prob.family in X_FAMILIES
+    lnpre = math.log(2.0) if xform else math.log(4.0) - math.lgamma(d + 1)
     ln_abs = math.log(abs(core)) + log2s * math.log(2.0) + lnpre
     log10 = ln_abs / math.log(10.0)
     if -700.0 < ln_abs < 700.0:
         # direct product when every factor is representable (keeps full fp64 accuracy)
-        if -1000 < log2s < 1000 and d <= 170:
-            value = math.ldexp(core, int(log2s)) * prefactor(d)
+        if -1000 < log2s < 1000 and (xform or d <= 170):
+            value = math.ldexp(core, int(log2s)) * prefactor(d, prob.family)
         else:
             value = sign * math.exp(ln_abs)
     else:
@@ -394,7 +395,7 @@ def integrate_exact(prob, state, fibers=None, dps=50):
         if core == 0:
             return 0.0, -math.inf, 0
         sign = 1 if core > 0 else -1
-        val = core * 4 / mpmath.factorial(d)
+        val = core * 2 if prob.family in X_FAMILIES else core * 4 / mpmath.factorial(d)
         return float(val), float(mpmath.log10(abs(val))), sign
 
 

@@ -36,6 +36,10 @@ import numpy as np
 
 FAMILY_C = 0
 FAMILY_D = 1
+FAMILY_CX = 2
+FAMILY_DX = 3
+FAMILY_EX = 4
+X_FAMILIES = (FAMILY_CX, FAMILY_DX, FAMILY_EX)
 
 _TWO52 = float(2 ** 52)
 _SPLIT = 134217729.0  # 2^27 + 1, Veltkamp/Dekker splitter
@@ -134,6 +138,8 @@ def entries(family, u_nodes, idx):
     Plain evaluation of the definition: S over all d coordinates, P over all d(d-1)/2
     pairs in lexicographic order (the order does not matter for the rounded result).
     """
+    if family in X_FAMILIES:
+        return entries_x(family, u_nodes, idx)
     u_nodes = np.asarray(u_nodes, dtype=np.float64)
     idx = np.asarray(idx)
     d = idx.shape[-1]
@@ -151,8 +157,57 @@ def entries(family, u_nodes, idx):
     return prod.rounded() / SS
 
 
-def prefactor(d):
-    """4/d! of the (4/d!)-normalised Ising integrals (BASELINE.json configs)."""
+def entries_x(family, x_nodes, idx):
+    """The paper's x-form integrands (eq. (9)-(11), lines 843-851) at the grid
+    multi-indices ``idx`` (..., m), m = d-1 modes holding x_2..x_d:
+
+        B_d = (1 + sum_{k=2}^d x_2..x_k)^{-1} (1 + sum_{k=2}^d x_k..x_d)^{-1}
+        A_d = prod_{1<=i<j<=d} ((1 - x_{i+1}..x_j) / (1 + x_{i+1}..x_j))^2
+        C: B_d,  D: A_d * B_d,  E: A_d.
+
+    Plain fp64 in this fixed operation order (the CUDA path repeats it; no fused
+    multiply-add): S1 accumulates the prefix products left to right, S2 the suffix
+    products right to left, B = 1 / (S1 * S2); A multiplies q*q, q = (1-p)/(1+p), over
+    i = 1..d-1 then j = i+1..d with the running product p = x_{i+1}..x_j.
+    """
+    x_nodes = np.asarray(x_nodes, dtype=np.float64)
+    idx = np.asarray(idx)
+    m = idx.shape[-1]
+    X = [x_nodes[j][idx[..., j]] for j in range(m)]
+    shape = idx.shape[:-1]
+    A = np.ones(shape)
+    if family in (FAMILY_DX, FAMILY_EX):
+        for i in range(m):           # paper i' = i + 1 (x_{i'+1} = X[i])
+            p = np.ones(shape)
+            for j in range(i, m):    # paper j' = j + 2, p = x_{i'+1}..x_{j'}
+                p = p * X[j]
+                q = (1.0 - p) / (1.0 + p)
+                A = A * (q * q)
+    if family == FAMILY_EX:
+        return A
+    S1 = np.ones(shape)
+    p = np.ones(shape)
+    for k in range(m):
+        p = p * X[k]
+        S1 = S1 + p
+    S2 = np.ones(shape)
+    p = np.ones(shape)
+    for k in range(m - 1, -1, -1):
+        p = p * X[k]
+        S2 = S2 + p
+    B = 1.0 / (S1 * S2)
+    if family == FAMILY_CX:
+        return B
+    if family != FAMILY_DX:
+        raise ValueError(f"unknown family {family}")
+    return A * B
+
+
+def prefactor(d, family=FAMILY_C):
+    """Integral prefactor: 4/d! of the (4/d!)-normalised t-form (BASELINE.json configs), 2
+    for the x-form (eq. (9)-(11)).  For the x-form `d` is the number of modes."""
+    if family in X_FAMILIES:
+        return 2.0
     return 4.0 / math.factorial(d)
 
 
@@ -177,4 +232,4 @@ def brute_force(family, u_nodes, weights, chunk=1 << 21):
         for j in range(d):
             w = w * weights[j][idx[:, j]]
         acc += float(np.sum(w * entries(family, u_nodes, idx)))
-    return acc * prefactor(d)
+    return acc * prefactor(d, family)

@@ -17,6 +17,9 @@ LIB_PATH = os.path.join(HERE, "libttcross.so")
 TTC_OK = 0
 TTC_FAMILY_C = 0
 TTC_FAMILY_D = 1
+TTC_FAMILY_CX = 2
+TTC_FAMILY_DX = 3
+TTC_FAMILY_EX = 4
 TTC_MEM_HOST = 0
 TTC_MEM_DEVICE = 1
 

@@ -151,6 +151,16 @@ int check_launch(const char* what) {
 int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
   DevCtx& dc = c->dc;
   const int n = dc.n, tup = dc.cap;
+  if (dc.family >= 2) {
+    const int gx = std::min(4096, (tup * n + 255) / 256);
+    {
+      Timed t(c, K_FIBER);
+      if (dc.family == 2) k_fiber_x<2><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+      else if (dc.family == 3) k_fiber_x<3><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+      else k_fiber_x<4><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+    }
+    return check_launch("k_fiber_x");
+  }
   {
     Timed t(c, K_FROZEN_SIDES);
     k_frozen_sides<<<dim3((tup + 63) / 64, 2, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
@@ -345,13 +355,15 @@ int do_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sig
     l10 = core == 0.0 ? -INFINITY : NAN;
     val = core;
   } else {
-    const double lnpre = std::log(4.0) - std::lgamma((double)d + 1.0);
+    const bool xform = c->dc.family >= 2;  // PAPER.md eq. (9)-(11): prefactor 2
+    const double lnpre = xform ? std::log(2.0) : std::log(4.0) - std::lgamma((double)d + 1.0);
     const double ln_abs = std::log(std::fabs(core)) + lg2 * std::log(2.0) + lnpre;
     l10 = ln_abs / std::log(10.0);
     if (ln_abs > -700.0 && ln_abs < 700.0) {
-      if (lg2 > -1000 && lg2 < 1000 && d <= 170) {
-        double pre = 4.0;
-        for (int k = 2; k <= d; ++k) pre /= (double)k;
+      if (lg2 > -1000 && lg2 < 1000 && (xform || d <= 170)) {
+        double pre = xform ? 2.0 : 4.0;
+        if (!xform)
+          for (int k = 2; k <= d; ++k) pre /= (double)k;
         val = std::ldexp(core, (int)lg2) * pre;
       } else {
         val = sg * std::exp(ln_abs);
@@ -468,7 +480,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   if (!out || !cfg || !nodes_u || !weights) return fail(TTC_ERR_ARG, "null argument");
   *out = nullptr;
   const ttc_config& k = *cfg;
-  if (k.family != TTC_FAMILY_C && k.family != TTC_FAMILY_D) return fail(TTC_ERR_ARG, "family must be 0 (C) or 1 (D)");
+  if (k.family < TTC_FAMILY_C || k.family > TTC_FAMILY_EX)
+    return fail(TTC_ERR_ARG, "family must be 0 (C), 1 (D), 2 (Cx), 3 (Dx) or 4 (Ex)");
   if (k.d < 2 || k.d > 2000) return fail(TTC_ERR_ARG, "d must be in [2, 2000]");
   if (k.n < 2 || k.n > 4096) return fail(TTC_ERR_ARG, "n must be in [2, 4096]");
   if (k.rank_cap < 1 || k.rank_cap > TTC_MAX_RANK) return fail(TTC_ERR_ARG, "rank_cap must be in [1, 64]");
@@ -573,6 +586,13 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     allow((const void*)k_sweeps<1, false, 512>, 180 * 1024);
     allow((const void*)k_sweeps<0, true, 512>, 180 * 1024);
     allow((const void*)k_sweeps<1, true, 512>, 180 * 1024);
+    for (const void* f : {(const void*)k_sweep<2, false, 256>, (const void*)k_sweep<2, false, 512>,
+                          (const void*)k_sweep<3, false, 256>, (const void*)k_sweep<3, false, 512>,
+                          (const void*)k_sweep<4, false, 256>, (const void*)k_sweep<4, false, 512>,
+                          (const void*)k_sweeps<2, false, 256>, (const void*)k_sweeps<2, false, 512>,
+                          (const void*)k_sweeps<3, false, 256>, (const void*)k_sweeps<3, false, 512>,
+                          (const void*)k_sweeps<4, false, 256>, (const void*)k_sweeps<4, false, 512>})
+      allow(f, 180 * 1024);
     allow((const void*)k_sweep<0, false, 256>, 180 * 1024);
     allow((const void*)k_sweep<1, false, 256>, 180 * 1024);
     allow((const void*)k_sweep<0, true, 256>, 180 * 1024);
@@ -625,11 +645,17 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     // T = threads per CTA; kernels are compiled for 256 (two CTAs per SM) and 512 (one)
     auto fn_for = [&](bool cached) -> const void* {
       const bool big = T > 256;
-      if (k.family == TTC_FAMILY_C)
-        return big ? (cached ? (const void*)k_sweep<0, true, 512> : (const void*)k_sweep<0, false, 512>)
-                   : (cached ? (const void*)k_sweep<0, true, 256> : (const void*)k_sweep<0, false, 256>);
-      return big ? (cached ? (const void*)k_sweep<1, true, 512> : (const void*)k_sweep<1, false, 512>)
-                 : (cached ? (const void*)k_sweep<1, true, 256> : (const void*)k_sweep<1, false, 256>);
+      switch (k.family) {
+        case TTC_FAMILY_C:
+          return big ? (cached ? (const void*)k_sweep<0, true, 512> : (const void*)k_sweep<0, false, 512>)
+                     : (cached ? (const void*)k_sweep<0, true, 256> : (const void*)k_sweep<0, false, 256>);
+        case TTC_FAMILY_D:
+          return big ? (cached ? (const void*)k_sweep<1, true, 512> : (const void*)k_sweep<1, false, 512>)
+                     : (cached ? (const void*)k_sweep<1, true, 256> : (const void*)k_sweep<1, false, 256>);
+        case TTC_FAMILY_CX: return big ? (const void*)k_sweep<2, false, 512> : (const void*)k_sweep<2, false, 256>;
+        case TTC_FAMILY_DX: return big ? (const void*)k_sweep<3, false, 512> : (const void*)k_sweep<3, false, 256>;
+        default: return big ? (const void*)k_sweep<4, false, 512> : (const void*)k_sweep<4, false, 256>;
+      }
     };
     // resident clusters for (G, cached)
     auto resident = [&](int g, bool cached) -> int {
@@ -654,7 +680,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     // prefer: all nj clusters resident; cached rows when they fit; then the largest G
     bool cached = false;
     for (;; G >>= 1) {
-      const bool can_cache = cache_for(G) <= smem_lim;
+      const bool can_cache = cache_for(G) <= smem_lim && k.family < TTC_FAMILY_CX;
       if (can_cache && resident(G, true) >= std::min(nj, 1 << 30)) { cached = true; break; }
       if (resident(G, false) >= nj) { cached = false; break; }
       if (G == 1) { cached = false; break; }
@@ -677,12 +703,19 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     c->greedy_fn = fn_for(c->greedy_cached);
     {
       const bool big = T > 256;
-      if (k.family == TTC_FAMILY_C)
-        c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<0, true, 512> : (const void*)k_sweeps<0, false, 512>)
-                           : (cached ? (const void*)k_sweeps<0, true, 256> : (const void*)k_sweeps<0, false, 256>);
-      else
-        c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<1, true, 512> : (const void*)k_sweeps<1, false, 512>)
-                           : (cached ? (const void*)k_sweeps<1, true, 256> : (const void*)k_sweeps<1, false, 256>);
+      switch (k.family) {
+        case TTC_FAMILY_C:
+          c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<0, true, 512> : (const void*)k_sweeps<0, false, 512>)
+                             : (cached ? (const void*)k_sweeps<0, true, 256> : (const void*)k_sweeps<0, false, 256>);
+          break;
+        case TTC_FAMILY_D:
+          c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<1, true, 512> : (const void*)k_sweeps<1, false, 512>)
+                             : (cached ? (const void*)k_sweeps<1, true, 256> : (const void*)k_sweeps<1, false, 256>);
+          break;
+        case TTC_FAMILY_CX: c->sweeps_fn = big ? (const void*)k_sweeps<2, false, 512> : (const void*)k_sweeps<2, false, 256>; break;
+        case TTC_FAMILY_DX: c->sweeps_fn = big ? (const void*)k_sweeps<3, false, 512> : (const void*)k_sweeps<3, false, 256>; break;
+        default: c->sweeps_fn = big ? (const void*)k_sweeps<4, false, 512> : (const void*)k_sweeps<4, false, 256>; break;
+      }
       // the wavefront needs every cluster resident at once
       c->persistent = k.world == 1 && resident(G, cached) >= nj && !std::getenv("TTC_NO_PERSISTENT");
     }

@@ -39,6 +39,8 @@ __device__ __forceinline__ int init_coord(const DevCtx& c, int q, int j) {
 
 __device__ double init_entry(const DevCtx& c, int q) {
   const int d = c.d, n = c.n;
+  if (c.family >= 2)
+    return x_entry_dyn(c.family, d, [&](int j) { return c.u[j * n + init_coord(c, q, j)]; });
   ESum s = esum_zero();
   for (int j = 0; j < d; ++j) {
     const int t = init_coord(c, q, j);
@@ -191,6 +193,15 @@ __device__ void sb_cx_table(const DevCtx& c, int job, int al, int be, int rl, in
 template <int FAMILY>
 __device__ __forceinline__ double sb_entry(const DevCtx& c, int job, int k, int al, int a, int be, int b) {
   const int n = c.n;
+  if (FAMILY >= 2) {  // x-form: direct evaluation of the full coordinate tuple
+    const int d = c.d;
+    const int* TL = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d : nullptr;
+    const int* TR = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d : nullptr;
+    return x_entry<FAMILY>(d, [&](int j) {
+      const int node = j < k ? TL[j] : (j == k ? a : (j == k + 1 ? b : TR[j]));
+      return c.u[(long long)j * n + node];
+    });
+  }
   const long long oa = ((long long)job * c.cap + al) * n;
   const long long ob = ((long long)job * c.cap + be) * n;
   ESum s = c.SA[oa + a];
@@ -421,7 +432,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, xb = X.xb, xe = X.xe, rpcap = X.rpcap;
   const int be = y / n, b = y - (y / n) * n;
   if (tid < r) S.vec[tid] = X.V[tid * sbn + y];
-  if (tid == 0) {
+  if (tid == 0 && FAMILY < 2) {
     S.fs = c.SB[jo + (long long)be * n + b];
     if (FAMILY == 1) S.fp = c.PB[jo + (long long)be * n + b];
   }
@@ -442,14 +453,20 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   for (long long x = xb + tid; x < xe; x += T, ++jrow) {
     const int al = (int)(x / n), a = (int)(x - (long long)al * n);
     const double ua = X.uk[a];
-    ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
-    esum_add(s, S.fs);
-    const double Sd = esum_round(s);
-    const double SS = __dmul_rn(Sd, Sd);
     double raw;
-    if (FAMILY == 0) {
+    if (FAMILY >= 2) {
+      raw = sb_entry<FAMILY>(c, X.job, X.k, al, a, be, b);
+    } else if (FAMILY == 0) {
+      ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
+      esum_add(s, S.fs);
+      const double Sd = esum_round(s);
+      const double SS = __dmul_rn(Sd, Sd);
       raw = __drcp_rn(SS);
     } else {
+      ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
+      esum_add(s, S.fs);
+      const double Sd = esum_round(s);
+      const double SS = __dmul_rn(Sd, Sd);
       DDE p = CACHED ? X.PAc[x - xb] : c.PA[jo + x];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[al]);
@@ -490,7 +507,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, yb = X.yb, ye = X.ye, rpcap = X.rpcap;
   const int al = x / n, a = x - (x / n) * n;
   if (tid < r) S.vec[tid] = X.U[tid * sbn + x];
-  if (tid == 0) {
+  if (tid == 0 && FAMILY < 2) {
     S.fs = c.SA[jo + x];
     if (FAMILY == 1) S.fp = c.PA[jo + x];
   }
@@ -511,14 +528,20 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   for (long long y = yb + tid; y < ye; y += T, ++jcol) {
     const int be = (int)(y / n), b = (int)(y - (long long)be * n);
     const double ub = X.uk1[b];
-    ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
-    esum_add(s, S.fs);
-    const double Sd = esum_round(s);
-    const double SS = __dmul_rn(Sd, Sd);
     double e;
-    if (FAMILY == 0) {
+    if (FAMILY >= 2) {
+      e = sb_entry<FAMILY>(c, X.job, X.k, al, a, be, b);
+    } else if (FAMILY == 0) {
+      ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
+      esum_add(s, S.fs);
+      const double Sd = esum_round(s);
+      const double SS = __dmul_rn(Sd, Sd);
       e = __drcp_rn(SS);
     } else {
+      ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
+      esum_add(s, S.fs);
+      const double Sd = esum_round(s);
+      const double SS = __dmul_rn(Sd, Sd);
       DDE p = CACHED ? X.PBc[y - yb] : c.PB[jo + y];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[be]);
@@ -642,7 +665,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
 
   // ---- phase 1: factor tables of the new left slots [rows_done, rl) and right slots
   // [cols_done, rr); every CTA of the cluster takes a strided share of the nodes a
-  {
+  if (FAMILY < 2) {
     // with G >= 2 the first half of the cluster builds the left tables, the second half the
     // right ones; each CTA takes a strided share of the nodes a
     const int gl = G >= 2 ? G / 2 : 1;

@@ -158,6 +158,33 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
   }
 }
 
+// quadrature fibers of the x-form families: direct evaluation of every entry (the x-form
+// integrand is not a function of per-mode node values, so the frozen-part factorisation
+// of the t-form does not apply); grid x = flat (beta*n + a) chunks, y = alpha, z = job
+template <int FAM>
+__global__ void __launch_bounds__(256) k_fiber_x(DevCtx c, int kind, int jbase) {
+  const int j = jbase + blockIdx.z, al = blockIdx.y;
+  Job jb = make_job(c, kind, j);
+  if (al >= jb.rx) return;
+  const int n = c.n, m = jb.m, d = c.d;
+  const int total = jb.ry * n;
+  if (al == 0 && blockIdx.x == 0 && threadIdx.x == 0 && c.counters) {
+    atomicAdd(&c.counters[CNT_EVALS], (unsigned long long)jb.rx * jb.ry * n);
+    atomicAdd(&c.counters[CNT_FIBER_ENTRIES], (unsigned long long)jb.rx * jb.ry * n);
+  }
+  const int* TX = jb.X ? jb.X + (long long)al * d : nullptr;
+  double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+    const int be = f / n;
+    const int a = f - be * n;
+    const int* TY = jb.Y ? jb.Y + (long long)be * d : nullptr;
+    F[f] = x_entry<FAM>(d, [&](int q) {
+      const int node = q < m ? TX[q] : (q == m ? a : TY[q]);
+      return c.u[(long long)q * n + node];
+    });
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // quadrature (§4.1)
 // ---------------------------------------------------------------------------------------
@@ -172,6 +199,11 @@ __global__ void k_intersection(DevCtx c, int ibase) {
   if (s >= r || t >= r) return;
   const int* Ps = rec_piv(c.rec_cur, c.RS, i) + (long long)s * d;
   const int* Pt = rec_piv(c.rec_cur, c.RS, i) + (long long)t * d;
+  if (c.family >= 2) {
+    c.M[((long long)i * c.cap + s) * c.cap + t] =
+        x_entry_dyn(c.family, d, [&](int q) { return c.u[(long long)q * n + (q <= i ? Ps[q] : Pt[q])]; });
+    return;
+  }
   ESum S = esum_zero();
   for (int q = 0; q < d; ++q) {
     int node = q <= i ? Ps[q] : Pt[q];

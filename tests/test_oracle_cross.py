@@ -287,3 +287,18 @@ def test_dd_weighted_sum_is_accurate():
             ex = mpmath.fsum(terms)
             bound = mpmath.fsum([abs(t) for t in terms]) * mpmath.mpf(2) ** -98  # ~ n * 2^-106
             assert abs((mpmath.mpf(float(hi[a, b])) + mpmath.mpf(float(lo[a, b]))) - ex) <= bound
+
+
+def test_xform_d8_reproduces_paper_value():
+    """End to end (cross + quadrature) on the paper's own setup: D_8 with 33-point
+    Gauss-Legendre (§5.2) against the value printed in PAPER.md Fig. 5
+    (tests/golden/paper_values.json, 32 digits): rank 24 gives ~1e-11."""
+    import json
+    import os
+    from workloads import X_WORKLOADS
+    wl = X_WORKLOADS["Dx8"]
+    u, w = wl.grid()
+    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed)
+    st, val, _ = X.run(prob, wl.sweeps)
+    ref = float(json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))["D"]["8"])
+    assert abs(val - ref) < 1e-9 * ref, (val, ref)

@@ -173,3 +173,64 @@ def test_paper_delta_consistency():
     d256 = mpmath.mpf(vals["D"]["256"])
     delta = (d128 / d256) ** (mpmath.mpf(1) / 128)
     assert abs(delta - mpmath.mpf(vals["Delta"])) < 1e-8
+
+
+# ---------------------------------------------------------------- x-form (eq. (9)-(11))
+def _xform_brute(fam, d, n):
+    from workloads import xform_grid
+    x, w = xform_grid(d, n)
+    return ig.brute_force(fam, x, w)
+
+
+@pytest.mark.parametrize("fam,d,n,tol", [("C", 2, 20, 1e-14), ("C", 3, 24, 1e-13), ("C", 4, 24, 1e-12),
+                                         ("D", 2, 20, 1e-14), ("D", 3, 24, 1e-12), ("D", 4, 24, 1e-10)])
+def test_xform_gauss_legendre_matches_closed_forms(fam, d, n, tol):
+    """Full Gauss-Legendre tensor sums of the x-form oracle integrand (eq. (9)-(10))
+    against the closed forms of BASELINE.json north_star (no reading involved)."""
+    from workloads import FAMILY_CX, FAMILY_DX
+    got = _xform_brute(FAMILY_CX if fam == "C" else FAMILY_DX, d, n)
+    ref = float(CLOSED[(fam, d)]())
+    assert abs(got - ref) <= tol * abs(ref), (got, ref)
+
+
+def test_xform_e2_closed_form():
+    """E_2 = 2 int_0^1 ((1-x)/(1+x))^2 dx = 6 - 8 log 2 (elementary antiderivative)."""
+    from workloads import FAMILY_EX
+    assert abs(_xform_brute(FAMILY_EX, 2, 20) - (6 - 8 * math.log(2))) < 1e-14
+
+
+def test_xform_e3_numerical_quadrature():
+    """E_3 = 2 int_{[0,1]^2} A_3 against mpmath's own adaptive quadrature."""
+    from workloads import FAMILY_EX
+    f = lambda x2, x3: ((1 - x2) / (1 + x2)) ** 2 * ((1 - x2 * x3) / (1 + x2 * x3)) ** 2 * ((1 - x3) / (1 + x3)) ** 2
+    ref = 2 * mpmath.quad(f, [0, 1], [0, 1])
+    assert abs(_xform_brute(FAMILY_EX, 3, 24) - float(ref)) < 1e-12 * float(ref)
+
+
+def test_xform_entry_order_is_plain_fp64():
+    """The x-form entry is exactly the documented operation sequence (retyped with Python
+    floats, scalar by scalar)."""
+    from workloads import FAMILY_CX, FAMILY_DX, xform_grid
+    x, _ = xform_grid(5, 9)
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        idx = rng.integers(0, 9, 4)
+        X = [float(x[j][idx[j]]) for j in range(4)]
+        S1, p = 1.0, 1.0
+        for v in X:
+            p = p * v
+            S1 = S1 + p
+        S2, p = 1.0, 1.0
+        for v in reversed(X):
+            p = p * v
+            S2 = S2 + p
+        B = 1.0 / (S1 * S2)
+        A = 1.0
+        for i in range(4):
+            p = 1.0
+            for j in range(i, 4):
+                p = p * X[j]
+                q = (1.0 - p) / (1.0 + p)
+                A = A * (q * q)
+        assert ig.entries(FAMILY_CX, x, idx[None])[0] == B
+        assert ig.entries(FAMILY_DX, x, idx[None])[0] == A * B

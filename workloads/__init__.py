@@ -21,9 +21,15 @@ from dataclasses import dataclass
 
 import numpy as np
 
-FAMILY_C = 0  # C_d : f = 1/(sum_j (u_j + 1/u_j))^2
+FAMILY_C = 0  # C_d : f = 1/(sum_j (u_j + 1/u_j))^2                         (t-form, u-nodes)
 FAMILY_D = 1  # D_d : f = prod_{i<j} ((u_i-u_j)/(u_i+u_j))^2 / (sum_j (u_j + 1/u_j))^2
-FAMILY_NAMES = {FAMILY_C: "C", FAMILY_D: "D"}
+# the paper's own x-form (eq. (9)-(11)) on [0,1]^{d-1}: the tensor has d-1 modes
+# (x_2..x_d) and the integral prefactor is 2
+FAMILY_CX = 2  # C_d = 2 int B_d
+FAMILY_DX = 3  # D_d = 2 int A_d B_d
+FAMILY_EX = 4  # E_d = 2 int A_d
+FAMILY_NAMES = {FAMILY_C: "C", FAMILY_D: "D", FAMILY_CX: "Cx", FAMILY_DX: "Dx", FAMILY_EX: "Ex"}
+X_FAMILIES = (FAMILY_CX, FAMILY_DX, FAMILY_EX)
 
 
 def trapezoid_t_grid(n: int, L: float):
@@ -35,6 +41,20 @@ def trapezoid_t_grid(n: int, L: float):
     w = np.full(n, h, dtype=np.float64)
     w[0] = w[-1] = h / 2
     return t, w
+
+
+def gauss_legendre01(n: int):
+    """n-point Gauss-Legendre rule on [0, 1] (nodes ascending, weights summing to 1);
+    PAPER.md §5.2 "tensor product of one-dimensional Gauss--Legendre quadratures"."""
+    x, w = np.polynomial.legendre.leggauss(n)
+    return (x + 1.0) / 2.0, w / 2.0
+
+
+def xform_grid(d: int, n: int):
+    """x-nodes (d-1, n) and weights (d-1, n) of the x-form integrals (eq. (9)-(11)):
+    one Gauss-Legendre rule per variable x_2..x_d."""
+    x, w = gauss_legendre01(n)
+    return np.ascontiguousarray(np.tile(x, (d - 1, 1))), np.ascontiguousarray(np.tile(w, (d - 1, 1)))
 
 
 def ising_grid(d: int, n: int, L: float):
@@ -66,11 +86,18 @@ class Workload:
         enough to reach the rank cap from rank 1 in the configured number (R7)."""
         return self.sweeps * max(1, -(-(self.rank_cap - 1) // self.sweeps))
 
+    @property
+    def modes(self) -> int:
+        """Modes of the tensor: d for the t-form, d-1 (x_2..x_d) for the x-form."""
+        return self.d - 1 if self.family in X_FAMILIES else self.d
+
     def grid(self):
+        if self.family in X_FAMILIES:
+            return xform_grid(self.d, self.n)
         return ising_grid(self.d, self.n, self.L)
 
     def prefactor(self) -> float:
-        return 4.0 / math.factorial(self.d)
+        return 2.0 if self.family in X_FAMILIES else 4.0 / math.factorial(self.d)
 
 
 # BASELINE.json configs[0..4].  `sweeps` is the BASELINE sweep count (4 where a config
@@ -86,4 +113,13 @@ WORKLOADS = {
                     note="configs[3]: D_20, 513-pt trapezoid on [-24,24], rank cap 64, tol 1e-12"),
     "C200": Workload("C200", FAMILY_C, 200, 257, 20.0, 32, 1e-12, 6,
                      note="configs[4]: C_200, 257-pt trapezoid on [-20,20], rank cap 32, 6 sweeps"),
+}
+
+# The paper's own setup (§5.2-5.4): x-form integrands, n-point Gauss-Legendre per
+# variable.  Not BASELINE configs -- validation workloads for the "next" row of DESIGN.md §8
+# (D_8 is printed in PAPER.md Fig. 5 to 32 digits; C_d -> 2 exp(-2 gamma)).
+X_WORKLOADS = {
+    "Dx8": Workload("Dx8", FAMILY_DX, 8, 33, 0.0, 24, 1e-14, 24, note="D_8, 33-pt Gauss-Legendre, rank cap 24"),
+    "Cx64": Workload("Cx64", FAMILY_CX, 64, 33, 0.0, 16, 1e-14, 16, note="C_64, 33-pt Gauss-Legendre, rank cap 16"),
+    "Ex6": Workload("Ex6", FAMILY_EX, 6, 33, 0.0, 20, 1e-14, 20, note="E_6, 33-pt Gauss-Legendre, rank cap 20"),
 }
