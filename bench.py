@@ -184,7 +184,7 @@ def oracle_sample(wl, budget_s):
     from threadpoolctl import threadpool_limits
     from oracle import cross as X
     u, w = wl.grid()
-    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed)
+    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed, wl.fold)
     nsw = wl.alg6_sweeps
     evals, t0 = 0, time.perf_counter()
     with threadpool_limits(1):
@@ -245,7 +245,7 @@ def workload_config(wl, n):
             "rank_cap": wl.rank_cap, "tol": wl.tol, "sweeps": wl.sweeps, "alg6_sweeps": wl.alg6_sweeps,
             "n_samples": wl.n_samples, "rook_iters": wl.rook_iters, "seed": wl.seed,
             "parallelism": f"superblocks/{n}",
-            "l2": "flushed (256 MiB memset) before every timed step"}
+            "fold_weights": wl.fold, "l2": "flushed (256 MiB memset) before every timed step"}
 
 
 # --------------------------------------------------------------------------------------
@@ -280,6 +280,8 @@ def main():
     u_d = torch.from_numpy(u).to(dev)
     w_d = torch.from_numpy(w).to(dev)
     kw = dict(n_samples=wl.n_samples, rook_iters=wl.rook_iters, seed=wl.seed)
+    if wl.fold:
+        kw["fold_weights"] = True
     nsw = wl.alg6_sweeps
     use_graph = world == 1 and not args.no_graph
     if world == 1:

@@ -65,6 +65,8 @@ typedef struct ttc_config {
   uint64_t seed;       /* counter-based RNG seed of the first pivot and the samples        */
   int32_t  rank;       /* this process' index among `world` (superblocks are partitioned)  */
   int32_t  world;      /* number of processes (GPUs) sharing the problem, >= 1             */
+  int32_t  fold_weights; /* 1: cross on B = w x ... x w * f and contract with unit weights
+                          (§4.1); x-form families only; 0: off   */
 } ttc_config;
 
 typedef struct ttc_stats {

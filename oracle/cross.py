@@ -72,6 +72,7 @@ class Problem:
     n_samples: int = 32    # |L| of Alg. 2 line 1
     rook_iters: int = 4    # column+row rounds of the rook search (Alg. 2 lines 2-5)
     seed: int = 0
+    fold: bool = False     # cross on B = w x ... x w * f (§4.1), x-form
 
     @property
     def d(self):
@@ -81,8 +82,22 @@ class Problem:
     def n(self):
         return self.u.shape[1]
 
+    @property
+    def qw(self):
+        """Quadrature weights of the contraction: the rule's weights, or ones when they are
+        folded into the tensor (B = w x ... x w * f sums with unit weights)."""
+        return np.ones_like(self.w) if self.fold else self.w
+
     def A(self, idx):
-        return entries(self.family, self.u, idx)
+        f = entries(self.family, self.u, idx)
+        if not self.fold:
+            return f
+        # B(i) = f(i) * (((1 * w_0[i_0]) * w_1[i_1]) * ...), this order on both sides
+        idx = np.asarray(idx)
+        W = np.ones(idx.shape[:-1])
+        for j in range(idx.shape[-1]):
+            W = W * self.w[j][idx[..., j]]
+        return f * W
 
 
 @dataclass
@@ -323,7 +338,7 @@ def integrate(prob, state, fibers=None):
     log2s = 0.0
     v = None
     for m in range(d):
-        W = fibers[m] @ prob.w[m]                      # (r_{m-1}, r_m)
+        W = fibers[m] @ prob.qw[m]                     # (r_{m-1}, r_m)
         v = W[0] if v is None else v @ W
         if m < d - 1:
             M = intersection(prob, state, m)
@@ -382,7 +397,7 @@ def integrate_exact(prob, state, fibers=None, dps=50):
     with mpmath.workdps(dps):
         v = None
         for m in range(d):
-            hi, lo = _dd_weighted_sum(fibers[m], prob.w[m])
+            hi, lo = _dd_weighted_sum(fibers[m], prob.qw[m])
             W = mpmath.matrix(hi.shape[0], hi.shape[1])
             for a in range(hi.shape[0]):
                 for b in range(hi.shape[1]):

@@ -40,6 +40,7 @@ class TtcConfig(ctypes.Structure):
         ("family", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int32),
         ("rank_cap", ctypes.c_int32), ("n_samples", ctypes.c_int32), ("rook_iters", ctypes.c_int32),
         ("tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+        ("fold_weights", ctypes.c_int32),
     ]
 
 
@@ -137,12 +138,12 @@ class TTCross:
     """Handle on one TT-cross problem (C-ABI context)."""
 
     def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, rank=0, world=1,
-                 stream=None):
+                 stream=None, fold_weights=False):
         self.lib = load()
         self.d, self.n = int(u.shape[0]), int(u.shape[1])
         self.cap = int(rank_cap)
         self.cfg = TtcConfig(int(family), self.d, self.n, self.cap, int(n_samples), int(rook_iters), float(tol),
-                             int(seed) & ((1 << 64) - 1), int(rank), int(world))
+                             int(seed) & ((1 << 64) - 1), int(rank), int(world), 1 if fold_weights else 0)
         pu, ku, keep_u = _ptr_and_kind(u)
         pw, kw, keep_w = _ptr_and_kind(w)
         if ku != kw:

@@ -489,6 +489,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   if (k.rook_iters < 0 || k.rook_iters > 64) return fail(TTC_ERR_ARG, "rook_iters must be in [0, 64]");
   if (!(k.tol >= 0.0 && k.tol < 1.0)) return fail(TTC_ERR_ARG, "tol must be in [0, 1)");
   if (k.world < 1 || k.rank < 0 || k.rank >= k.world) return fail(TTC_ERR_ARG, "need 0 <= rank < world");
+  if (k.fold_weights != 0 && k.fold_weights != 1) return fail(TTC_ERR_ARG, "fold_weights must be 0 or 1");
+  if (k.fold_weights && k.family < TTC_FAMILY_CX)
+    return fail(TTC_ERR_ARG, "weight folding is supported for the x-form families (uniform trapezoid weights)");
   if (mem_kind != TTC_MEM_HOST && mem_kind != TTC_MEM_DEVICE) return fail(TTC_ERR_ARG, "mem_kind");
   if (mem_kind == TTC_MEM_HOST) {
     for (long long t = 0; t < (long long)k.d * k.n; ++t)
@@ -533,13 +536,15 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     return e;
   };
   int e = 0;
-  double *u = nullptr, *w = nullptr;
+  double *u = nullptr, *w = nullptr, *wf = nullptr;
   long long *chi = nullptr, *clo = nullptr;
   if ((e = dalloc(c, &u, (size_t)d * n)) || (e = dalloc(c, &w, (size_t)d * n)) ||
+      (k.fold_weights && (e = dalloc(c, &wf, (size_t)d * n))) ||
       (e = dalloc(c, &chi, (size_t)d * n)) || (e = dalloc(c, &clo, (size_t)d * n)))
     return bail(e);
   dc.u = u;
   dc.w = w;
+  dc.wf = wf;
   dc.chi = chi;
   dc.clo = clo;
   const size_t tab = (size_t)nj * cap * n;
@@ -736,7 +741,13 @@ int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights,
   if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   const cudaMemcpyKind kind = mem_kind == TTC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   CK(cudaMemcpyAsync(const_cast<double*>(c->dc.u), nodes_u, sizeof(double) * d * n, kind, c->stream));
-  CK(cudaMemcpyAsync(const_cast<double*>(c->dc.w), weights, sizeof(double) * d * n, kind, c->stream));
+  if (c->dc.wf) {  // folded: the entries carry the weights, the contraction sums with ones
+    CK(cudaMemcpyAsync(const_cast<double*>(c->dc.wf), weights, sizeof(double) * d * n, kind, c->stream));
+    k_fill<<<(d * n + 255) / 256, 256, 0, c->stream>>>(const_cast<double*>(c->dc.w), 1.0, (long long)d * n);
+    if (int e = check_launch("k_fill")) return e;
+  } else {
+    CK(cudaMemcpyAsync(const_cast<double*>(c->dc.w), weights, sizeof(double) * d * n, kind, c->stream));
+  }
   {
     Timed t(c, K_PREP);
     k_prep_nodes<<<(d * n + 255) / 256, 256, 0, c->stream>>>(c->dc.u, const_cast<long long*>(c->dc.chi),

@@ -39,8 +39,7 @@ __device__ __forceinline__ int init_coord(const DevCtx& c, int q, int j) {
 
 __device__ double init_entry(const DevCtx& c, int q) {
   const int d = c.d, n = c.n;
-  if (c.family >= 2)
-    return x_entry_dyn(c.family, d, [&](int j) { return c.u[j * n + init_coord(c, q, j)]; });
+  if (c.family >= 2) return x_entry_dyn(c.family, c.u, c.wf, d, n, [&](int j) { return init_coord(c, q, j); });
   ESum s = esum_zero();
   for (int j = 0; j < d; ++j) {
     const int t = init_coord(c, q, j);
@@ -197,10 +196,8 @@ __device__ __forceinline__ double sb_entry(const DevCtx& c, int job, int k, int 
     const int d = c.d;
     const int* TL = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d : nullptr;
     const int* TR = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d : nullptr;
-    return x_entry<FAMILY>(d, [&](int j) {
-      const int node = j < k ? TL[j] : (j == k ? a : (j == k + 1 ? b : TR[j]));
-      return c.u[(long long)j * n + node];
-    });
+    return x_entry_at<FAMILY>(c.u, c.wf, d, n,
+                              [&](int j) { return j < k ? TL[j] : (j == k ? a : (j == k + 1 ? b : TR[j])); });
   }
   const long long oa = ((long long)job * c.cap + al) * n;
   const long long ob = ((long long)job * c.cap + be) * n;

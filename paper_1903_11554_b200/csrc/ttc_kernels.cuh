@@ -124,6 +124,11 @@ __global__ void k_frozen_lr(DevCtx c, int kind, int jbase) {
   c.pf[(base + al) * c.cap + be] = p;
 }
 
+__global__ void k_fill(double* p, double v, long long count) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count; t += (long long)gridDim.x * blockDim.x)
+    p[t] = v;
+}
+
 // ---------------------------------------------------------------------------------------
 // fiber entries: grid x = flat (beta*n + a) chunks, y = alpha, z = job
 // ---------------------------------------------------------------------------------------
@@ -178,10 +183,7 @@ __global__ void __launch_bounds__(256) k_fiber_x(DevCtx c, int kind, int jbase) 
     const int be = f / n;
     const int a = f - be * n;
     const int* TY = jb.Y ? jb.Y + (long long)be * d : nullptr;
-    F[f] = x_entry<FAM>(d, [&](int q) {
-      const int node = q < m ? TX[q] : (q == m ? a : TY[q]);
-      return c.u[(long long)q * n + node];
-    });
+    F[f] = x_entry_at<FAM>(c.u, c.wf, d, n, [&](int q) { return q < m ? TX[q] : (q == m ? a : TY[q]); });
   }
 }
 
@@ -201,7 +203,7 @@ __global__ void k_intersection(DevCtx c, int ibase) {
   const int* Pt = rec_piv(c.rec_cur, c.RS, i) + (long long)t * d;
   if (c.family >= 2) {
     c.M[((long long)i * c.cap + s) * c.cap + t] =
-        x_entry_dyn(c.family, d, [&](int q) { return c.u[(long long)q * n + (q <= i ? Ps[q] : Pt[q])]; });
+        x_entry_dyn(c.family, c.u, c.wf, d, n, [&](int q) { return q <= i ? Ps[q] : Pt[q]; });
     return;
   }
   ESum S = esum_zero();

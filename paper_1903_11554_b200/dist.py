@@ -82,13 +82,14 @@ class DistTTCross:
     All device work (the library's and NCCL's) is ordered on torch's current CUDA stream.
     """
 
-    def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, group=None):
+    def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, group=None,
+                 fold_weights=False):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.stream = torch.cuda.current_stream()
         self.tt = TTCross(family, u, w, rank_cap, tol, n_samples=n_samples, rook_iters=rook_iters, seed=seed,
-                          rank=self.rank, world=self.world, stream=self.stream.cuda_stream)
+                          rank=self.rank, world=self.world, stream=self.stream.cuda_stream, fold_weights=fold_weights)
         dev = torch.device("cuda", torch.cuda.current_device())
         xv, xper = self.tt.exchange_view()
         self.xbuf = torch.as_tensor(xv, device=dev)

@@ -46,13 +46,14 @@ def test_build_info_and_error_string(lib):
 
 def good_config(binding):
     # family, d, n, rank_cap, n_samples, rook_iters, tol, seed, rank, world
-    return binding.TtcConfig(0, 4, 9, 4, 16, 4, 1e-12, 1, 0, 1)
+    return binding.TtcConfig(0, 4, 9, 4, 16, 4, 1e-12, 1, 0, 1, 0)
 
 
 @pytest.mark.parametrize("field,value", [("d", 1), ("d", 2001), ("n", 1), ("n", 4097), ("rank_cap", 0),
                                          ("rank_cap", 65), ("family", 7), ("n_samples", 0),
                                          ("n_samples", 1025), ("rook_iters", -1), ("rook_iters", 65),
-                                         ("tol", 1.5), ("tol", -1.0), ("world", 0), ("rank", 1)])
+                                         ("tol", 1.5), ("tol", -1.0), ("world", 0), ("rank", 1),
+                                         ("fold_weights", 1), ("fold_weights", 2), ("family", 5)])
 def test_invalid_arguments_rejected_without_gpu(lib, field, value):
     from paper_1903_11554_b200 import binding
     cfg = good_config(binding)
@@ -67,7 +68,7 @@ def test_invalid_arguments_rejected_without_gpu(lib, field, value):
 
 def test_nonpositive_nodes_rejected(lib):
     from paper_1903_11554_b200 import binding
-    cfg = binding.TtcConfig(0, 3, 5, 4, 16, 4, 1e-12, 1, 0, 1)
+    cfg = binding.TtcConfig(0, 3, 5, 4, 16, 4, 1e-12, 1, 0, 1, 0)
     u = np.ones((3, 5))
     u[1, 2] = -1.0
     h = ctypes.c_void_p()
@@ -81,6 +82,6 @@ def test_config_struct_layout_matches_header():
     """The ctypes mirror of ttc_config / ttc_stats has the C layout (offsets from the header's
     field order and natural alignment)."""
     from paper_1903_11554_b200 import binding
-    assert ctypes.sizeof(binding.TtcConfig) == 6 * 4 + 8 + 8 + 2 * 4
+    assert ctypes.sizeof(binding.TtcConfig) == 6 * 4 + 8 + 8 + 3 * 4 + 4  # trailing pad to 8
     assert binding.TtcConfig.tol.offset == 24 and binding.TtcConfig.seed.offset == 32
     assert ctypes.sizeof(binding.TtcStats) == 8 + 8 + 4 + 4 + 4 * 8 + 6 * 8

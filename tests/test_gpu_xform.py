@@ -15,11 +15,11 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
-def run_pair(family, d, n, cap, sweeps, ns=16, rook=4, seed=5, tol=1e-14):
+def run_pair(family, d, n, cap, sweeps, ns=16, rook=4, seed=5, tol=1e-14, fold=False):
     from paper_1903_11554_b200 import TTCross
     x, w = xform_grid(d, n)
-    tt = TTCross(family, x, w, cap, tol, n_samples=ns, rook_iters=rook, seed=seed)
-    prob = X.Problem(family, x, w, cap, tol, ns, rook, seed)
+    tt = TTCross(family, x, w, cap, tol, n_samples=ns, rook_iters=rook, seed=seed, fold_weights=fold)
+    prob = X.Problem(family, x, w, cap, tol, ns, rook, seed, fold)
     st = X.initial_state(prob)
     for s in range(sweeps):
         tt.sweep(1)
@@ -51,3 +51,19 @@ def test_xform_d8_against_paper(lib):
     val = run_pair(wl.family, wl.d, wl.n, wl.rank_cap, wl.sweeps, wl.n_samples, wl.rook_iters, wl.seed, wl.tol)
     ref = float(json.load(open(os.path.join(GOLD, "paper_values.json")))["D"]["8"])
     assert abs(val - ref) < 1e-9 * ref, (val, ref)
+
+
+@pytest.mark.parametrize("family,d,n,cap,sweeps", [(FAMILY_CX, 5, 17, 8, 8), (FAMILY_DX, 6, 13, 8, 8)])
+def test_xform_folded_parity(lib, family, d, n, cap, sweeps):
+    """Weights folded into the tensor (§4.1): bit-exact as well."""
+    run_pair(family, d, n, cap, sweeps, fold=True)
+
+
+def test_xform_d8_folded_against_paper(lib):
+    """Folding converges faster: rank 24 reaches ~4e-12 of the printed
+    D_8 (unfolded: ~2e-11)."""
+    wl = X_WORKLOADS["Dx8f"]
+    val = run_pair(wl.family, wl.d, wl.n, wl.rank_cap, wl.sweeps, wl.n_samples, wl.rook_iters, wl.seed, wl.tol,
+                   fold=True)
+    ref = float(json.load(open(os.path.join(GOLD, "paper_values.json")))["D"]["8"])
+    assert abs(val - ref) < 2e-11 * ref, (val, ref)

@@ -302,3 +302,15 @@ def test_xform_d8_reproduces_paper_value():
     st, val, _ = X.run(prob, wl.sweeps)
     ref = float(json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))["D"]["8"])
     assert abs(val - ref) < 1e-9 * ref, (val, ref)
+
+
+def test_folded_weights_integrate_to_the_same_grid_sum():
+    """B = w x ... x w * f contracted with unit weights equals f contracted with w, both
+    against the full Gauss-Legendre grid sum (small exact-enough cross)."""
+    from workloads import FAMILY_DX, xform_grid
+    x, w = xform_grid(4, 7)
+    ref = ig.brute_force(FAMILY_DX, x, w)
+    for fold in (False, True):
+        prob = X.Problem(FAMILY_DX, x, w, 7, 1e-14, 64, 4, 3, fold)   # rank 7 = full rank here
+        st, val, _ = X.run(prob, 8)
+        assert abs(val - ref) < 1e-12 * abs(ref), (fold, val, ref)

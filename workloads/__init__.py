@@ -78,6 +78,7 @@ class Workload:
     rook_iters: int = 4      # rook rounds of Alg. 2 (R6)
     seed: int = 20190327
     note: str = ""
+    fold: bool = False       # cross on w x ... x w * f (§4.1)
 
     @property
     def alg6_sweeps(self) -> int:
@@ -122,4 +123,6 @@ X_WORKLOADS = {
     "Dx8": Workload("Dx8", FAMILY_DX, 8, 33, 0.0, 24, 1e-14, 24, note="D_8, 33-pt Gauss-Legendre, rank cap 24"),
     "Cx64": Workload("Cx64", FAMILY_CX, 64, 33, 0.0, 16, 1e-14, 16, note="C_64, 33-pt Gauss-Legendre, rank cap 16"),
     "Ex6": Workload("Ex6", FAMILY_EX, 6, 33, 0.0, 20, 1e-14, 20, note="E_6, 33-pt Gauss-Legendre, rank cap 20"),
+    "Dx8f": Workload("Dx8f", FAMILY_DX, 8, 33, 0.0, 24, 1e-14, 24, fold=True,
+                     note="D_8, 33-pt Gauss-Legendre, rank cap 24, weights folded into the tensor"),
 }
