@@ -137,17 +137,34 @@ __device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int
     hi = d;
   }
   if (!T) hi = lo;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // the frozen tuple's S (exact limbs) and P (double-double) by warp 0: lanes split the
+    // coordinates and the pair rows, then a shuffle reduction -- any order gives the same
+    // rounded entries (R3)
+    const int lane = threadIdx.x;
     ESum s = esum_zero();
     DDE p = dde_one();
-    for (int q = lo; q < hi; ++q) esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
+    for (int q = lo + lane; q < hi; q += 32) esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
     if (c.family == 1)
-      for (int a = lo; a < hi; ++a) {
+      for (int a = lo + lane; a < hi; a += 32) {
         const double ua = c.u[a * n + T[a]];
         for (int b = a + 1; b < hi; ++b) dde_mul_d(p, rho_ool(ua, c.u[b * n + T[b]]));
       }
-    sS = s;
-    sP = p;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s.h += __shfl_xor_sync(0xffffffffu, s.h, o);
+      s.l += __shfl_xor_sync(0xffffffffu, s.l, o);
+      DDE y;
+      y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
+      y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
+      y.e = __shfl_xor_sync(0xffffffffu, p.e, o);
+      y.pad = 0;
+      dde_mul(p, y);
+    }
+    if (lane == 0) {
+      sS = s;
+      sP = p;
+    }
   }
   __syncthreads();
   const long long o = ((long long)job * c.cap + slot) * n;
@@ -236,6 +253,9 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
+// ranks above which the extension recurrence runs a warp per row (lanes over s) instead of
+// a thread per row (measured: thread-per-row wins at r = 16 and r = 64; kept for r > 64)
+#define EXT_WARP_RANK 64
 
 template <int FAMILY>
 __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
@@ -268,16 +288,36 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
                                    : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
     }
     __syncthreads();
-    // (2) the recurrence, a thread per row, column-oriented (t outer, s > t inner): for every
-    // s the same subtractions in the same t order as the oracle's row-oriented sum
-    for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
-      for (int t = 0; t < r; ++t) {
-        double f = tile[t * TS + j];
-        if (side == 1) {
-          f = __ddiv_rn(f, pdiag[t]);  // v_t final
-          tile[t * TS + j] = f;
+    // (2) the recurrence, column-oriented (t outer, s > t inner): for every s the same
+    // subtractions in the same t order as the oracle's row-oriented sum.  Small ranks: a
+    // thread per row (short chains, many rows); large ranks: a warp per row, lanes over s.
+    if (r <= EXT_WARP_RANK) {
+      for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
+        for (int t = 0; t < r; ++t) {
+          double f = tile[t * TS + j];
+          if (side == 1) {
+            f = __ddiv_rn(f, pdiag[t]);  // v_t final
+            tile[t * TS + j] = f;
+          }
+          for (int q = t + 1; q < r; ++q)
+            tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
         }
-        for (int q = t + 1; q < r; ++q) tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
+      }
+    } else {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int j = warp; j < nrow; j += nw) {
+        double acc0 = lane < r ? tile[lane * TS + j] : 0.0;
+        double acc1 = lane + 32 < r ? tile[(lane + 32) * TS + j] : 0.0;
+        for (int t = 0; t < r; ++t) {
+          double f = __shfl_sync(0xffffffffu, t < 32 ? acc0 : acc1, t & 31);
+          if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t final
+          if (t < 32 && lane == t) acc0 = f;
+          if (t >= 32 && lane == t - 32) acc1 = f;
+          if (lane > t) acc0 = __dsub_rn(acc0, __dmul_rn(f, coef[t * cap + lane]));
+          if (lane + 32 > t && lane + 32 < r) acc1 = __dsub_rn(acc1, __dmul_rn(f, coef[t * cap + lane + 32]));
+        }
+        if (lane < r) tile[lane * TS + j] = acc0;
+        if (lane + 32 < r) tile[(lane + 32) * TS + j] = acc1;
       }
     }
     __syncthreads();
