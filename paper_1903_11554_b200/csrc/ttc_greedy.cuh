@@ -242,7 +242,7 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 
 // ---------------------------------------------------------------------------------------
 // phase 2: u/v of the existing pivots on the rows / columns that are new this sweep, in tiles
-// of EXT_TILE rows: (1) all raw entries A(x, y_s) (A(x_s, y)) of the tile at once, one per
+// of c.ext_tile rows: (1) all raw entries A(x, y_s) (A(x_s, y)) of the tile at once, one per
 // thread, into shared memory -- the batched fiber evaluation; (2) a thread per row runs the
 // triangular recurrence column-oriented:
 //   for t = 0..r-1: u_t final; acc_s -= u_t * V[t][y_s]  (s > t)
@@ -253,9 +253,6 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
-// ranks above which the extension recurrence runs a warp per row (lanes over s) instead of
-// a thread per row (measured: thread-per-row wins at r = 16 and r = 64; kept for r > 64)
-#define EXT_WARP_RANK 64
 
 template <int FAMILY>
 __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
@@ -288,36 +285,18 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
                                    : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
     }
     __syncthreads();
-    // (2) the recurrence, column-oriented (t outer, s > t inner): for every s the same
-    // subtractions in the same t order as the oracle's row-oriented sum.  Small ranks: a
-    // thread per row (short chains, many rows); large ranks: a warp per row, lanes over s.
-    if (r <= EXT_WARP_RANK) {
-      for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
-        for (int t = 0; t < r; ++t) {
-          double f = tile[t * TS + j];
-          if (side == 1) {
-            f = __ddiv_rn(f, pdiag[t]);  // v_t final
-            tile[t * TS + j] = f;
-          }
-          for (int q = t + 1; q < r; ++q)
-            tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
+    // (2) the recurrence, a thread per row, column-oriented (t outer, s > t inner): for every
+    // s the same subtractions in the same t order as the oracle's row-oriented sum.  (A warp
+    // per row with lanes over s measured slower at r = 16 and at r = 64.)
+    for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
+      for (int t = 0; t < r; ++t) {
+        double f = tile[t * TS + j];
+        if (side == 1) {
+          f = __ddiv_rn(f, pdiag[t]);  // v_t final
+          tile[t * TS + j] = f;
         }
-      }
-    } else {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-      for (int j = warp; j < nrow; j += nw) {
-        double acc0 = lane < r ? tile[lane * TS + j] : 0.0;
-        double acc1 = lane + 32 < r ? tile[(lane + 32) * TS + j] : 0.0;
-        for (int t = 0; t < r; ++t) {
-          double f = __shfl_sync(0xffffffffu, t < 32 ? acc0 : acc1, t & 31);
-          if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t final
-          if (t < 32 && lane == t) acc0 = f;
-          if (t >= 32 && lane == t - 32) acc1 = f;
-          if (lane > t) acc0 = __dsub_rn(acc0, __dmul_rn(f, coef[t * cap + lane]));
-          if (lane + 32 > t && lane + 32 < r) acc1 = __dsub_rn(acc1, __dmul_rn(f, coef[t * cap + lane + 32]));
-        }
-        if (lane < r) tile[lane * TS + j] = acc0;
-        if (lane + 32 < r) tile[(lane + 32) * TS + j] = acc1;
+        for (int q = t + 1; q < r; ++q)
+          tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
       }
     }
     __syncthreads();
