@@ -119,6 +119,12 @@ int tt_cross_reset(ttc_ctx* ctx);
  * tt_cross_sweep -- n_sweeps dimension-parallel sweeps (Alg. 6): every superblock
  * adds at most one pivot found by Alg. 2 from the index sets of the previous sweep.
  * world == 1 only (multi-process callers use tt_cross_sweep_local + exchange + commit).
+ * When every superblock's thread-block cluster fits on the device at once (see
+ * tt_cross_get_launch_shape), the n sweeps run as ONE persistent launch in which superblock k
+ * starts sweep s as soon as superblocks k-1 and k+1 have published sweep s-1 (the
+ * neighbour-only exchange of Alg. 6 lines 6-8, through release/acquire flags); otherwise one
+ * launch per sweep.  Results are identical either way.  A neighbour wait longer than ~2 s
+ * (clusters not co-resident) is reported by the next tt_integrate* as TTC_ERR_CUDA.
  * Fully asynchronous on the context stream.
  */
 int tt_cross_sweep(ttc_ctx* ctx, int32_t n_sweeps);
