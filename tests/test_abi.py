@@ -85,3 +85,13 @@ def test_config_struct_layout_matches_header():
     assert ctypes.sizeof(binding.TtcConfig) == 6 * 4 + 8 + 8 + 3 * 4 + 4  # trailing pad to 8
     assert binding.TtcConfig.tol.offset == 24 and binding.TtcConfig.seed.offset == 32
     assert ctypes.sizeof(binding.TtcStats) == 8 + 8 + 4 + 4 + 4 * 8 + 6 * 8
+
+
+def test_c_demo_links_against_the_library(lib):
+    """examples/ttcross_demo.c uses the C-ABI from plain C; build() links it against the
+    in-tree libttcross.so."""
+    import subprocess
+    demo = os.path.join(ROOT, "examples", "ttcross_demo")
+    assert os.path.exists(demo)
+    out = subprocess.run(["ldd", demo], capture_output=True, text=True).stdout
+    assert "libttcross.so" in out and "not found" not in out.split("libttcross.so")[1].split("\n")[0]

@@ -284,3 +284,21 @@ def test_theorem1_interpolation_of_gpu_cross(lib, name, modes):
             assert abs(float(v[0]) - exact) <= max(1e-10, 1e-15 * conds * d) * max(abs(exact), 1e-300) \
                 or abs(float(v[0]) - exact) <= 1e-13 * np.max(np.abs(F)), (m, float(v[0]), exact)
     tt.close()
+
+
+def test_c_demo_matches_python_binding(lib):
+    """The plain-C program (examples/ttcross_demo.c) and the Python binding give the same
+    D_5 integral bit for bit (one library, no Python in the C path)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([os.path.join(root, "examples", "ttcross_demo")], capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0, out.stderr
+    c_val = float(out.stdout.split("D_5 = ")[1].split()[0])
+    wl = WORKLOADS["D5"]
+    tt, prob = make_wl(wl)
+    tt.sweep(wl.alg6_sweeps)
+    py_val = tt.integrate()[0]
+    tt.close()
+    assert c_val == py_val, (c_val, py_val)
