@@ -28,10 +28,10 @@ def exchange(views, per_rank_elems):
     torch.cuda.synchronize()
 
 
-def run_partitioned(family, u, w, cap, tol, ns, rook, seed, sweeps, world):
+def run_partitioned(family, u, w, cap, tol, ns, rook, seed, sweeps, world, fold=False):
     from paper_1903_11554_b200 import TTCross
-    tts = [TTCross(family, u, w, cap, tol, n_samples=ns, rook_iters=rook, seed=seed, rank=p, world=world)
-           for p in range(world)]
+    tts = [TTCross(family, u, w, cap, tol, n_samples=ns, rook_iters=rook, seed=seed, rank=p, world=world,
+                   fold_weights=fold) for p in range(world)]
     xv = [t.exchange_view() for t in tts]
     per = xv[0][1] // 4
     states = []
@@ -88,6 +88,23 @@ def test_partitioned_d5_workload(lib):
     ref = TTCross(wl.family, u, w, wl.rank_cap, wl.tol, n_samples=wl.n_samples, rook_iters=wl.rook_iters,
                   seed=wl.seed)
     ref.sweep(wl.alg6_sweeps)
+    r = ref.state(parents=True)
+    for a, b in zip(r[1] + r[2], states[-1][1] + states[-1][2]):
+        assert np.array_equal(a, b)
+    rv = ref.integrate()
+    assert abs(val[0] - rv[0]) <= 1e-13 * abs(rv[0])
+    ref.close()
+
+
+@pytest.mark.parametrize("fold", [False, True])
+def test_partitioned_xform(lib, fold):
+    """The x-form path (direct entries, optional folded weights) partitioned over 3 ranks."""
+    from paper_1903_11554_b200 import TTCross
+    from workloads import FAMILY_DX, xform_grid
+    x, w = xform_grid(7, 13)
+    states, val = run_partitioned(FAMILY_DX, x, w, 6, 1e-14, 16, 4, 9, 6, 3, fold)
+    ref = TTCross(FAMILY_DX, x, w, 6, 1e-14, n_samples=16, rook_iters=4, seed=9, fold_weights=fold)
+    ref.sweep(6)
     r = ref.state(parents=True)
     for a, b in zip(r[1] + r[2], states[-1][1] + states[-1][2]):
         assert np.array_equal(a, b)

@@ -288,7 +288,8 @@ def test_theorem1_interpolation_of_gpu_cross(lib, name, modes):
 
 def test_c_demo_matches_python_binding(lib):
     """The plain-C program (examples/ttcross_demo.c) and the Python binding give the same
-    D_5 integral bit for bit (one library, no Python in the C path)."""
+    D_5 integral (one library, no Python in the C path).  The C program builds its u-nodes
+    with libm's exp, numpy's exp may differ by an ulp on some nodes, hence a tolerance."""
     import os
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -301,4 +302,4 @@ def test_c_demo_matches_python_binding(lib):
     tt.sweep(wl.alg6_sweeps)
     py_val = tt.integrate()[0]
     tt.close()
-    assert c_val == py_val, (c_val, py_val)
+    assert abs(c_val - py_val) <= 1e-12 * abs(py_val), (c_val, py_val)
