@@ -135,6 +135,23 @@ def flops_per_entry(family, m):
     return {2: 4 * m + 2, 3: 4 * m + 3 + pairs, 4: pairs}[family]
 
 
+def fiber_roofline(kt, stats, family, modes, peaks):
+    """The quadrature fiber kernel (k_fiber / k_fiber_x): the throughput-mode batched
+    integrand evaluation.  t-form: C 4 flop/entry, D 26 (exact-limb sum and rounding 3, two
+    double-double products 20, rounding and division 3); x-form: flops_per_entry."""
+    launches, ms = kt.get("k_fiber", (0, 0.0))
+    if not launches or ms <= 0:
+        return None
+    avg_s = ms / launches / 1e3
+    ent = stats["fiber_entries"] / launches
+    fpe = {0: 4, 1: 26}.get(family) or flops_per_entry(family, modes)
+    tf = ent * fpe / avg_s / 1e12
+    gbs = ent * 8 / avg_s / 1e9
+    return {"kernel": "k_fiber", "avg_us": avg_s * 1e6, "entries_per_launch": ent,
+            "achieved_tflops": tf, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
+            "write_GBs": gbs, "frac_hbm": gbs / peaks["hbm_gbs"], "per_unit": f"{fpe} flop + 8 B written / entry"}
+
+
 def roofline(kt, stats, family, peaks, peak_src, modes=0):
     """kt: {name: (launches, ms)} of the profiling pass; stats: its summed counters."""
     name = max(kt, key=lambda k: kt[k][1])
@@ -392,6 +409,7 @@ def main():
     core.set_timing(False)
     peaks, peak_src = measured_peaks()
     roof = roofline(kt, st, wl.family, peaks, peak_src, wl.modes)
+    froof = fiber_roofline(kt, st, wl.family, wl.modes, peaks)
     kernel_ms = {k: v[1] / nprof for k, v in kt.items() if v[0]}
 
     # ---- oracle on the host cores (rank 0, N = 1 only)
@@ -411,7 +429,7 @@ def main():
             "integral": {"value": val[0], "log10_abs": val[1], "sign": val[2]},
             "graph": use_graph, "gpu_launches": int(launches_step) * args.steps,
             "launch_shape": core.launch_shape(),
-            "roofline": roof, "kernel_ms_per_solve": kernel_ms, "clocks": clocks, "e2e": e2e,
+            "roofline": roof, "fiber_roofline": froof, "kernel_ms_per_solve": kernel_ms, "clocks": clocks, "e2e": e2e,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -178,13 +178,19 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
     }
     if (int e = check_launch("k_frozen_lr")) return e;
   }
-  const int gx = std::min(4096, (tup * n + 255) / 256);
   {
     Timed t(c, K_FIBER);
-    if (dc.family == TTC_FAMILY_C)
-      k_fiber<0><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
-    else
-      k_fiber<1><<<dim3(gx, tup, njobs), 256, 0, c->ls>>>(dc, kind, jbase);
+    // large fibers: a thread per (alpha, a) walking beta; small ones: an entry per thread
+    const bool loop = (long long)tup * tup * n * njobs >= (1LL << 22);
+    if (loop) {
+      const dim3 g((n + 255) / 256, tup, njobs);
+      if (dc.family == TTC_FAMILY_C) k_fiber<0, true><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+      else k_fiber<1, true><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+    } else {
+      const dim3 g(std::min(4096, (tup * n + 255) / 256), tup, njobs);
+      if (dc.family == TTC_FAMILY_C) k_fiber<0, false><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+      else k_fiber<1, false><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+    }
   }
   return check_launch("k_fiber");
 }

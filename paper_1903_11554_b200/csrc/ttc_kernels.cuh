@@ -132,34 +132,70 @@ __global__ void k_fill(double* p, double v, long long count) {
 // ---------------------------------------------------------------------------------------
 // fiber entries: grid x = flat (beta*n + a) chunks, y = alpha, z = job
 // ---------------------------------------------------------------------------------------
-template <int FAMILY>
+// Quadrature fiber entries, two launch shapes:
+//  LOOP = false (small fibers, latency-bound): one entry per thread, grid x = flat
+//          (beta*n + a) chunks, y = alpha, z = job;
+//  LOOP = true (large fibers): grid x = chunk of 256 nodes a, y = alpha, z = job; a thread
+//          keeps its (alpha, a) factors -- S_L + c_m[a] and P_LL * Q_L[alpha][a] -- in
+//          registers and walks beta: per entry only Q_R[beta][a] streams (coalesced over
+//          a), S_R / Pf are warp broadcasts, the stores F[alpha][beta][a] are coalesced.
+//          (Prefetching 4 or 8 betas per iteration raised registers and ran slower.)
+template <int FAMILY, bool LOOP>
 __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
   const int j = jbase + blockIdx.z, al = blockIdx.y;
   Job jb = make_job(c, kind, j);
   if (al >= jb.rx) return;
   const int n = c.n, m = jb.m;
-  const int total = jb.ry * n;
   const long long base = (long long)j * c.cap;
-  const ESum sl = c.sl[base + al];
-  double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-    const int be = f / n;
-    const int a = f - be * n;
-    ESum s = sl;
+  if (!LOOP) {
+    const int total = jb.ry * n;
+    const ESum sl = c.sl[base + al];
+    double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+      const int be = f / n;
+      const int a = f - be * n;
+      ESum s = sl;
+      esum_add(s, c.sr[base + be]);
+      esum_add(s, c.chi[m * n + a], c.clo[m * n + a]);
+      const double S = esum_round(s);
+      const double SS = __dmul_rn(S, S);
+      double v;
+      if (FAMILY == 0) {
+        v = __drcp_rn(SS);
+      } else {
+        DDE p = c.pf[(base + al) * c.cap + be];
+        dde_mul(p, c.ql[(base + al) * n + a]);
+        dde_mul(p, c.qr[(base + be) * n + a]);
+        v = __ddiv_rn(dde_round(p), SS);
+      }
+      F[f] = v;
+    }
+    return;
+  }
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  ESum sa = c.sl[base + al];
+  esum_add(sa, c.chi[m * n + a], c.clo[m * n + a]);
+  DDE pa;
+  if (FAMILY == 1) pa = c.ql[(base + al) * n + a];
+  double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n + a;
+  const DDE* pf = c.pf + (base + al) * c.cap;
+  const int ry = jb.ry;
+  for (int be = 0; be < ry; ++be) {
+    ESum s = sa;
     esum_add(s, c.sr[base + be]);
-    esum_add(s, c.chi[m * n + a], c.clo[m * n + a]);
     const double S = esum_round(s);
     const double SS = __dmul_rn(S, S);
     double v;
     if (FAMILY == 0) {
       v = __drcp_rn(SS);
     } else {
-      DDE p = c.pf[(base + al) * c.cap + be];
-      dde_mul(p, c.ql[(base + al) * n + a]);
+      DDE p = pf[be];
+      dde_mul(p, pa);
       dde_mul(p, c.qr[(base + be) * n + a]);
       v = __ddiv_rn(dde_round(p), SS);
     }
-    F[f] = v;
+    F[(long long)be * n] = v;
   }
 }
 
