@@ -477,6 +477,17 @@ extern "C" {
 
 const char* tt_last_error(void) { return g_err.c_str(); }
 
+#ifdef TTC_TRACE
+// trace build only (tools/trace_steps.py): copy out and clear the step trace
+int ttc_trace_read(unsigned long long* events, int* counts) {
+  if (cudaMemcpyFromSymbol(events, ttc::g_trace, sizeof(ttc::g_trace)) != cudaSuccess) return TTC_ERR_CUDA;
+  if (cudaMemcpyFromSymbol(counts, ttc::g_trace_n, sizeof(ttc::g_trace_n)) != cudaSuccess) return TTC_ERR_CUDA;
+  static int zero[TTC_TRACE_SLOTS];
+  if (cudaMemcpyToSymbol(ttc::g_trace_n, zero, sizeof(zero)) != cudaSuccess) return TTC_ERR_CUDA;
+  return TTC_OK;
+}
+#endif
+
 const char* tt_build_info(void) {
   return "libttcross 0.2 (sm_100a, fp64, -fmad=false, dimension-parallel greedy cross, cluster rook search)";
 }

@@ -355,6 +355,7 @@ struct GreedySmem {
   DDE f_node[STAGE_N];               // column step: QR0[beta][a]; row step: QL1[alpha][b]
   ESum fs;                           // SB[beta][b] (column step) or SA[alpha][a] (row step)
   DDE fp;                            // PB[beta][b] or PA[alpha][a]
+  double pv;                         // E(x*, y*) of the final pivot (owner CTA of column y*)
 };
 
 // CTA-wide argmax of (v, f) -> S.best (all threads call)
@@ -447,6 +448,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
   const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, xb = X.xb, xe = X.xe, rpcap = X.rpcap;
   const int be = y / n, b = y - (y / n) * n;
+  TRACE(10);
   if (tid < r) S.vec[tid] = X.V[tid * sbn + y];
   if (tid == 0 && FAMILY < 2) {
     S.fs = c.SB[jo + (long long)be * n + b];
@@ -462,6 +464,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + (long long)be * n + a];
   }
   __syncthreads();
+  TRACE(11);
   const double ub = X.uk1[b];
   double bv = -1.0;
   long long bf = LLONG_MAX;
@@ -522,6 +525,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
   const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, yb = X.yb, ye = X.ye, rpcap = X.rpcap;
   const int al = x / n, a = x - (x / n) * n;
+  TRACE(20);
   if (tid < r) S.vec[tid] = X.U[tid * sbn + x];
   if (tid == 0 && FAMILY < 2) {
     S.fs = c.SA[jo + x];
@@ -537,6 +541,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + (long long)al * n + b];
   }
   __syncthreads();
+  TRACE(21);
   const double ua = X.uk[a];
   double bv = -1.0;
   long long bf = LLONG_MAX;
@@ -589,6 +594,7 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
   warp_argmax(v, f);
   if (lane == 0) S->red[warp] = {v, f};
   __syncthreads();
+  TRACE(31);
   if (warp == 0) {
     const int nw = blockDim.x >> 5;
     double bv = lane < nw ? S->red[lane].val : -1.0;
@@ -606,8 +612,10 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
     __syncthreads();
     return;
   }
+  TRACE(32);
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  TRACE(33);
   if (warp == 0) {
     double bv = -1.0;
     long long bf = LLONG_MAX;
@@ -620,6 +628,7 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
     if (lane == 0) S->best = {bv, bf};
   }
   __syncthreads();
+  TRACE(34);
 }
 
 // One Alg. 6 sweep of superblock `job` (all CTAs of its cluster): phases 1-3 with the ranks
@@ -677,6 +686,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   const int rows_done = c.sbstate[job * 4 + 0], cols_done = c.sbstate[job * 4 + 1];
   const bool first = rows_done == 0 && cols_done == 0;
   __syncthreads();
+  TRACE(1);
   unsigned long long ext_ent = 0, ext_upd = 0;
 
   // ---- phase 1: factor tables of the new left slots [rows_done, rl) and right slots
@@ -708,7 +718,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       sb_cx_table(c, job, al, be, rl, rr);
     }
   }
+  TRACE(2);
   cl.sync();  // tables visible to the whole cluster
+  TRACE(3);
   phase(PH_TABLES);
 
   // ---- phase 2: u / v of the existing pivots on the new rows and columns
@@ -748,7 +760,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
                           ext_ent, ext_upd);
     }
   }
+  TRACE(4);
   cl.sync();  // u / v of the new rows and columns visible to the whole cluster
+  TRACE(5);
   phase(PH_EXTEND);
 
   bool active = r < cap;
@@ -803,6 +817,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         }
       }
       cp_async_wait_all();
+      TRACE(6);
       // visibility of the cache to the other threads: the __syncthreads of the first step
     }
     // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically)
@@ -823,6 +838,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         if (masked) e = 0.0;
         if (cand_better(fabs(e), q, bv, bf)) { bv = fabs(e); bf = q; }
       }
+      TRACE(7);
       argmax_step(&S, bv, bf, 1, 0);   // CTA-local: every CTA drew the same samples
       const int q = (int)S.best.idx;
       xst = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
@@ -933,9 +949,15 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
 #pragma unroll 1
       for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
     }
-    if (G > 1) cl.sync();  // U[r][:], V[r][:], Araw visible to the whole cluster
+    // the pivot value E(x*, y*) is read from the shared memory of the CTA owning column y*,
+    // not from V[r][y*]: that CTA rescales V[r][:] in place right after the barrier
+    const int own = (int)(yst / cpc);
+    if (cr == own && tid == 0) S.pv = CACHED ? Erow[yst - yb] : V[r * sbn + yst];
+    TRACE(8);
+    if (G > 1) cl.sync();  // U[r][:], V[r][:], Araw, S.pv visible to the whole cluster
     else __syncthreads();
-    const double pv = V[r * sbn + yst];
+    TRACE(9);
+    const double pv = G > 1 ? cl.map_shared_rank(&S.pv, own)[0] : S.pv;
     raw_star = Araw[xst];
     if (fabs(pv) > c.tol * scale) {
       added = true;
@@ -977,7 +999,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
+  TRACE(40);
   if (G > 1) cl.sync();  // no CTA may leave while another can still read its shared memory
+  TRACE(41);
   phase(PH_END);
   if (timer) atomicAdd(&c.phase_ns[PH_LAUNCHES], 1ULL);
   return added ? r + 1 : r;
@@ -1007,6 +1031,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   const int rr = k < d - 2 ? rec_rank(c.rec_cur, c.RS, k + 1) : 1;
   int* Rn = c.rec_next + (long long)k * c.RS;
   const int* Rc = c.rec_cur + (long long)k * c.RS;
+  TRACE_INIT();
   if (cl.block_rank() == 0)
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
   __syncthreads();
@@ -1015,6 +1040,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
     c.done[k] = sweep + 1;
   }
+  TRACE_FLUSH();
 }
 
 // Sweeps [s0, s0 + nsweeps) in one launch (world == 1, all clusters resident): superblock k
@@ -1026,14 +1052,20 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
 template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
   __shared__ GreedySmem S;
-  __shared__ int s_abort;
+  __shared__ int s_abort, s_any;
   extern __shared__ double dyn[];
   cg::cluster_group cl = cg::this_cluster();
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   int* Rk = c.rec_cur + (long long)k * c.RS;
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
+  TRACE_INIT();
   for (int s = s0; s < s0 + nsweeps; ++s) {
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    TRACE_FLUSH();
+    TRACE(49);
+    // every CTA acquires the neighbours' flags itself: the acquire also makes this SM's L1
+    // drop lines of neighbour data (records, rank ring) cached in an earlier sweep, which a
+    // cluster barrier after a single CTA's acquire does not guarantee
+    if (threadIdx.x == 0) {
       int abort = 0;
       const long long t0 = clock64();
       if (k > 0)
@@ -1045,9 +1077,16 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort = abort;
     }
-    cl.sync();  // the acquire of thread 0 orders every CTA's reads of the neighbours' records
-    if (cl.map_shared_rank(&s_abort, 0)[0]) break;
+    TRACE(50);
     cl.sync();
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int i = 0; i < (int)cl.num_blocks(); ++i) any |= cl.map_shared_rank(&s_abort, i)[0];
+      s_any = any;
+    }
+    cl.sync();  // s_abort may be rewritten only after every CTA has read it
+    TRACE(51);
+    if (s_any) break;
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
     r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk);
@@ -1056,6 +1095,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
       st_release(&c.done[k], s + 1);  // the record writes above happen-before this release
     }
   }
+  TRACE_FLUSH();
 }
 
 }  // namespace ttc

@@ -7,8 +7,12 @@ CTAs and ragged tails; the BASELINE configs C_4, D_5 and C_10 run whole; D_20 an
 checked on their first sweeps (the oracle's cost grows like r^3 n d^2 per sweep) plus
 size-independent properties of the full run.
 """
+import os
+
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 from oracle import cross as X
 from oracle import integrand as ig
@@ -303,3 +307,15 @@ def test_c_demo_matches_python_binding(lib):
     py_val = tt.integrate()[0]
     tt.close()
     assert abs(c_val - py_val) <= 1e-12 * abs(py_val), (c_val, py_val)
+
+
+def test_perturbed_timing_same_pivots(lib):
+    """Race detector: the step-trace build (thread 0 of every CTA delayed at every phase and
+    rook-step boundary) must reproduce the product build's pivots exactly, run after run, on
+    a cached (D_5) and an uncached 16-CTA-cluster (C_10) configuration.  This caught a read of
+    the pivot value E(x*, y*) racing with its owner's in-place rescaling of V[r][:]."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_trace_build.py"), "C10", "D5"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
