@@ -117,7 +117,7 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 //                                QR0 = prod_{j>k+1} rho(u_k[a], Y_j)
 // blockIdx.z >= 2*jobs (family D): CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j)
 // for the new (alpha, beta) pairs, z = 2*jobs + job, y = alpha, x*128 + tid = beta.
-__device__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride, int rl,
+__device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride, int rl,
                                int rr) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int* st = c.sbstate + job * 4;
@@ -255,11 +255,11 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 #define EXT_SMEM_DOUBLES 8192
 
 template <int FAMILY>
-__device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, long long x_lo, long long x_hi,
+__device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int side, int r, int x_lo, int x_hi,
                             const int* p_al, const int* p_a, const double* pdiag, double* coef, double* tile,
                             unsigned long long& ent, unsigned long long& upd) {
   const int n = c.n, cap = c.cap;
-  const long long sbn = c.sbn;
+  const int sbn = (int)c.sbn;
   double* U = c.U + (long long)job * cap * sbn;
   double* V = c.V + (long long)job * cap * sbn;
   if (x_lo >= x_hi) return;
@@ -267,20 +267,20 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
     const int t = e / r, s = e - t * r;
     double v = 0.0;
     if (t < s) {
-      const long long q = (long long)p_al[s] * n + p_a[s];
-      v = side == 0 ? V[(long long)t * sbn + q] : U[(long long)t * sbn + q];
+      const int q = p_al[s] * n + p_a[s];
+      v = side == 0 ? V[t * sbn + q] : U[t * sbn + q];
     }
     coef[t * cap + s] = v;
   }
   const int tile_rows = c.ext_tile, TS = c.ext_tile + 1;
   double* dst = side == 0 ? U : V;
-  for (long long x0 = x_lo; x0 < x_hi; x0 += tile_rows) {
-    const int nrow = (int)min((long long)tile_rows, x_hi - x0);
+  for (int x0 = x_lo; x0 < x_hi; x0 += tile_rows) {
+    const int nrow = min(tile_rows, x_hi - x0);
     // (1) raw entries of the tile, one per thread
     for (int e = threadIdx.x; e < nrow * r; e += blockDim.x) {
       const int s = e / nrow, j = e - s * nrow;
-      const long long x = x0 + j;
-      const int al = (int)(x / n), a = (int)(x - (long long)al * n);
+      const int x = x0 + j;
+      const int al = x / n, a = x - al * n;
       tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
                                    : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
     }
@@ -302,7 +302,7 @@ __device__ void extend_side(const DevCtx& c, int job, int k, int side, int r, lo
     __syncthreads();
     for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
       const int s = e / nrow, j = e - s * nrow;
-      dst[(long long)s * sbn + x0 + j] = tile[s * TS + j];
+      dst[s * sbn + x0 + j] = tile[s * TS + j];
     }
     __syncthreads();
   }
@@ -344,7 +344,8 @@ __device__ __forceinline__ void warp_argmax(double& v, long long& f) {
 }
 
 struct GreedySmem {
-  Cand cand[2];                      // published CTA candidate (double-buffered per step)
+  Cand xc[2][16];                    // cluster exchange: candidate of CTA j in xc[step & 1][j]
+  unsigned long long xbar[2];        // mbarriers of the two exchange buffers
   Cand red[GREEDY_MAX_THREADS / 32];
   Cand best;                         // CTA argmax / cluster winner
   int xs[TTC_MAX_RANK_DEV];          // pivot rows
@@ -357,53 +358,6 @@ struct GreedySmem {
   DDE fp;                            // PB[beta][b] or PA[alpha][a]
   double pv;                         // E(x*, y*) of the final pivot (owner CTA of column y*)
 };
-
-// CTA-wide argmax of (v, f) -> S.best (all threads call)
-__device__ __forceinline__ void cta_argmax(GreedySmem& S, double v, long long f) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  warp_argmax(v, f);
-  if (lane == 0) S.red[warp] = {v, f};
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    double bv = lane < nw ? S.red[lane].val : -1.0;
-    long long bf = lane < nw ? S.red[lane].idx : LLONG_MAX;
-    warp_argmax(bv, bf);
-    if (lane == 0) S.best = {bv, bf};
-  }
-  __syncthreads();
-}
-
-// cluster-wide argmax: every CTA publishes S.best in cand[ph]; after the barrier every CTA
-// reduces all G candidates (DSMEM) in cluster-rank order -> S.best
-__device__ __forceinline__ void cluster_argmax(GreedySmem& S, cg::cluster_group& cl, int G, int& ph) {
-  if (G == 1) {
-    ph ^= 1;
-    return;
-  }
-  // only thread 0 publishes, so only it needs release semantics: fence, then a relaxed arrive
-  // by every thread and the (acquiring) wait
-  if (threadIdx.x == 0) {
-    S.cand[ph] = S.best;
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-  }
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double bv = -1.0;
-    long long bf = LLONG_MAX;
-    if (lane < G) {
-      const GreedySmem* R = cl.map_shared_rank(&S, lane);
-      bv = R->cand[ph].val;
-      bf = R->cand[ph].idx;
-    }
-    warp_argmax(bv, bf);
-    if (lane == 0) S.best = {bv, bf};
-  }
-  ph ^= 1;
-  __syncthreads();
-}
 
 // asynchronous global -> shared copies (LDGSTS): the whole cache fill is one round trip
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -425,7 +379,7 @@ struct StepCtx {
   const DevCtx* c;
   GreedySmem* S;
   int job, k, n, cap, r, rl, rr, tid, T;
-  long long xb, xe, yb, ye, sbn, rpcap, jo, jcx;
+  int xb, xe, yb, ye, sbn, rpcap, jo, jcx;  // intra-superblock indices: < 2^31 (n <= 4096, cap <= 64)
   double *U, *V, *Araw, *Uc, *Ecol, *Acol, *Vc, *Erow;
   ESum* SAc;
   DDE* PAc;
@@ -446,31 +400,32 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   const DevCtx& c = *X.c;
   GreedySmem& S = *X.S;
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
-  const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, xb = X.xb, xe = X.xe, rpcap = X.rpcap;
+  const int sbn = X.sbn, jo = X.jo, jcx = X.jcx, xb = X.xb, xe = X.xe, rpcap = X.rpcap;
   const int be = y / n, b = y - (y / n) * n;
   TRACE(10);
   if (tid < r) S.vec[tid] = X.V[tid * sbn + y];
   if (tid == 0 && FAMILY < 2) {
-    S.fs = c.SB[jo + (long long)be * n + b];
-    if (FAMILY == 1) S.fp = c.PB[jo + (long long)be * n + b];
+    S.fs = c.SB[jo + be * n + b];
+    if (FAMILY == 1) S.fp = c.PB[jo + be * n + b];
   }
   if (FAMILY == 1) {
     for (int al = tid; al < X.rl; al += T) {
-      DDE f = c.CX[jcx + (long long)al * cap + be];
-      dde_mul(f, c.QL1[jo + (long long)al * n + b]);
+      DDE f = c.CX[jcx + al * cap + be];
+      dde_mul(f, c.QL1[jo + al * n + b]);
       S.f_slot[al] = f;
     }
     if (X.stage_n)
-      for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + (long long)be * n + a];
+      for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + be * n + a];
   }
+  const double ub = X.uk1[b];
   __syncthreads();
   TRACE(11);
-  const double ub = X.uk1[b];
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jrow = 0;
-  for (long long x = xb + tid; x < xe; x += T, ++jrow) {
-    const int al = (int)(x / n), a = (int)(x - (long long)al * n);
+  #pragma unroll 1
+  for (int x = xb + tid; x < xe; x += T, ++jrow) {
+    const int al = x / n, a = x - al * n;
     const double ua = X.uk[a];
     double raw;
     if (FAMILY >= 2) {
@@ -489,7 +444,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       DDE p = CACHED ? X.PAc[x - xb] : c.PA[jo + x];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[al]);
-      dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + (long long)be * n + a]);
+      dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + be * n + a]);
       dde_mul_d(p, rho(ua, ub));
       raw = __ddiv_rn(dde_round(p), SS);
     }
@@ -523,7 +478,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   const DevCtx& c = *X.c;
   GreedySmem& S = *X.S;
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
-  const long long sbn = X.sbn, jo = X.jo, jcx = X.jcx, yb = X.yb, ye = X.ye, rpcap = X.rpcap;
+  const int sbn = X.sbn, jo = X.jo, jcx = X.jcx, yb = X.yb, ye = X.ye, rpcap = X.rpcap;
   const int al = x / n, a = x - (x / n) * n;
   TRACE(20);
   if (tid < r) S.vec[tid] = X.U[tid * sbn + x];
@@ -533,21 +488,22 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   }
   if (FAMILY == 1) {
     for (int be = tid; be < X.rr; be += T) {
-      DDE f = c.CX[jcx + (long long)al * cap + be];
-      dde_mul(f, c.QR0[jo + (long long)be * n + a]);
+      DDE f = c.CX[jcx + al * cap + be];
+      dde_mul(f, c.QR0[jo + be * n + a]);
       S.f_slot[be] = f;
     }
     if (X.stage_n)
-      for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + (long long)al * n + b];
+      for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + al * n + b];
   }
+  const double ua = X.uk[a];
   __syncthreads();
   TRACE(21);
-  const double ua = X.uk[a];
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jcol = 0;
-  for (long long y = yb + tid; y < ye; y += T, ++jcol) {
-    const int be = (int)(y / n), b = (int)(y - (long long)be * n);
+  #pragma unroll 1
+  for (int y = yb + tid; y < ye; y += T, ++jcol) {
+    const int be = y / n, b = y - be * n;
     const double ub = X.uk1[b];
     double e;
     if (FAMILY >= 2) {
@@ -566,7 +522,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       DDE p = CACHED ? X.PBc[y - yb] : c.PB[jo + y];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[be]);
-      dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + (long long)al * n + b]);
+      dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + al * n + b]);
       dde_mul_d(p, rho(ua, ub));
       e = __ddiv_rn(dde_round(p), SS);
     }
@@ -586,10 +542,32 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   bf_out = bf;
 }
 
+// cluster exchange of the per-CTA candidates without a cluster barrier: CTA j writes its
+// candidate into slot j of every CTA's xc[p] with st.async, which completes bytes on the
+// receiver's mbarrier xbar[p]; each CTA waits on its own barrier (expecting 16*G bytes) and
+// reduces the G slots in cluster-rank order.  p = step & 1 double-buffers the slots: a CTA can
+// send step s+2 only after every CTA has sent step s+1, i.e. finished reading step s.
+__device__ __forceinline__ void xbar_init(GreedySmem* S) {
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < 2; ++p) {
+      const unsigned a = (unsigned)__cvta_generic_to_shared(&S->xbar[p]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // (the caller's cluster barrier orders the init before any remote complete_tx)
+}
+
+__device__ __forceinline__ unsigned cluster_addr(const void* p, int cta) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
+  return r;
+}
+
 // CTA argmax + cluster argmax of (v, f) -> S->best, out of line (one copy of the shuffle
-// trees for all steps: the sweep kernel is instruction-cache bound).  ph alternates the
-// published candidate buffer between steps.
-__device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, int G, int ph) {
+// trees for all steps: the sweep kernel is instruction-cache bound).  xstep counts the
+// cluster exchanges of this launch (identical on every CTA of the cluster).
+__device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, int G, int xstep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   warp_argmax(v, f);
   if (lane == 0) S->red[warp] = {v, f};
@@ -599,33 +577,43 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
     const int nw = blockDim.x >> 5;
     double bv = lane < nw ? S->red[lane].val : -1.0;
     long long bf = lane < nw ? S->red[lane].idx : LLONG_MAX;
+    TRACE(35);
     warp_argmax(bv, bf);
-    if (lane == 0) {
-      S->best = {bv, bf};
-      if (G > 1) {
-        S->cand[ph] = {bv, bf};
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    TRACE(36);
+    if (G == 1) {
+      if (lane == 0) S->best = {bv, bf};
+    } else {
+      const int p = xstep & 1;
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&S->xbar[p]);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(16 * G) : "memory");
+      TRACE(37);
+      if (lane < G) {
+        const int me = (int)cg::this_cluster().block_rank();
+        const unsigned ra = cluster_addr(&S->xc[p][me], lane), rb = cluster_addr(&S->xbar[p], lane);
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                     "l"(__double_as_longlong(bv)), "l"(bf), "r"(rb)
+                     : "memory");
       }
+      TRACE(32);
+      const unsigned par = (unsigned)(xstep >> 1) & 1u;
+      unsigned ok = 0;
+      while (!ok)
+        asm volatile(
+            "{\n .reg .pred q;\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, q;\n}"
+            : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+      TRACE(33);
+      bv = -1.0;
+      bf = LLONG_MAX;
+      if (lane < G) {
+        bv = S->xc[p][lane].val;
+        bf = S->xc[p][lane].idx;
+      }
+      warp_argmax(bv, bf);
+      if (lane == 0) S->best = {bv, bf};
     }
-  }
-  if (G == 1) {
-    __syncthreads();
-    return;
-  }
-  TRACE(32);
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-  TRACE(33);
-  if (warp == 0) {
-    double bv = -1.0;
-    long long bf = LLONG_MAX;
-    if (lane < G) {
-      const Cand* rc = cg::this_cluster().map_shared_rank(&S->cand[ph], lane);
-      bv = rc->val;
-      bf = rc->idx;
-    }
-    warp_argmax(bv, bf);
-    if (lane == 0) S->best = {bv, bf};
   }
   __syncthreads();
   TRACE(34);
@@ -636,25 +624,26 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
 // new pivot (if any) is written to the record Rn (slot r and rank); returns the new rank.
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
-                                          int rl, int rr, int* Rn) {
+                                          int rl, int rr, int* Rn, int& xstep) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
   const int k = c.kb + job, d = c.d, n = c.n, cap = c.cap;
   const int tid = threadIdx.x, T = blockDim.x;
-  const long long R = (long long)rl * n, C = (long long)rr * n;
+  // intra-superblock indices are int: n <= 4096, cap <= 64 (tt_cross_init)
+  const int R = rl * n, C = rr * n;
   // rows / columns of this CTA (contiguous blocks); the cached variant's shared-memory
   // stride is the capacity block rpcap >= rpc, cpc
-  const long long rpc = (R + G - 1) / G, cpc = (C + G - 1) / G;
-  const long long rpcap = (c.sbn + G - 1) / G;
-  const long long xb = cr * rpc, xe = min(R, xb + rpc);
-  const long long yb = cr * cpc, ye = min(C, yb + cpc);
-  const long long sbn = c.sbn;
+  const int rpc = (R + G - 1) / G, cpc = (C + G - 1) / G;
+  const int rpcap = (int)((c.sbn + G - 1) / G);
+  const int xb = cr * rpc, xe = min(R, xb + rpc);
+  const int yb = cr * cpc, ye = min(C, yb + cpc);
+  const int sbn = (int)c.sbn;
   double* U = c.U + (long long)job * cap * sbn;
   double* V = c.V + (long long)job * cap * sbn;
   double* Araw = c.Araw + (long long)job * sbn;
-  const long long jo = (long long)job * cap * n;   // table offset of this job
-  const long long jcx = (long long)job * cap * cap;
+  const int jo = job * cap * n;   // table offset of this job
+  const int jcx = job * cap * cap;
   const double* uk = c.u + (long long)k * n;
   const double* uk1 = c.u + (long long)(k + 1) * n;
   // cached layout (rpcap rows / columns per CTA)
@@ -710,11 +699,11 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   }
   if (FAMILY == 1) {
     // CX for the new pairs: new alpha x all beta, then old alpha x new beta
-    const long long na = (long long)(rl - rows_done) * rr, nb = (long long)rows_done * (rr - cols_done);
-    for (long long e = (long long)cr * T + tid; e < na + nb; e += (long long)G * T) {
+    const int na = (rl - rows_done) * rr, nb = rows_done * (rr - cols_done);
+    for (int e = cr * T + tid; e < na + nb; e += G * T) {
       int al, be;
       if (e < na) { al = rows_done + (int)(e / rr); be = (int)(e % rr); }
-      else { const long long f = e - na; al = (int)(f / (rr - cols_done)); be = cols_done + (int)(f % (rr - cols_done)); }
+      else { const int f = e - na; al = f / (rr - cols_done); be = cols_done + f % (rr - cols_done); }
       sb_cx_table(c, job, al, be, rl, rr);
     }
   }
@@ -729,22 +718,22 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     __shared__ double pdiag[TTC_MAX_RANK_DEV];
     double* coef = dyn;
     double* tile = dyn + (long long)cap * cap;
-    const long long nr_new = (long long)(rl - rows_done) * n, nc_new = (long long)(rr - cols_done) * n;
+    const int nr_new = (rl - rows_done) * n, nc_new = (rr - cols_done) * n;
     // with G >= 2 the first half of the cluster extends the rows, the second half the columns
     // (independent: the column recurrence reads u only at old pivot rows, or A(t0) at the
     // first sweep), so the two latency chains overlap
     const int gr = G >= 2 ? G / 2 : 1, gc = G >= 2 ? G - gr : 1;
     const bool do_rows = G == 1 || cr < gr, do_cols = G == 1 || cr >= gr;
     const int rr_i = G == 1 ? 0 : cr, cc_i = G == 1 ? 0 : cr - gr;
-    const long long rchunk = (nr_new + gr - 1) / gr, cchunk = (nc_new + gc - 1) / gc;
+    const int rchunk = (nr_new + gr - 1) / gr, cchunk = (nc_new + gc - 1) / gc;
     if (do_rows) {   // rows: fixed index = pivot columns y_s
       if (tid < r) {
         p_al[tid] = S.ys[tid] / n;
         p_a[tid] = S.ys[tid] - (S.ys[tid] / n) * n;
       }
       __syncthreads();
-      const long long lo = (long long)rows_done * n + (long long)rr_i * rchunk;
-      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, (long long)rl * n), p_al, p_a, pdiag, coef, tile,
+      const int lo = rows_done * n + rr_i * rchunk;
+      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, coef, tile,
                           ext_ent, ext_upd);
       __syncthreads();
     }
@@ -752,11 +741,11 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       if (tid < r) {
         p_al[tid] = S.xs[tid] / n;
         p_a[tid] = S.xs[tid] - (S.xs[tid] / n) * n;
-        pdiag[tid] = first ? *c.p0val : U[(long long)tid * sbn + S.xs[tid]];
+        pdiag[tid] = first ? *c.p0val : U[tid * sbn + S.xs[tid]];
       }
       __syncthreads();
-      const long long lo = (long long)cols_done * n + (long long)cc_i * cchunk;
-      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, (long long)rr * n), p_al, p_a, pdiag, coef, tile,
+      const int lo = cols_done * n + cc_i * cchunk;
+      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, coef, tile,
                           ext_ent, ext_upd);
     }
   }
@@ -772,7 +761,6 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   if (scale < 0.0) scale = fabs(p0);
   unsigned long long evals = 0, upd = 0;
   int steps = 0;
-  int ph = 0;
   int xst = 0, yst = 0;
   bool added = false;
   double raw_star = 0.0;
@@ -781,14 +769,14 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   if (active) {
     if (CACHED) {
 #pragma unroll 1
-      for (long long e = tid; e < (long long)r * rpcap; e += T) {
-        const int t = (int)(e / rpcap);
-        const long long j = e - (long long)t * rpcap;
-        if (xb + j < xe) cp_async8(&Uc[t * rpcap + j], &U[t * sbn + xb + j]);
-        if (yb + j < ye) cp_async8(&Vc[t * rpcap + j], &V[t * sbn + yb + j]);
-      }
+      for (int t = 0; t < r; ++t)
 #pragma unroll 1
-      for (long long j = tid; j < rpcap; j += T) {
+        for (int j = tid; j < rpcap; j += T) {
+          if (xb + j < xe) cp_async8(&Uc[t * rpcap + j], &U[t * sbn + xb + j]);
+          if (yb + j < ye) cp_async8(&Vc[t * rpcap + j], &V[t * sbn + yb + j]);
+        }
+#pragma unroll 1
+      for (int j = tid; j < rpcap; j += T) {
         if (xb + j < xe) {
           const double* sa = reinterpret_cast<const double*>(&c.SA[jo + xb + j]);
           double* da = reinterpret_cast<double*>(&SAc[j]);
@@ -826,10 +814,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       double bv = -1.0;
       long long bf = LLONG_MAX;
       for (int q = tid; q < c.ns; q += T) {
-        const long long sx = (long long)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
-        const long long sy = (long long)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
-        const int al = (int)(sx / n), a = (int)(sx - (long long)al * n);
-        const int be = (int)(sy / n), b = (int)(sy - (long long)be * n);
+        const int sx = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
+        const int sy = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
+        const int al = sx / n, a = sx - al * n;
+        const int be = sy / n, b = sy - be * n;
         double e = sb_entry<FAMILY>(c, job, k, al, a, be, b);
         for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + sx], V[t * sbn + sy]));
         bool masked = false;
@@ -855,10 +843,17 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     //   f_node[a] = QR0[beta][a]
     // pivot rows / columns among this thread's first 64 rows / columns (a search beyond)
     unsigned long long rowmask = 0, colmask = 0;
-    for (int t = 0; t < r; ++t) {
-      const long long x = S.xs[t], y = S.ys[t];
-      if (x >= xb && x < xe && (x - xb) % T == tid && (x - xb) / T < 64) rowmask |= 1ULL << ((x - xb) / T);
-      if (y >= yb && y < ye && (y - yb) % T == tid && (y - yb) / T < 64) colmask |= 1ULL << ((y - yb) / T);
+#pragma unroll 1
+    for (int t = 0; t < r; ++t) {   // (32-bit: a superblock side has < 2^31 rows)
+      const int jx = S.xs[t] - (int)xb, jy = S.ys[t] - (int)yb;
+      if (jx >= 0 && jx < (int)(xe - xb)) {
+        const int q = jx / T;
+        if (jx - q * T == tid && q < 64) rowmask |= 1ULL << q;
+      }
+      if (jy >= 0 && jy < (int)(ye - yb)) {
+        const int q = jy / T;
+        if (jy - q * T == tid && q < 64) colmask |= 1ULL << q;
+      }
     }
     StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
               U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
@@ -870,19 +865,19 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       column_eval<FAMILY, CACHED>(X, y, bv, bf);
       const unsigned long long t1 = timer ? gtimer() : 0;
       if (tid == 0) {
-        evals += (unsigned long long)max(0LL, xe - xb);
-        upd += (unsigned long long)max(0LL, xe - xb) * r;
+        evals += (unsigned long long)max(0, xe - xb);
+        upd += (unsigned long long)max(0, xe - xb) * r;
       }
       if (!search) {
         __syncthreads();
         return -1;
       }
-      argmax_step(&S, bv, bf, G, ph);
+      argmax_step(&S, bv, bf, G, xstep);
       if (timer) {
         atomicAdd(&c.phase_ns[PH_COL_EVAL], t1 - t0);
         atomicAdd(&c.phase_ns[PH_COL_ARGMAX], gtimer() - t1);
       }
-      ph ^= 1;
+      ++xstep;
       return (int)S.best.idx;
     };
     auto row = [&](int x, bool search) -> int {
@@ -892,19 +887,19 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       row_eval<FAMILY, CACHED>(X, x, bv, bf);
       const unsigned long long t1 = timer ? gtimer() : 0;
       if (tid == 0) {
-        evals += (unsigned long long)max(0LL, ye - yb);
-        upd += (unsigned long long)max(0LL, ye - yb) * r;
+        evals += (unsigned long long)max(0, ye - yb);
+        upd += (unsigned long long)max(0, ye - yb) * r;
       }
       if (!search) {
         __syncthreads();
         return -1;
       }
-      argmax_step(&S, bv, bf, G, ph);
+      argmax_step(&S, bv, bf, G, xstep);
       if (timer) {
         atomicAdd(&c.phase_ns[PH_ROW_EVAL], t1 - t0);
         atomicAdd(&c.phase_ns[PH_ROW_ARGMAX], gtimer() - t1);
       }
-      ph ^= 1;
+      ++xstep;
       return (int)S.best.idx;
     };
     // ---- Alg. 2 lines 2-5: rook search
@@ -924,12 +919,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         stage = 1;
       } else {
         const bool search = !done;
-        if (!search) {
-          if (g_at != xst) row(xst, false);
-          break;
-        }
-        const int yn = row(xst, true);
+        if (!search && g_at == xst) break;
+        const int yn = row(xst, search);
         g_at = xst;
+        if (!search) break;
         steps += 1;
         const bool conv = (yn == yst);
         yst = yn;
@@ -942,12 +935,12 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
     }
     if (CACHED) {   // the final column / row leave the chip once
-      for (long long x = xb + tid; x < xe; x += T) {
+      for (int x = xb + tid; x < xe; x += T) {
         U[r * sbn + x] = Ecol[x - xb];
         Araw[x] = Acol[x - xb];
       }
 #pragma unroll 1
-      for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
+      for (int y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
     }
     // the pivot value E(x*, y*) is read from the shared memory of the CTA owning column y*,
     // not from V[r][y*]: that CTA rescales V[r][:] in place right after the barrier
@@ -962,7 +955,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (fabs(pv) > c.tol * scale) {
       added = true;
 #pragma unroll 1
-      for (long long y = yb + tid; y < ye; y += T) V[r * sbn + y] = __ddiv_rn(V[r * sbn + y], pv);
+      for (int y = yb + tid; y < ye; y += T) V[r * sbn + y] = __ddiv_rn(V[r * sbn + y], pv);
     }
   }
 
@@ -1032,10 +1025,12 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   int* Rn = c.rec_next + (long long)k * c.RS;
   const int* Rc = c.rec_cur + (long long)k * c.RS;
   TRACE_INIT();
+  xbar_init(&S);
   if (cl.block_rank() == 0)
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
-  __syncthreads();
-  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn);
+  cl.sync();  // record copy and exchange barriers ready
+  int xstep = 0;
+  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
     c.done[k] = sweep + 1;
@@ -1058,7 +1053,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   int* Rk = c.rec_cur + (long long)k * c.RS;
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
+  int xstep = 0;
   TRACE_INIT();
+  xbar_init(&S);  // ordered before remote use by the cluster barriers of the first sweep
   for (int s = s0; s < s0 + nsweeps; ++s) {
     TRACE_FLUSH();
     TRACE(49);
@@ -1089,7 +1086,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     if (s_any) break;
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
-    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk);
+    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
       c.rank_ring[k * 2 + (s & 1)] = r;
       st_release(&c.done[k], s + 1);  // the record writes above happen-before this release

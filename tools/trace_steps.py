@@ -2,7 +2,7 @@
 """Step trace of the persistent sweep kernel (diagnostics, not part of the product).
 
 Builds tools/libttcross_trace.so (the library with -DTTC_TRACE: thread 0 of every CTA appends
-(point, globaltimer) events at the phase and rook-step boundaries of ttc_greedy.cuh), runs one
+(point, clock64) events at the phase and rook-step boundaries of ttc_greedy.cuh), runs one
 solve of each named workload and prints, per superblock, where the time of a sweep goes:
   tables / extend / cache+samples / rook steps (staging, evaluation incl. the CTA reduce,
   cluster barrier wait, DSMEM reduce) / final / neighbour wait.
@@ -21,6 +21,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+MHZ = 1965.0   # SM clock under load on this pool's B200s (bench.py "clocks"): cycles -> us
 LIB = os.path.join(ROOT, "tools", "libttcross_trace.so")          # heavy: race detector
 LIB_LIGHT = os.path.join(ROOT, "tools", "libttcross_tracel.so")   # light: timing
 
@@ -41,7 +42,7 @@ def build(force=False, light=False):
 POINT = {1: "start", 2: "tables_done", 3: "tables_sync", 4: "extend_done", 5: "extend_sync", 6: "cache",
          7: "samples_eval", 8: "rook_done", 9: "final_sync", 10: "col_begin", 11: "col_staged",
          20: "row_begin", 21: "row_staged", 31: "cta_reduced", 32: "published", 33: "cluster_wait",
-         34: "step_end", 40: "end", 41: "end_sync", 49: "loop", 50: "nbr_waited", 51: "nbr_sync"}
+         34: "step_end", 35: "red_read", 36: "red_reduced", 37: "expect_tx", 40: "end", 41: "end_sync", 49: "loop", 50: "nbr_waited", 51: "nbr_sync"}
 
 
 def analyse(ev, cnt, G, njobs):
@@ -57,7 +58,7 @@ def analyse(ev, cnt, G, njobs):
             ts = (ev[b, :m] & np.uint64((1 << 56) - 1)).astype(np.int64)
             for i in range(1, m):
                 a, z = pts[i - 1], pts[i]
-                dt = (ts[i] - ts[i - 1]) / 1e3
+                dt = (ts[i] - ts[i - 1]) / MHZ
                 key = f"{POINT.get(a, a)}->{POINT.get(z, z)}"
                 acc[key] += dt / G
                 nst[key] += 1
@@ -102,9 +103,9 @@ def main():
             b = job * G
             m = min(int(cnt[b]), nev)
             ts = (ev[b, :m] & np.uint64((1 << 56) - 1)).astype(np.int64)
-            total[job] = round((ts[-1] - ts[0]) / 1e3, 1) if m else 0
+            total[job] = round((ts[-1] - ts[0]) / MHZ, 1) if m else 0
         print(json.dumps({"workload": name, "shape": shape, "events_cta0": int(cnt[0]), "span_us": total,
-                          "per_job_us": {j: dict(list(v.items())[:14]) for j, v in res.items() if j < 4}}),
+                          "per_job_us": {j: dict(list(v.items())[:24]) for j, v in res.items() if j < 4}}),
               flush=True)
         tt.close()
 
