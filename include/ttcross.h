@@ -220,12 +220,14 @@ int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64
 int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, int32_t* cached,
                               int64_t* smem_bytes);
 
-/* tt_cross_get_phase_times -- with timing enabled, k_sweep's first CTA of the first owned
- * superblock accumulates its phases (globaltimer): us_out[0..6] = microseconds spent in
- * [prologue, tables, u/v extension, samples, rook search, final column/row + append, exit
- * barrier], us_out[7] = launches measured, us_out[8..11] = [column evaluation, column argmax
- * (CTA + cluster), row evaluation, row argmax] summed over the search steps.  count >= 12.
- * Reset by tt_cross_set_timing(1). */
+/* tt_cross_get_phase_times -- with timing enabled, k_sweep's first CTA of one owned
+ * superblock (the first, or the one environment variable TTC_PHASE_JOB names when the context
+ * is created) accumulates its phases (globaltimer): us_out[0..6] = microseconds spent in
+ * [neighbour wait of the persistent kernel, tables, u/v extension, samples, rook search, final
+ * column/row + append, exit barrier], us_out[7] = sweeps measured, us_out[8..11] = [column
+ * evaluation, column argmax (CTA + cluster), row evaluation, row argmax] summed over the search
+ * steps, us_out[12..13] = [raw entries, recurrence] of the extension's row tiles (written when
+ * count >= 14).  count >= 12.  Reset by tt_cross_set_timing(1). */
 int tt_cross_get_phase_times(ttc_ctx* ctx, double* us_out, int32_t count);
 
 /* tt_cross_set_timing -- 1: bracket every kernel launch with CUDA events on the context

@@ -259,12 +259,13 @@ class TTCross:
 
 
     def phase_times(self):
-        """k_sweep phase clocks (us, first superblock's CTA 0) accumulated while timing is on."""
-        out = np.zeros(12)
-        _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), 12),
+        """k_sweep phase clocks (us, CTA 0 of superblock TTC_PHASE_JOB, default the first) accumulated
+        while timing is on."""
+        out = np.zeros(14)
+        _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), 14),
                "tt_cross_get_phase_times")
         names = ["prologue", "tables", "extend", "samples", "rook", "final", "exit", "launches",
-                 "col_eval", "col_argmax", "row_eval", "row_argmax"]
+                 "col_eval", "col_argmax", "row_eval", "row_argmax", "ext_raw", "ext_rec"]
         return dict(zip(names, out.tolist()))
 
     def launch_shape(self):

@@ -540,7 +540,6 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.ke = c->ke;
   dc.RS = 1 + cap * d + 2 * cap;
   dc.sbn = (long long)cap * n;
-  dc.ext_tile = extend_tile_rows(cap);
   dc.G = 1;  // cluster size of k_sweep, chosen below once the device is known
   c->slots = d;
   c->nrec = k.world * c->chunk;
@@ -651,6 +650,10 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       const int t = std::atoi(e);
       if (t == 256 || t == 512) { T = t; G = std::max(1, pick_g(t == 512 ? sms : 2LL * sms)); }
     }
+    if (const char* e = std::getenv("TTC_PHASE_JOB")) {   // profiling: superblock of the phase clocks
+      const int j = std::atoi(e);
+      dc.phase_job = (j >= 0 && j < nj) ? j : 0;
+    }
     if (const char* e = std::getenv("TTC_GREEDY_G")) {
       const int g = std::atoi(e);
       if (g >= 1 && g <= 16 && (g & (g - 1)) == 0) G = g;
@@ -661,8 +664,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     };
     const size_t ext_bytes = (size_t)extend_smem_doubles(cap) * sizeof(double);
     const size_t smem_lim = 180 * 1024;
+    // the non-cached variant also holds the rook steps' DotRing (at least 4 terms per stage)
     auto smem_for = [&](int g, bool cached) -> size_t {
-      return std::max(ext_bytes, cached ? cache_for(g) : (size_t)0);
+      return std::max(ext_bytes, cached ? cache_for(g) : (size_t)RING_P * 4 * T * sizeof(double));
     };
     // T = threads per CTA; kernels are compiled for 256 (two CTAs per SM) and 512 (one)
     auto fn_for = [&](bool cached) -> const void* {
@@ -722,6 +726,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     c->greedy_threads = T;
     c->greedy_cached = cached;
     c->greedy_smem = smem_for(G, cached);
+    dc.ring_tb = (int)std::min<size_t>(8, c->greedy_smem / (sizeof(double) * RING_P * T));
+    dc.ext_tile = extend_tile_rows(cap);
     c->greedy_fn = fn_for(c->greedy_cached);
     {
       const bool big = T > 256;
@@ -969,11 +975,11 @@ int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
 
 int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
   if (!c || !us_out) return fail(TTC_ERR_ARG, "null argument");
-  if (count < TTC_NPHASES) return fail(TTC_ERR_ARG, "need 12 slots");
+  if (count < 12) return fail(TTC_ERR_ARG, "need 12 slots");
   unsigned long long v[TTC_NPHASES] = {};
   CK(cudaMemcpyAsync(v, c->phase_buf, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (int i = 0; i < TTC_NPHASES; ++i) us_out[i] = i == PH_LAUNCHES ? (double)v[i] : v[i] * 1e-3;
+  for (int i = 0; i < TTC_NPHASES && i < count; ++i) us_out[i] = i == PH_LAUNCHES ? (double)v[i] : v[i] * 1e-3;
   return TTC_OK;
 }
 

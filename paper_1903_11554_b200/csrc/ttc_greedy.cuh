@@ -249,7 +249,7 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // -- per s the same operations in the same order as the oracle's row-oriented
 // u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s) (t ascending), hence the same bits.
 // Columns: v_t = acc_t / u_t(x_t) final; acc_s -= U[t][x_s] * v_t.
-// Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][c.ext_tile + 1].
+// Rows [x_lo, x_hi) of this CTA; coef = [t][s] (stride cap), tile = [s][TS], TS <= c.ext_tile + 1.
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
@@ -272,37 +272,99 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
     }
     coef[t * cap + s] = v;
   }
-  const int tile_rows = c.ext_tile, TS = c.ext_tile + 1;
+  // rows per tile, tile stride and lanes per row of the recurrence (host: extend_tile_shape)
+  const int tile_rows = c.ext_tile;
   double* dst = side == 0 ? U : V;
-  for (int x0 = x_lo; x0 < x_hi; x0 += tile_rows) {
-    const int nrow = min(tile_rows, x_hi - x0);
-    // (1) raw entries of the tile, one per thread
-    for (int e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-      const int s = e / nrow, j = e - s * nrow;
-      const int x = x0 + j;
-      const int al = x / n, a = x - al * n;
-      tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
-                                   : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+  const bool timer = c.phase_ns && job == c.phase_job && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0;
+  unsigned long long tm = timer ? gtimer() : 0;
+  auto clock_to = [&](int ph) {
+    if (timer) {
+      const unsigned long long t = gtimer();
+      atomicAdd(&c.phase_ns[ph], t - tm);
+      tm = t;
+    }
+  };
+  int nrow;
+  for (int x0 = x_lo; x0 < x_hi; x0 += nrow) {
+    // tile shape: nrow rows, L recurrence lanes per row (as many as the rows leave threads
+    // for, <= 8), stride TS <= tile_rows + 1.  L adjacent lanes work on L different s of one
+    // row: TS = 8 (L = 4) or 4 (L = 8) mod 16 doubles spreads a warp's 32 accesses evenly over
+    // the banks (L <= 2: any stride does); a full tile shrinks to such a stride when needed.
+    nrow = min(tile_rows, x_hi - x0);
+    int L = 1;
+    while (L < 8 && 2 * L * nrow <= (int)blockDim.x) L *= 2;
+    int TS = nrow + 1;
+    if (L >= 4) {
+      const int res = L == 4 ? 8 : 4;
+      TS = ((nrow + 15 - res) & ~15) + res;   // smallest >= nrow with TS = res mod 16
+      if (TS > tile_rows + 1) {
+        TS = ((tile_rows + 1 - res) & ~15) + res;   // largest <= capacity
+        if (TS >= 16) nrow = TS;
+        else TS = nrow + 1;
+      }
+    }
+    // (1) raw entries of the tile, one per thread, two per iteration: the two independent
+    // latency chains (table loads, double-double products, division) overlap
+    {
+      auto raw_entry = [&](int e) {
+        const int s = e / nrow, j = e - s * nrow;
+        const int x = x0 + j;
+        const int al = x / n, a = x - al * n;
+        tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                                     : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+      };
+      const int ne = nrow * r, B = blockDim.x;
+      int e = threadIdx.x;
+#pragma unroll 1
+      for (; e + B < ne; e += 2 * B) {
+        const int e1 = e + B;
+        const int s0 = e / nrow, j0 = e - s0 * nrow, s1 = e1 / nrow, j1 = e1 - s1 * nrow;
+        const int x0a = x0 + j0, x1a = x0 + j1;
+        const int al0 = x0a / n, a0 = x0a - al0 * n, al1 = x1a / n, a1 = x1a - al1 * n;
+        double v0, v1;
+        if (side == 0) {
+          v0 = sb_entry<FAMILY>(c, job, k, al0, a0, p_al[s0], p_a[s0]);
+          v1 = sb_entry<FAMILY>(c, job, k, al1, a1, p_al[s1], p_a[s1]);
+        } else {
+          v0 = sb_entry<FAMILY>(c, job, k, p_al[s0], p_a[s0], al0, a0);
+          v1 = sb_entry<FAMILY>(c, job, k, p_al[s1], p_a[s1], al1, a1);
+        }
+        tile[s0 * TS + j0] = v0;
+        tile[s1 * TS + j1] = v1;
+      }
+      if (e < ne) raw_entry(e);
     }
     __syncthreads();
-    // (2) the recurrence, a thread per row, column-oriented (t outer, s > t inner): for every
-    // s the same subtractions in the same t order as the oracle's row-oriented sum.  (A warp
-    // per row with lanes over s measured slower at r = 16 and at r = 64.)
-    for (int j = threadIdx.x; j < nrow; j += blockDim.x) {
-      for (int t = 0; t < r; ++t) {
-        double f = tile[t * TS + j];
-        if (side == 1) {
-          f = __ddiv_rn(f, pdiag[t]);  // v_t final
-          tile[t * TS + j] = f;
+    clock_to(PH_EXT_RAW);
+    // (2) the recurrence, L adjacent lanes per row (L = 1, 2, 4, 8: as many as the tile's rows
+    // leave threads for), column-oriented (t outer, s > t inner), lane l updating s = l mod L:
+    // for every s the same subtractions in the same t order as the oracle's row-oriented sum.
+    // Columns divide by u_t(x_t) on the fly (every lane computes the same v_t bits); the final
+    // v_t = tile / u_t(x_t) is formed again in the store below.  (A warp per row with lanes
+    // over s measured slower at r = 16 and at r = 64.)
+    {
+      const int ln = threadIdx.x & (L - 1), lane = threadIdx.x & 31;
+      const unsigned gmask = (L == 32 ? 0xffffffffu : ((1u << L) - 1u)) << (lane & ~(L - 1));
+#pragma unroll 1
+      for (int j = threadIdx.x / L; j < nrow; j += blockDim.x / L) {
+#pragma unroll 1
+        for (int t = 0; t < r; ++t) {
+          if (L > 1) __syncwarp(gmask);   // tile[t][j] final (updated at step t-1 by lane t mod L)
+          double f = tile[t * TS + j];
+          if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t
+          const int q0 = t + 1 + ((ln - (t + 1)) & (L - 1));
+          for (int q = q0; q < r; q += L)
+            tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
         }
-        for (int q = t + 1; q < r; ++q)
-          tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
+        if (L > 1) __syncwarp(gmask);
       }
     }
     __syncthreads();
+    clock_to(PH_EXT_REC);
     for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
       const int s = e / nrow, j = e - s * nrow;
-      dst[s * sbn + x0 + j] = tile[s * TS + j];
+      const double f = tile[s * TS + j];
+      dst[s * sbn + x0 + j] = side == 1 ? __ddiv_rn(f, pdiag[s]) : f;
     }
     __syncthreads();
   }
@@ -365,6 +427,63 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Per-thread staging ring of the non-cached rook steps.  A column step needs, for each of the
+// thread's rows x, the r factors F[t][x] = U[t][x] (a row step: V[t][y]) -- an HBM stream of
+// r*8 bytes per row (D_20: 2 MB per CTA per step).  Loading them with plain loads leaves one
+// unrolled batch (8 loads) in flight per thread and the step latency-bound; here each thread
+// streams its own factors through shared memory with cp.async in RING_P stages of `tb` terms,
+// RING_P - 1 stages ahead of the chain, so ~ (RING_P - 1) * tb loads per thread are in flight.
+// A thread reads back only what it copied itself: no block barrier, only cp.async.wait_group.
+// Layout: buf[stage][i][T] (conflict-free per warp).  Stage s = (row j, term block b), row-major.
+#define RING_P 4
+struct DotRing {
+  double* buf;
+  const double* F;
+  int T, tid, tb, nb, sbn, r;
+  int z0, total;          // first row of the thread, stages in all
+  int is, irow, iblk;     // next stage to issue
+  int cs;                 // next stage to consume
+  __device__ __forceinline__ void init(double* b, const double* f, int T_, int tid_, int tb_, int sbn_, int r_, int zb,
+                                       int ze) {
+    buf = b; F = f; T = T_; tid = tid_; tb = tb_; sbn = sbn_; r = r_;
+    nb = (r + tb - 1) / tb;
+    z0 = zb + tid;
+    const int rows = z0 < ze ? (ze - z0 + T - 1) / T : 0;
+    total = rows * nb;
+    is = irow = iblk = cs = 0;
+#pragma unroll 1
+    for (int q = 0; q < RING_P - 1; ++q) issue();
+  }
+  __device__ __forceinline__ void issue() {
+    if (is < total) {
+      double* dst = buf + (is & (RING_P - 1)) * tb * T + tid;
+      const int t0 = iblk * tb, tn = min(tb, r - t0);
+      const double* src = F + t0 * sbn + z0 + irow * T;
+#pragma unroll 1
+      for (int i = 0; i < tn; ++i) cp_async8(dst + i * T, src + i * sbn);
+      if (++iblk == nb) { iblk = 0; ++irow; }
+    }
+    ++is;
+    cp_async_commit();   // (empty groups keep the wait count uniform)
+  }
+  // e -= F[t][row] * vec[t], t = 0 .. r-1 in order, for the thread's next row
+  __device__ __forceinline__ double dot_sub(double e, const double* vec) {
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      issue();
+      cp_async_wait_group<RING_P - 1>();
+      const double* src = buf + (cs & (RING_P - 1)) * tb * T + tid;
+      const int t0 = b * tb, tn = min(tb, r - t0);
+      for (int i = 0; i < tn; ++i) e = __dsub_rn(e, __dmul_rn(src[i * T], vec[t0 + i]));
+      ++cs;
+    }
+    return e;
+  }
+};
 
 // dynamic shared memory of the CACHED variant (phase 3): own rows' U[t][x], SA, PA and own
 // columns' V[t][y], SB, PB stay on chip for the whole rook search, plus the E / raw values of
@@ -389,6 +508,8 @@ struct StepCtx {
   bool stage_n;
   unsigned long long rowmask, colmask;  // bit j: this thread's j-th row / column is a pivot's
   bool timer;                           // phase clock owner (tt_cross_get_phase_times)
+  double* ring;                         // non-cached: DotRing buffer (dyn, RING_P * ring_tb * T doubles)
+  int ring_tb;                          // terms per ring stage
 };
 
 // column step E(:, y) on this CTA's rows -> U[r][:] (or the row cache), raw values; returns
@@ -423,6 +544,8 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jrow = 0;
+  DotRing ring;
+  if (!CACHED) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
   #pragma unroll 1
   for (int x = xb + tid; x < xe; x += T, ++jrow) {
     const int al = x / n, a = x - al * n;
@@ -452,7 +575,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.Uc[t * rpcap + (x - xb)], S.vec[t]));
     else
-      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.U[t * sbn + x], S.vec[t]));
+      e = ring.dot_sub(e, S.vec);
     bool piv = jrow < 64 && ((X.rowmask >> jrow) & 1ULL);   // a pivot row (E is exactly 0 there)
     if (jrow >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.xs[t] == x);
@@ -501,6 +624,8 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jcol = 0;
+  DotRing ring;
+  if (!CACHED) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
   #pragma unroll 1
   for (int y = yb + tid; y < ye; y += T, ++jcol) {
     const int be = y / n, b = y - be * n;
@@ -529,7 +654,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));
     else
-      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.V[t * sbn + y]));
+      e = ring.dot_sub(e, S.vec);   // (S.vec[t] * V[t][y]: the product commutes bitwise)
     bool piv = jcol < 64 && ((X.colmask >> jcol) & 1ULL);   // a pivot column
     if (jcol >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.ys[t] == y);
@@ -657,7 +782,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   ESum* SBc = reinterpret_cast<ESum*>(Erow + rpcap);  // [rpcap]
   DDE* PBc = reinterpret_cast<DDE*>(SBc + rpcap);     // [rpcap]
 
-  const bool timer = c.phase_ns && job == 0 && cr == 0 && tid == 0;
+  const bool timer = c.phase_ns && job == c.phase_job && cr == 0 && tid == 0;
   unsigned long long t_last = timer ? gtimer() : 0;
   auto phase = [&](int ph) {
     if (timer) {
@@ -857,7 +982,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     }
     StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
               U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
-              timer};
+              timer, dyn, c.ring_tb};
     auto column = [&](int y, bool search) -> int {
       double bv;
       long long bf;
@@ -1065,6 +1190,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     if (threadIdx.x == 0) {
       int abort = 0;
       const long long t0 = clock64();
+      const unsigned long long w0 = c.phase_ns ? gtimer() : 0;
       if (k > 0)
         while (ld_acquire(&c.done[k - 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
         }
@@ -1073,6 +1199,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         }
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort = abort;
+      if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) atomicAdd(&c.phase_ns[PH_START], gtimer() - w0);
     }
     TRACE(50);
     cl.sync();

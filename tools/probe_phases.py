@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Per-phase device time of k_sweep (globaltimer, first superblock's CTA 0) for workloads.
+"""Per-phase device time of k_sweep (globaltimer, CTA 0 of one superblock: the middle one
+unless TTC_PHASE_JOB is set; "prologue" = the neighbour wait of the persistent kernel).
 Usage (GPU): python tools/probe_phases.py D5 C10 ..."""
 import json
 import os
@@ -15,6 +16,8 @@ from workloads import WORKLOADS  # noqa: E402
 
 for name in sys.argv[1:] or ["D5"]:
     wl = WORKLOADS[name]
+    job = int(os.environ.get("TTC_PHASE_JOB", (wl.d - 1) // 2))
+    os.environ["TTC_PHASE_JOB"] = str(job)
     u, w = wl.grid()
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
@@ -31,6 +34,7 @@ for name in sys.argv[1:] or ["D5"]:
     tt.set_timing(False)
     nl = max(1.0, ph.pop("launches"))
     per = {k: round(v / nl, 2) for k, v in ph.items()}
-    print(json.dumps({"workload": name, "shape": tt.launch_shape(), "k_sweep_us": kt["k_sweep"][1] * 1e3 / kt["k_sweep"][0],
+    print(json.dumps({"workload": name, "job": job, "shape": tt.launch_shape(), "k_sweep_us": kt["k_sweep"][1] * 1e3 / kt["k_sweep"][0],
                       "phase_us_per_launch": per, "rook_steps": tt.stats()["rook_steps"]}), flush=True)
     tt.close()
+    os.environ.pop("TTC_PHASE_JOB")
