@@ -136,20 +136,25 @@ def flops_per_entry(family, m):
 
 
 def fiber_roofline(kt, stats, family, modes, peaks):
-    """The quadrature fiber kernel (k_fiber / k_fiber_x): the throughput-mode batched
-    integrand evaluation.  t-form: C 4 flop/entry, D 26 (exact-limb sum and rounding 3, two
-    double-double products 20, rounding and division 3); x-form: flops_per_entry."""
+    """The quadrature fiber kernel: the throughput-mode batched integrand evaluation.
+    t-form (k_fiber_wsum, fused with the weighted sum, nothing written per entry): C 4 flop
+    per entry, D 26 (exact-limb sum and rounding 3, two double-double products 20, rounding
+    and division 3), plus 23 for the double-double accumulation of w_a * A (product 1, its
+    error 2, double-double add 20); x-form (k_fiber_x, 8 B written per entry):
+    flops_per_entry."""
     launches, ms = kt.get("k_fiber", (0, 0.0))
     if not launches or ms <= 0:
         return None
     avg_s = ms / launches / 1e3
     ent = stats["fiber_entries"] / launches
-    fpe = {0: 4, 1: 26}.get(family) or flops_per_entry(family, modes)
+    fused = family in (0, 1)
+    fpe = {0: 4 + 23, 1: 26 + 23}[family] if fused else flops_per_entry(family, modes)
     tf = ent * fpe / avg_s / 1e12
-    gbs = ent * 8 / avg_s / 1e9
-    return {"kernel": "k_fiber", "avg_us": avg_s * 1e6, "entries_per_launch": ent,
+    gbs = 0.0 if fused else ent * 8 / avg_s / 1e9
+    return {"kernel": "k_fiber_wsum" if fused else "k_fiber_x", "avg_us": avg_s * 1e6, "entries_per_launch": ent,
             "achieved_tflops": tf, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
-            "write_GBs": gbs, "frac_hbm": gbs / peaks["hbm_gbs"], "per_unit": f"{fpe} flop + 8 B written / entry"}
+            "write_GBs": gbs, "frac_hbm": gbs / peaks["hbm_gbs"],
+            "per_unit": f"{fpe} flop / entry" + ("" if fused else " + 8 B written")}
 
 
 def roofline(kt, stats, family, peaks, peak_src, modes=0):

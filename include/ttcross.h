@@ -198,8 +198,10 @@ int tt_integrate_finish(ttc_ctx* ctx, double* value, double* log10_abs, int32_t*
  * State inspection (synchronise the stream).
  *   tt_cross_get_state : ranks_out[d-1]; piv_out[(d-1)*rank_cap*d] (slots >= r_k are -1);
  *                        par_out[(d-1)*rank_cap*2] (may be NULL)
- *   tt_cross_get_fiber : fiber of mode m from the last quadrature pass,
- *                        out[rx*ry*n] as [alpha][beta][a]; capacity in doubles.
+ *   tt_cross_get_fiber : fiber A(I_{<=m-1}, i_m, I_{>m}) of mode m of the current cross,
+ *                        evaluated on demand (the same entries the quadrature contracts),
+ *                        out[rx*ry*n] as [alpha][beta][a]; capacity in doubles; out NULL:
+ *                        only rx, ry.  TTC_ERR_STATE while a local sweep is uncommitted.
  *   tt_cross_get_stats : counters and (if enabled) device times.
  */
 int tt_cross_get_state(ttc_ctx* ctx, int32_t* ranks_out, int32_t* piv_out, int32_t* par_out);

@@ -147,9 +147,13 @@ int check_launch(const char* what) {
 }
 
 // ------------------------------------------------------------------ launch sequences
-// quadrature fibers: frozen parts + entries for modes [jbase, jbase+njobs)
-int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
-  DevCtx& dc = c->dc;
+// quadrature fibers: frozen parts + entries for modes [jbase, jbase+njobs).  fused (t-form
+// families only): the entries are not stored, k_fiber_wsum contracts them with the weights
+// into W directly (the product path of tt_integrate); otherwise k_fiber writes dc.fib
+// (tt_cross_get_fiber) and the caller runs k_wsum.
+int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false, bool count = true) {
+  DevCtx dc = c->dc;
+  if (!count) dc.counters = nullptr;   // (tt_cross_get_fiber: not part of the method's work)
   const int n = dc.n, tup = dc.cap;
   if (dc.family >= 2) {
     const int gx = std::min(4096, (tup * n + 255) / 256);
@@ -177,6 +181,15 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs) {
       k_frozen_lr<<<dim3((tup + 63) / 64, tup, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_lr")) return e;
+  }
+  if (fused) {
+    {
+      Timed t(c, K_FIBER);
+      const dim3 g((tup + 7) / 8, tup, njobs);
+      if (dc.family == TTC_FAMILY_C) k_fiber_wsum<0><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+      else k_fiber_wsum<1><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+    }
+    return check_launch("k_fiber_wsum");
   }
   {
     Timed t(c, K_FIBER);
@@ -275,12 +288,15 @@ int do_integrate_local(ttc_ctx* c) {
   if (rank == 0) m_lo = 0;
   const int nm = (c->n_owned > 0) ? (m_hi - m_lo + 1) : (rank == 0 ? 1 : 0);
   if (nm > 0) {
-    if (int e = launch_fibers(c, JOB_INT, m_lo, nm)) return e;
-    {
-      Timed t(c, K_WSUM);
-      k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->ls>>>(dc, m_lo);
+    const bool fused = dc.family < TTC_FAMILY_CX;
+    if (int e = launch_fibers(c, JOB_INT, m_lo, nm, fused)) return e;
+    if (!fused) {
+      {
+        Timed t(c, K_WSUM);
+        k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->ls>>>(dc, m_lo);
+      }
+      if (int e = check_launch("k_wsum")) return e;
     }
-    if (int e = check_launch("k_wsum")) return e;
   }
   CK(cudaMemsetAsync(dc.flags, 0, sizeof(int), c->ls));  // flags[1] (sweep timeout) stays
   if (c->n_owned > 0) {
@@ -291,7 +307,9 @@ int do_integrate_local(ttc_ctx* c) {
     if (int e = check_launch("k_intersection")) return e;
     {
       Timed t(c, K_SOLVE);
-      k_solve<<<c->n_owned, 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc);
+      // split the right-hand sides over 4 CTAs when the interfaces leave SMs idle
+      const int split = (cap >= 32 && 4 * c->n_owned <= c->sms) ? 4 : 1;
+      k_solve<<<dim3(c->n_owned, split), 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc);
     }
     if (int e = check_launch("k_solve")) return e;
   }
@@ -301,6 +319,13 @@ int do_integrate_local(ttc_ctx* c) {
   if (items == 0) {  // a rank without superblocks contributes an empty record
     CK(cudaMemsetAsync(rec, 0, 3 * sizeof(double), c->ls));
     return TTC_OK;
+  }
+  if (with_head && c->n_owned <= CHAIN_VEC_MAX) {   // rank 0: a vector chain (see k_chain_vec)
+    {
+      Timed t(c, K_CHAIN);
+      k_chain_vec<<<1, 256, 0, c->ls>>>(dc, c->kb, c->kb + c->n_owned, rec);
+    }
+    return check_launch("k_chain_vec");
   }
   {
     Timed t(c, K_CHAIN);
@@ -916,6 +941,10 @@ int tt_cross_get_fiber(ttc_ctx* c, int32_t mode, double* out, int64_t capacity, 
   const long long cnt = (long long)a * b * n;
   if (out) {
     if (capacity < cnt) return fail(TTC_ERR_ARG, "fiber buffer too small");
+    if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+    // evaluated on demand from the current index sets (the quadrature pass contracts the
+    // t-form fibers without storing them)
+    if (int e = launch_fibers(c, JOB_INT, mode, 1, false, false)) return e;
     CK(cudaMemcpyAsync(out, c->dc.fib + (long long)mode * c->dc.fib_stride, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }

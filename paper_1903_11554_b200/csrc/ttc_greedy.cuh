@@ -440,6 +440,7 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 // A thread reads back only what it copied itself: no block barrier, only cp.async.wait_group.
 // Layout: buf[stage][i][T] (conflict-free per warp).  Stage s = (row j, term block b), row-major.
 #define RING_P 4
+#define RING_MIN_ROWS 4   // rows per thread from which a step streams through the ring
 struct DotRing {
   double* buf;
   const double* F;
@@ -545,7 +546,8 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   long long bf = LLONG_MAX;
   int jrow = 0;
   DotRing ring;
-  if (!CACHED) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
+  const bool use_ring = !CACHED && xe - xb >= RING_MIN_ROWS * T;
+  if (use_ring) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
   #pragma unroll 1
   for (int x = xb + tid; x < xe; x += T, ++jrow) {
     const int al = x / n, a = x - al * n;
@@ -574,8 +576,10 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
     double e = raw;
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.Uc[t * rpcap + (x - xb)], S.vec[t]));
-    else
+    else if (use_ring)
       e = ring.dot_sub(e, S.vec);
+    else
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.U[t * sbn + x], S.vec[t]));
     bool piv = jrow < 64 && ((X.rowmask >> jrow) & 1ULL);   // a pivot row (E is exactly 0 there)
     if (jrow >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.xs[t] == x);
@@ -625,7 +629,8 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   long long bf = LLONG_MAX;
   int jcol = 0;
   DotRing ring;
-  if (!CACHED) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
+  const bool use_ring = !CACHED && ye - yb >= RING_MIN_ROWS * T;
+  if (use_ring) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
   #pragma unroll 1
   for (int y = yb + tid; y < ye; y += T, ++jcol) {
     const int be = y / n, b = y - be * n;
@@ -653,8 +658,10 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
     }
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));
-    else
+    else if (use_ring)
       e = ring.dot_sub(e, S.vec);   // (S.vec[t] * V[t][y]: the product commutes bitwise)
+    else
+      for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.V[t * sbn + y]));
     bool piv = jcol < 64 && ((X.colmask >> jcol) & 1ULL);   // a pivot column
     if (jcol >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.ys[t] == y);

@@ -199,6 +199,62 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
   }
 }
 
+// Fused quadrature fibers + weighted sums (t-form families), the product path of
+// tt_integrate: W_m[alpha][beta] = sum_a w_{m,a} A(X_alpha, a, Y_beta) with the entries
+// evaluated on the fly -- a warp per fiber (alpha, beta), lanes over the nodes a, no fiber
+// written to memory.  The entry arithmetic is k_fiber's and the accumulation is k_wsum's
+// (lane-strided double-double sums, then the xor tree), so W is bit-identical to the
+// unfused k_fiber -> k_wsum pair.  grid: x = chunk of 8 betas (one per warp), y = alpha,
+// z = mode (jbase + z); block 256.
+template <int FAMILY>
+__global__ void __launch_bounds__(256) k_fiber_wsum(DevCtx c, int kind, int jbase) {
+  const int j = jbase + blockIdx.z, al = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int be = blockIdx.x * (blockDim.x >> 5) + warp;
+  Job jb = make_job(c, kind, j);   // (entries counted by k_frozen_sides)
+  if (al >= jb.rx || be >= jb.ry) return;
+  const int n = c.n, m = jb.m;
+  const long long base = (long long)j * c.cap;
+  ESum s0 = c.sl[base + al];
+  esum_add(s0, c.sr[base + be]);
+  DDE p0;
+  const DDE* ql = nullptr;
+  const DDE* qr = nullptr;
+  if (FAMILY == 1) {
+    p0 = c.pf[(base + al) * c.cap + be];
+    ql = c.ql + (base + al) * n;
+    qr = c.qr + (base + be) * n;
+  }
+  const long long* chi = c.chi + (long long)m * n;
+  const long long* clo = c.clo + (long long)m * n;
+  const double* w = c.w + (long long)m * n;
+  DD acc = dd_make(0.0);
+#pragma unroll 2
+  for (int a = lane; a < n; a += 32) {
+    ESum s = s0;
+    esum_add(s, chi[a], clo[a]);
+    const double S = esum_round(s);
+    const double SS = __dmul_rn(S, S);
+    double v;
+    if (FAMILY == 0) {
+      v = __drcp_rn(SS);
+    } else {
+      DDE p = p0;
+      dde_mul(p, ql[a]);
+      dde_mul(p, qr[a]);
+      v = __ddiv_rn(dde_round(p), SS);
+    }
+    const double wa = w[a];
+    const double pr = wa * v;
+    acc = dd_add(acc, DD{pr, fma(wa, v, -pr)});
+  }
+  for (int o = 16; o; o >>= 1) {
+    DD other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+    acc = dd_add(acc, other);
+  }
+  if (lane == 0) c.W[((long long)j * c.cap + al) * c.cap + be] = acc;
+}
+
 // quadrature fibers of the x-form families: direct evaluation of every entry (the x-form
 // integrand is not a function of per-mode node values, so the frozen-part factorisation
 // of the t-form does not apply); grid x = flat (beta*n + a) chunks, y = alpha, z = job
@@ -286,87 +342,101 @@ __global__ void k_wsum(DevCtx c, int mode_base) {
   if (lane == 0) c.W[((long long)m * c.cap + al) * c.cap + be] = acc;
 }
 
-// H_i = M_i^{-1} W_{i+1}: LU with partial pivoting in double-double (shared memory),
-// one CTA per owned interface.  Per elimination step: warp-0 argmax of |A[row][k].hi| (first
-// index on ties), row swap, multipliers l[row] = A[row][k] / A[k][k] once per row, then the
-// rank-1 update of the trailing block of [A | B] by all threads; back substitution is
-// column-oriented (x_k = B[k] / A[k][k], then B[q] -= A[q][k] x_k for q < k).
+// H_i = M_i^{-1} W_{i+1}: LU with partial pivoting in double-double on [M_i | W_{i+1}] in
+// shared memory, one CTA per owned interface.  Rows are permuted through an index array (no
+// row swaps).  Elimination step k: warp 0 picks the pivot (first maximiser of |A[row][k].hi|
+// over the remaining rows in their current order) -- barrier -- every thread forms the pivot
+// reciprocal itself (one IEEE division + a double-double Newton step: the same bits on every
+// thread) and updates its share of the trailing block of [A | B] with l = A[row][k] * 1/akk --
+// barrier.  Back substitution, one barrier per step: X[k] = B[k] / U[k][k] goes straight to
+// H, and B[q] -= U[q][k] X[k] (q < k) recomputes X[k] locally.  (Double-double throughout:
+// the contraction is compared with the exact value at 1e-12, R9.)  grid: x = owned
+// interface, y = a share of the right-hand-side columns (each CTA eliminates A itself and
+// carries only its columns of B: the elimination is r^3/3, the right-hand sides r^2 nc).
+__device__ __forceinline__ DD dd_recip(DD y) {
+  const double q1 = 1.0 / y.hi;
+  const DD e = dd_sub(dd_make(1.0), dd_mul_d(y, q1));   // 1 - y q1, tiny
+  return dd_add(dd_make(q1), dd_mul_d(e, q1));
+}
+
 __global__ void __launch_bounds__(256) k_solve(DevCtx c) {
   const int i = blockIdx.x + c.kb;
   const int cap = c.cap, d = c.d;
   extern __shared__ DD smd[];
   DD* A = smd;                 // [cap][cap]
   DD* Bm = smd + cap * cap;    // [cap][cap]
-  __shared__ DD l[TTC_MAX_RANK_DEV];
-  __shared__ int piv_row;
+  __shared__ DD dinv[TTC_MAX_RANK_DEV];
+  __shared__ int perm[TTC_MAX_RANK_DEV];
   const int r = rec_rank(c.rec_cur, c.RS, i);
-  const int nc = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+  const int nc_all = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+  const int cps = (nc_all + gridDim.y - 1) / gridDim.y, c0 = blockIdx.y * cps;
+  const int nc = min(nc_all - c0, cps);   // this CTA's columns [c0, c0 + nc)
+  if (nc <= 0) return;
   for (int t = threadIdx.x; t < r * r; t += blockDim.x) {
     const int a = t / r, b = t % r;
     A[a * cap + b] = dd_make(c.M[((long long)i * cap + a) * cap + b]);
   }
   for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
     const int a = t / nc, b = t % nc;
-    Bm[a * cap + b] = c.W[((long long)(i + 1) * cap + a) * cap + b];
+    Bm[a * cap + b] = c.W[((long long)(i + 1) * cap + a) * cap + c0 + b];
   }
+  for (int t = threadIdx.x; t < r; t += blockDim.x) perm[t] = t;
   __syncthreads();
   for (int k = 0; k < r; ++k) {
     if (threadIdx.x < 32) {
       double bv = -1.0;
-      int bi = k;
-      for (int row = k + threadIdx.x; row < r; row += 32) {
-        const double v = fabs(A[row * cap + k].hi);
-        if (v > bv) { bv = v; bi = row; }
+      int bq = k;
+      for (int q = k + threadIdx.x; q < r; q += 32) {
+        const double v = fabs(A[perm[q] * cap + k].hi);
+        if (v > bv) { bv = v; bq = q; }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+        if (ov > bv || (ov == bv && oq < bq)) { bv = ov; bq = oq; }
       }
       if (threadIdx.x == 0) {
-        piv_row = bi;
-        if (!(bv > 0.0)) atomicOr(&c.flags[0], 1);
+        const int t = perm[k];
+        perm[k] = perm[bq];
+        perm[bq] = t;
+        if (!(bv > 0.0) && blockIdx.y == 0) atomicOr(&c.flags[0], 1);
       }
     }
     __syncthreads();
-    const int pr = piv_row;
-    if (pr != k) {
-      for (int t = threadIdx.x; t < cap; t += blockDim.x) {
-        if (t < r) { DD x = A[k * cap + t]; A[k * cap + t] = A[pr * cap + t]; A[pr * cap + t] = x; }
-        if (t < nc) { DD y = Bm[k * cap + t]; Bm[k * cap + t] = Bm[pr * cap + t]; Bm[pr * cap + t] = y; }
-      }
-      __syncthreads();
-    }
-    const DD akk = A[k * cap + k];
-    for (int row = k + 1 + threadIdx.x; row < r; row += blockDim.x) l[row] = dd_div(A[row * cap + k], akk);
-    __syncthreads();
-    const int width = (r - k - 1) + nc;
-    for (int t = threadIdx.x; t < (r - k - 1) * width; t += blockDim.x) {
-      const int row = k + 1 + t / width;
-      const int colx = t % width;
-      if (colx < r - k - 1) {
+    const int pk = perm[k];
+    const DD inv = dd_recip(A[pk * cap + k]);
+    if (threadIdx.x == 0) dinv[k] = inv;
+    const int nr = r - k - 1, width = nr + nc;
+    for (int t = threadIdx.x; t < nr * width; t += blockDim.x) {
+      const int q = t / width, colx = t - q * width;
+      const int row = perm[k + 1 + q];
+      const DD l = dd_mul(A[row * cap + k], inv);
+      if (colx < nr) {
         const int col = k + 1 + colx;
-        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l[row], A[k * cap + col]));
+        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l, A[pk * cap + col]));
       } else {
-        const int col = colx - (r - k - 1);
-        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l[row], Bm[k * cap + col]));
+        const int col = colx - nr;
+        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l, Bm[pk * cap + col]));
       }
     }
     __syncthreads();
   }
+  DD* H = c.H + (long long)i * cap * cap;
   for (int k = r - 1; k >= 0; --k) {
-    for (int col = threadIdx.x; col < nc; col += blockDim.x) Bm[k * cap + col] = dd_div(Bm[k * cap + col], A[k * cap + k]);
-    __syncthreads();
-    for (int t = threadIdx.x; t < k * nc; t += blockDim.x) {
-      const int q = t / nc, col = t % nc;
-      Bm[q * cap + col] = dd_sub(Bm[q * cap + col], dd_mul(A[q * cap + k], Bm[k * cap + col]));
+    const int pk = perm[k];
+    const DD dk = dinv[k];
+    for (int t = threadIdx.x; t < (k + 1) * nc; t += blockDim.x) {
+      const int q = t / nc, col = t - q * nc;   // q == k: write X[k]; q < k: update row q
+      const DD xk = dd_mul(Bm[pk * cap + col], dk);
+      if (q == k) {
+        H[(long long)k * cap + c0 + col] = xk;
+      } else {
+        const int pq = perm[q];
+        Bm[pq * cap + col] = dd_sub(Bm[pq * cap + col], dd_mul(A[pq * cap + k], xk));
+      }
     }
     __syncthreads();
-  }
-  for (int t = threadIdx.x; t < r * nc; t += blockDim.x) {
-    const int a = t / nc, b = t % nc;
-    c.H[((long long)i * cap + a) * cap + b] = Bm[a * cap + b];
   }
 }
 
@@ -472,6 +542,82 @@ __global__ void __launch_bounds__(256) k_chain_level(int cap, const DD* src, con
       rec[3 + a * cap + col] = C[a * cap + col].hi;
       rec[3 + (long long)cap * cap + a * cap + col] = C[a * cap + col].lo;
     }
+  }
+}
+
+// Rank 0's partial product as a vector chain: v = W_0 H_kb H_kb+1 ... H_{ke-1}, one
+// vector-matrix product per interface in one CTA (r^2 double-double terms per step instead of
+// the tree's r^3 per product).  Column col of a step is summed by 4 adjacent lanes (terms
+// k = sub mod 4, then an xor combine); after every step v is rescaled by the exact power of
+// two 2^-e of its largest entry (e accumulated in log2scale) so long chains neither overflow
+// nor underflow.  Writes the chain record [1, cols, log2scale, hi[cols], lo[cols]].
+#define CHAIN_VEC_MAX 64   // interfaces up to which rank 0 uses the vector chain
+__global__ void __launch_bounds__(256) k_chain_vec(DevCtx c, int i_begin, int i_end, double* rec) {
+  const int cap = c.cap, d = c.d;
+  __shared__ DD v[2][TTC_MAX_RANK_DEV];
+  __shared__ double wmax[2][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col = tid >> 2, sub = tid & 3;
+  int len = d > 1 ? rec_rank(c.rec_cur, c.RS, 0) : 1;
+  for (int t = tid; t < len; t += blockDim.x) v[0][t] = c.W[t];   // W_0, row 0
+  long long lg = 0;
+  int cur = 0, ex = 0;
+  // this lane's terms of the next step's H column, prefetched a step ahead (cap <= 64)
+  constexpr int KPL = TTC_MAX_RANK_DEV / 4;
+  DD hn[KPL];
+  auto fetch = [&](int i) {
+    const int rows = i == i_begin ? len : rec_rank(c.rec_cur, c.RS, i);
+    const int cols = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+    const DD* H = c.H + (long long)i * cap * cap;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+      const int k = sub + 4 * q;
+      hn[q] = (col < cols && k < rows) ? H[(long long)k * cap + col] : dd_make(0.0);
+    }
+  };
+  if (i_begin < i_end) fetch(i_begin);
+  __syncthreads();
+  for (int i = i_begin; i < i_end; ++i) {
+    const int rows = len;
+    const int cols = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
+    DD hc[KPL];
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) hc[q] = hn[q];
+    if (i + 1 < i_end) fetch(i + 1);
+    // v * 2^-ex by two exact power-of-two factors (|ex| <= 1074)
+    const double sc1 = ldexp(1.0, -(ex / 2)), sc2 = ldexp(1.0, -(ex - ex / 2));
+    DD acc = dd_make(0.0);
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+      const int k = sub + 4 * q;
+      if (k < rows) {
+        const DD vk = v[cur][k];
+        acc = dd_add(acc, dd_mul(DD{vk.hi * sc1 * sc2, vk.lo * sc1 * sc2}, hc[q]));
+      }
+    }
+    acc = dd_add(acc, DD{__shfl_xor_sync(0xffffffffu, acc.hi, 1), __shfl_xor_sync(0xffffffffu, acc.lo, 1)});
+    acc = dd_add(acc, DD{__shfl_xor_sync(0xffffffffu, acc.hi, 2), __shfl_xor_sync(0xffffffffu, acc.lo, 2)});
+    double mx = (col < cols) ? fabs(acc.hi) : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int p = (i - i_begin) & 1;
+    if (lane == 0) wmax[p][warp] = mx;
+    if (sub == 0 && col < cols) v[cur ^ 1][col] = acc;
+    __syncthreads();
+    mx = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mx = fmax(mx, wmax[p][q]);
+    ex = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &ex);
+    lg += ex;
+    cur ^= 1;
+    len = cols;
+  }
+  if (tid == 0) { rec[0] = 1; rec[1] = len; rec[2] = (double)lg; }
+  const long long LO = (long long)cap * cap;
+  for (int t = tid; t < len; t += blockDim.x) {
+    const DD x = dd_ldexp(v[cur][t], -ex);
+    rec[3 + t] = x.hi;
+    rec[3 + LO + t] = x.lo;
   }
 }
 
