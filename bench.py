@@ -157,12 +157,31 @@ def fiber_roofline(kt, stats, family, modes, peaks):
             "per_unit": f"{fpe} flop / entry" + ("" if fused else " + 8 B written")}
 
 
-def roofline(kt, stats, family, peaks, peak_src, modes=0):
-    """kt: {name: (launches, ms)} of the profiling pass; stats: its summed counters."""
+def ncu_traffic(workload, kernel):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full`
+    capture (profiles/ncu_traffic.json, written by tools/ncu_report.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f).get(workload)
+    except Exception:
+        return None, None
+    if not e or not e["kernel"].startswith(kernel):
+        return None, None
+    return e["dram_bytes_per_launch"], e["source"]
+
+
+def roofline(kt, stats, family, peaks, peak_src, modes=0, workload=None, cached=False):
+    """kt: {name: (launches, ms)} of the profiling pass; stats: its summed counters.
+    The bound is the roof the kernel's algorithmic work comes closest to: fp64 flops against
+    the derived fp64 peak, or -- when the rook steps stream the u/v factors from memory (not
+    the cached launch shape) -- algorithmic bytes against the measured HBM bandwidth."""
     name = max(kt, key=lambda k: kt[k][1])
     launches, ms = kt[name]
     avg_s = ms / max(1, launches) / 1e3
-    out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": None}
+    traffic, tsrc = ncu_traffic(workload, name + "s" if name == "k_sweep" else name)
+    out = {"kernel": name, "avg_us": avg_s * 1e6, "launches": launches, "traffic": traffic}
+    if traffic is not None:
+        out["traffic_source"] = tsrc
     fpe = flops_per_entry(family, modes)
     if name == "k_sweep":
         ent = stats["sb_entries"] / max(1, launches)
@@ -177,18 +196,25 @@ def roofline(kt, stats, family, peaks, peak_src, modes=0):
         return out
     flops = ent * fpe + 2 * upd   # one multiply + one subtract per u_t(x) v_t(y) term
     tf = flops / avg_s / 1e12
-    if name == "k_sweep":
-        # memory side: every u_t(x) v_t(y) term reads one factor from memory (the other is
-        # staged), every entry writes its E (and the column its raw value) -- when the rook
-        # rows are not kept on chip this is HBM/L2 traffic
-        bytes_ = 8 * upd + 16 * ent
-        out["memory_GBs_if_uncached"] = bytes_ / avg_s / 1e9
-    out.update({"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": tf / FP64_PEAK_TFLOPS, "entries_per_launch": ent, "updates_per_launch": upd,
-                "limiter": "latency: the dependent argmax chain of Alg. 2 (DESIGN.md 5b)" if name == "k_sweep"
-                else "throughput",
-                "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
-                "peak_source": "derived fp64 FMA peak: 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §6)"})
+    alu = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+           "frac": tf / FP64_PEAK_TFLOPS,
+           "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
+           "peak_source": "derived fp64 FMA peak: 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §6)"}
+    out.update({"entries_per_launch": ent, "updates_per_launch": upd})
+    if name == "k_sweep" and not cached:
+        # memory side: every u_t(x) v_t(y) term streams one factor (the other is staged),
+        # every entry writes its E (and the column its raw value): 8 B/term + 16 B/entry
+        gbs = (8 * upd + 16 * ent) / avg_s / 1e9
+        hbm = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+               "frac": gbs / peaks["hbm_gbs"], "per_unit": "8 B/update term + 16 B/entry",
+               "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+        main, other = (hbm, alu) if hbm["frac"] >= alu["frac"] else (alu, hbm)
+        out.update(main)
+        out["other_roof"] = other
+    else:
+        out.update(alu)
+    out["limiter"] = ("latency: the dependent argmax chain of Alg. 2 (DESIGN.md 5b)" if name == "k_sweep"
+                      and out["frac"] < 0.1 else "throughput")
     return out
 
 
@@ -413,7 +439,8 @@ def main():
             st[k] = st.get(k, 0) + v
     core.set_timing(False)
     peaks, peak_src = measured_peaks()
-    roof = roofline(kt, st, wl.family, peaks, peak_src, wl.modes)
+    roof = roofline(kt, st, wl.family, peaks, peak_src, wl.modes, workload_config(wl, world)["workload"],
+                    core.launch_shape()["cached"])
     froof = fiber_roofline(kt, st, wl.family, wl.modes, peaks)
     kernel_ms = {k: v[1] / nprof for k, v in kt.items() if v[0]}
 
