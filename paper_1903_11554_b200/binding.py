@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libttcross.so")
+LIB_PATH = os.environ.get("TTC_LIB_PATH") or os.path.join(HERE, "libttcross.so")   # (override: build variants)
 
 TTC_OK = 0
 TTC_FAMILY_C = 0

@@ -185,9 +185,28 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false
   if (fused) {
     {
       Timed t(c, K_FIBER);
-      const dim3 g((tup + 7) / 8, tup, njobs);
-      if (dc.family == TTC_FAMILY_C) k_fiber_wsum<0><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
-      else k_fiber_wsum<1><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
+      // tiles of FW_TA x FW_TB fibers (the grid covers rank = cap; tiles beyond the actual
+      // ranks exit at once) x NS node ranges, NS (the cluster size) doubled up to 8 while
+      // the grid has fewer than 4 waves of 4 CTAs per SM and the ranges keep >= 32 nodes
+      const int ta = (tup + FW_TA - 1) / FW_TA, tb = (tup + FW_TB - 1) / FW_TB;
+      const long long tiles = (long long)ta * tb * njobs;
+      int ns = 1;
+      while (ns < 8 && tiles * ns < 16LL * c->sms && n / (2 * ns) >= 32) ns *= 2;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(ta * tb, ns, njobs);
+      lc.blockDim = dim3(FW_TA * FW_TB);
+      lc.dynamicSmemBytes = fw_smem_bytes();
+      lc.stream = c->ls;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1;
+      at[0].val.clusterDim.y = ns;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaError_t e = dc.family == TTC_FAMILY_C ? cudaLaunchKernelEx(&lc, k_fiber_wsum<0>, dc, kind, jbase, tb)
+                                                : cudaLaunchKernelEx(&lc, k_fiber_wsum<1>, dc, kind, jbase, tb);
+      if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_fiber_wsum launch: ") + cudaGetErrorString(e));
     }
     return check_launch("k_fiber_wsum");
   }
@@ -647,6 +666,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     allow((const void*)k_sweep<1, false, 512>, 180 * 1024);
     allow((const void*)k_sweep<0, true, 512>, 180 * 1024);
     allow((const void*)k_sweep<1, true, 512>, 180 * 1024);
+    allow((const void*)k_fiber_wsum<0>, fw_smem_bytes());
+    allow((const void*)k_fiber_wsum<1>, fw_smem_bytes());
     const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));

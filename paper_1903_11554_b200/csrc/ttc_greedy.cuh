@@ -53,7 +53,7 @@ __device__ double init_entry(const DevCtx& c, int q) {
     const double ui = c.u[i * n + init_coord(c, q, i)];
     for (int j = i + 1; j < d; ++j) dde_mul_d(p, rho_ool(ui, c.u[j * n + init_coord(c, q, j)]));
   }
-  return __ddiv_rn(dde_round(p), SS);
+  return dde_div(p, SS);
 }
 
 // one block of N_INIT threads: t0 = first argmax |A| over the seeded samples -> t0buf[d],
@@ -229,7 +229,7 @@ __device__ __forceinline__ double sb_entry(const DevCtx& c, int job, int k, int 
   dde_mul(p, c.QL1[oa + b]);
   dde_mul(p, c.QR0[ob + a]);
   dde_mul_d(p, rho(c.u[k * n + a], c.u[(k + 1) * n + b]));
-  return __ddiv_rn(dde_round(p), SS);
+  return dde_div(p, SS);
 }
 
 // pivot positions of interface k: xs = alpha_s*n + a_s, ys = beta_s*n + b_s
@@ -571,7 +571,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       dde_mul(p, S.f_slot[al]);
       dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + be * n + a]);
       dde_mul_d(p, rho(ua, ub));
-      raw = __ddiv_rn(dde_round(p), SS);
+      raw = dde_div(p, SS);
     }
     double e = raw;
     if (CACHED)
@@ -654,7 +654,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       dde_mul(p, S.f_slot[be]);
       dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + al * n + b]);
       dde_mul_d(p, rho(ua, ub));
-      e = __ddiv_rn(dde_round(p), SS);
+      e = dde_div(p, SS);
     }
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));

@@ -11,6 +11,7 @@
 // result equals the oracle's plain O(d^2)-per-entry evaluation bit for bit.
 #pragma once
 #include "ttc_common.cuh"
+#include "ttc_greedy.cuh"   // cooperative_groups, cp.async helpers
 
 namespace ttc {
 
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
         DDE p = c.pf[(base + al) * c.cap + be];
         dde_mul(p, c.ql[(base + al) * n + a]);
         dde_mul(p, c.qr[(base + be) * n + a]);
-        v = __ddiv_rn(dde_round(p), SS);
+        v = dde_div(p, SS);
       }
       F[f] = v;
     }
@@ -193,66 +194,178 @@ __global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
       DDE p = pf[be];
       dde_mul(p, pa);
       dde_mul(p, c.qr[(base + be) * n + a]);
-      v = __ddiv_rn(dde_round(p), SS);
+      v = dde_div(p, SS);
     }
     F[(long long)be * n] = v;
   }
 }
 
+__device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, double yl) {
+  const double p = __dmul_rn(h, yh);
+  const double err = fma(h, yh, -p);
+  const double t = fma(h, yl, fma(l, yh, err));
+  const double s = __dadd_rn(p, t);
+  l = __dsub_rn(t, __dsub_rn(s, p));
+  h = s;
+}
+
+
 // Fused quadrature fibers + weighted sums (t-form families), the product path of
 // tt_integrate: W_m[alpha][beta] = sum_a w_{m,a} A(X_alpha, a, Y_beta) with the entries
-// evaluated on the fly -- a warp per fiber (alpha, beta), lanes over the nodes a, no fiber
-// written to memory.  The entry arithmetic is k_fiber's and the accumulation is k_wsum's
-// (lane-strided double-double sums, then the xor tree), so W is bit-identical to the
-// unfused k_fiber -> k_wsum pair.  grid: x = chunk of 8 betas (one per warp), y = alpha,
-// z = mode (jbase + z); block 256.
+// evaluated on the fly, nothing written per entry.
+// A CTA owns a tile of FW_TA x FW_TB fibers (thread = fiber) and one of NS node ranges; the
+// NS CTAs of a tile form a cluster (1, NS, 1) and combine their partial sums through
+// distributed shared memory in node-range order.  The node range is walked in chunks of
+// FW_CH nodes, double-buffered in shared memory with cp.async: the chunk's Q_L rows of the
+// tile's alphas, Q_R rows of its betas (hi / lo / e planes, row stride FW_CH + 1 so the 16
+// rows a warp reads at one node fall in distinct banks) and c_m, w_m of its nodes -- every
+// factor is fetched once per tile instead of once per entry.  The fiber's frozen factors
+// (S_L + S_R, Pf) stay in registers.
+// P = Pf * Q_L * Q_R is formed without intermediate renormalisation: every stored factor has
+// hi in [2^-250, 1] (or 0), so the partial products and their error terms stay normal and
+// the result is the renormalised chain's up to an exact power of two; dde_div applies it --
+// the same bits as dde_mul + dde_round + division (R3).  Every
+// term w_a * A >= 0 (positive weights, positive entries), so the double-double accumulation
+// is the same-sign sum: two_sum of the high parts, low parts added, one renormalisation
+// (relative error ~2^-104 per term, no cancellation).
+#define FW_TA 16
+#define FW_TB 16
+#define FW_CH 32
+#define FW_RS (FW_CH + 1)
+struct FwBuf {
+  double qlh[FW_TA][FW_RS], qll[FW_TA][FW_RS];
+  double qrh[FW_TB][FW_RS], qrl[FW_TB][FW_RS];
+  int qle[FW_TA][FW_RS], qre[FW_TB][FW_RS];
+  long long chi[FW_CH], clo[FW_CH];
+  double w[FW_CH];
+};
+__host__ __device__ constexpr int fw_smem_bytes() { return 2 * (int)sizeof(FwBuf); }
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8g(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 template <int FAMILY>
-__global__ void __launch_bounds__(256) k_fiber_wsum(DevCtx c, int kind, int jbase) {
-  const int j = jbase + blockIdx.z, al = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int be = blockIdx.x * (blockDim.x >> 5) + warp;
+__global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int kind, int jbase, int tiles_b) {
+  extern __shared__ __align__(16) unsigned char fw_dyn[];
+  FwBuf* buf = reinterpret_cast<FwBuf*>(fw_dyn);
+  __shared__ DD part[FW_TA * FW_TB];
+  cg::cluster_group cl = cg::this_cluster();
+  const int j = jbase + blockIdx.z;
   Job jb = make_job(c, kind, j);   // (entries counted by k_frozen_sides)
-  if (al >= jb.rx || be >= jb.ry) return;
+  const int A0 = (blockIdx.x / tiles_b) * FW_TA, B0 = (blockIdx.x % tiles_b) * FW_TB;
+  if (A0 >= jb.rx || B0 >= jb.ry) return;   // (uniform over the cluster: same tile)
+  const int tid = threadIdx.x;
+  const int ra = tid / FW_TB, rb = tid % FW_TB;
+  const int al = A0 + ra, be = B0 + rb;
+  const bool live = al < jb.rx && be < jb.ry;
   const int n = c.n, m = jb.m;
+  const int NS = gridDim.y, ns = blockIdx.y;
+  const int len = (n + NS - 1) / NS;
+  const int a_lo = min(n, ns * len), a_hi = min(n, a_lo + len);
+  const int na = min(FW_TA, jb.rx - A0), nb = min(FW_TB, jb.ry - B0);
   const long long base = (long long)j * c.cap;
-  ESum s0 = c.sl[base + al];
-  esum_add(s0, c.sr[base + be]);
-  DDE p0;
-  const DDE* ql = nullptr;
-  const DDE* qr = nullptr;
-  if (FAMILY == 1) {
-    p0 = c.pf[(base + al) * c.cap + be];
-    ql = c.ql + (base + al) * n;
-    qr = c.qr + (base + be) * n;
-  }
-  const long long* chi = c.chi + (long long)m * n;
-  const long long* clo = c.clo + (long long)m * n;
-  const double* w = c.w + (long long)m * n;
-  DD acc = dd_make(0.0);
-#pragma unroll 2
-  for (int a = lane; a < n; a += 32) {
-    ESum s = s0;
-    esum_add(s, chi[a], clo[a]);
-    const double S = esum_round(s);
-    const double SS = __dmul_rn(S, S);
-    double v;
-    if (FAMILY == 0) {
-      v = __drcp_rn(SS);
-    } else {
-      DDE p = p0;
-      dde_mul(p, ql[a]);
-      dde_mul(p, qr[a]);
-      v = __ddiv_rn(dde_round(p), SS);
+  const long long* gchi = c.chi + (long long)m * n;
+  const long long* gclo = c.clo + (long long)m * n;
+  const double* gw = c.w + (long long)m * n;
+  const DDE* gql = FAMILY == 1 ? c.ql + (base + A0) * n : nullptr;
+  const DDE* gqr = FAMILY == 1 ? c.qr + (base + B0) * n : nullptr;
+  // stage chunk [a0, a0 + cn) into buffer b
+  auto stage = [&](int b, int a0, int cn) {
+    FwBuf& B = buf[b];
+    if (tid < cn) {
+      cp_async8g(&B.chi[tid], gchi + a0 + tid);
+      cp_async8g(&B.clo[tid], gclo + a0 + tid);
+      cp_async8g(&B.w[tid], gw + a0 + tid);
     }
-    const double wa = w[a];
-    const double pr = wa * v;
-    acc = dd_add(acc, DD{pr, fma(wa, v, -pr)});
+    if (FAMILY == 1) {
+      // (row, node) pairs of the tile's rows, node fastest (coalesced along each row); whole
+      // chunks of FW_CH nodes (nodes past the range but inside the grid are harmless)
+      for (int e = tid; e < (na + nb) * FW_CH; e += FW_TA * FW_TB) {
+        const int row = e / FW_CH, a = e % FW_CH;
+        if (a0 + a >= n) continue;
+        const bool left = row < na;
+        const int rr = left ? row : row - na;
+        const double* src = reinterpret_cast<const double*>((left ? gql : gqr) + (long long)rr * n + a0 + a);
+        if (left) {
+          cp_async8g(&B.qlh[rr][a], src);
+          cp_async8g(&B.qll[rr][a], src + 1);
+          cp_async4(&B.qle[rr][a], src + 2);
+        } else {
+          cp_async8g(&B.qrh[rr][a], src);
+          cp_async8g(&B.qrl[rr][a], src + 1);
+          cp_async4(&B.qre[rr][a], src + 2);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  ESum s0 = esum_zero();
+  DDE p0 = dde_one();
+  if (live) {
+    s0 = c.sl[base + al];
+    esum_add(s0, c.sr[base + be]);
+    if (FAMILY == 1) p0 = c.pf[(base + al) * c.cap + be];
   }
-  for (int o = 16; o; o >>= 1) {
-    DD other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
-    acc = dd_add(acc, other);
+  double hi = 0.0, lo = 0.0;
+  const int nchunk = (a_hi - a_lo + FW_CH - 1) / FW_CH;
+  if (nchunk > 0) stage(0, a_lo, min(FW_CH, a_hi - a_lo));
+  for (int ci = 0; ci < nchunk; ++ci) {
+    const int a0 = a_lo + ci * FW_CH, cn = min(FW_CH, a_hi - a0);
+    if (ci + 1 < nchunk) {
+      stage((ci + 1) & 1, a0 + FW_CH, min(FW_CH, a_hi - a0 - FW_CH));
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
+    __syncthreads();
+    const FwBuf& B = buf[ci & 1];
+    if (live) {
+#pragma unroll 2
+      for (int a = 0; a < cn; ++a) {
+        ESum s = s0;
+        esum_add(s, B.chi[a], B.clo[a]);
+        const double S = esum_round(s);
+        const double SS = __dmul_rn(S, S);
+        double v;
+        if (FAMILY == 0) {
+          v = __drcp_rn(SS);
+        } else {
+          double ph = p0.hi, pl = p0.lo;
+          dd_mul_raw(ph, pl, B.qlh[ra][a], B.qll[ra][a]);
+          dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
+          v = dde_div(DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0}, SS);
+        }
+        const double wa = B.w[a];
+        const double pr = __dmul_rn(wa, v);
+        const double pe = fma(wa, v, -pr);
+        const double s1 = __dadd_rn(hi, pr);
+        const double bb = __dsub_rn(s1, hi);
+        const double er = __dadd_rn(__dsub_rn(hi, __dsub_rn(s1, bb)), __dsub_rn(pr, bb));
+        const double l1 = __dadd_rn(lo, __dadd_rn(er, pe));
+        hi = __dadd_rn(s1, l1);
+        lo = __dsub_rn(l1, __dsub_rn(hi, s1));
+      }
+    }
+    __syncthreads();   // buffer ci & 1 is restaged at iteration ci + 1
   }
-  if (lane == 0) c.W[((long long)j * c.cap + al) * c.cap + be] = acc;
+  part[tid] = DD{hi, lo};
+  if (NS == 1) {
+    if (live) c.W[((long long)j * c.cap + al) * c.cap + be] = part[tid];
+    return;
+  }
+  cl.sync();
+  if (ns == 0 && live) {
+    DD acc = part[tid];
+    for (int r = 1; r < NS; ++r) acc = dd_add(acc, cl.map_shared_rank(part, r)[tid]);
+    c.W[((long long)j * c.cap + al) * c.cap + be] = acc;
+  }
+  cl.sync();   // the partials stay readable until rank 0 has summed them
 }
 
 // quadrature fibers of the x-form families: direct evaluation of every entry (the x-form
@@ -314,7 +427,7 @@ __global__ void k_intersection(DevCtx c, int ibase) {
       double ua = c.u[a * n + (a <= i ? Ps[a] : Pt[a])];
       for (int b = a + 1; b < d; ++b) dde_mul_d(p, rho(ua, c.u[b * n + (b <= i ? Ps[b] : Pt[b])]));
     }
-    v = __ddiv_rn(dde_round(p), SS);
+    v = dde_div(p, SS);
   }
   c.M[((long long)i * c.cap + s) * c.cap + t] = v;
 }
