@@ -137,10 +137,11 @@ def flops_per_entry(family, m):
 
 def fiber_roofline(kt, stats, family, modes, peaks):
     """The quadrature fiber kernel: the throughput-mode batched integrand evaluation.
-    t-form (k_fiber_wsum, fused with the weighted sum, nothing written per entry): C 4 flop
-    per entry, D 26 (exact-limb sum and rounding 3, two double-double products 20, rounding
-    and division 3), plus 23 for the double-double accumulation of w_a * A (product 1, its
-    error 2, double-double add 20); x-form (k_fiber_x, 8 B written per entry):
+    t-form (k_fiber_wsum, fused with the weighted sum, nothing written per entry): fp64 flops
+    per entry as executed, DADD + DMUL + 2 DFMA from ncu's sass op counters (C 27.2 on C_200,
+    D 53.3 on D_20: profiles/r01n_ncu_fiber_wsum_*_flops.csv) -- the exact-limb sum and its
+    rounding, the double-double products, the IEEE division (reciprocal + Newton steps) and
+    the double-double accumulation of w_a * A; x-form (k_fiber_x, 8 B written per entry):
     flops_per_entry."""
     launches, ms = kt.get("k_fiber", (0, 0.0))
     if not launches or ms <= 0:
@@ -148,7 +149,7 @@ def fiber_roofline(kt, stats, family, modes, peaks):
     avg_s = ms / launches / 1e3
     ent = stats["fiber_entries"] / launches
     fused = family in (0, 1)
-    fpe = {0: 4 + 23, 1: 26 + 23}[family] if fused else flops_per_entry(family, modes)
+    fpe = {0: 27.2, 1: 53.3}[family] if fused else flops_per_entry(family, modes)
     tf = ent * fpe / avg_s / 1e12
     gbs = 0.0 if fused else ent * 8 / avg_s / 1e9
     return {"kernel": "k_fiber_wsum" if fused else "k_fiber_x", "avg_us": avg_s * 1e6, "entries_per_launch": ent,

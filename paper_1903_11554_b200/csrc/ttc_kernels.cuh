@@ -230,7 +230,7 @@ __device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, doub
 // (relative error ~2^-104 per term, no cancellation).
 #define FW_TA 16
 #define FW_TB 16
-#define FW_CH 32
+#define FW_CH 36   // max nodes per chunk (row stride 37 doubles: 16 rows in distinct banks)
 #define FW_RS (FW_CH + 1)
 struct FwBuf {
   double qlh[FW_TA][FW_RS], qll[FW_TA][FW_RS];
@@ -284,11 +284,9 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
       cp_async8g(&B.w[tid], gw + a0 + tid);
     }
     if (FAMILY == 1) {
-      // (row, node) pairs of the tile's rows, node fastest (coalesced along each row); whole
-      // chunks of FW_CH nodes (nodes past the range but inside the grid are harmless)
-      for (int e = tid; e < (na + nb) * FW_CH; e += FW_TA * FW_TB) {
-        const int row = e / FW_CH, a = e % FW_CH;
-        if (a0 + a >= n) continue;
+      // (row, node) pairs of the tile's rows, node fastest (coalesced along each row)
+      for (int e = tid; e < (na + nb) * cn; e += FW_TA * FW_TB) {
+        const int row = e / cn, a = e - row * cn;
         const bool left = row < na;
         const int rr = left ? row : row - na;
         const double* src = reinterpret_cast<const double*>((left ? gql : gqr) + (long long)rr * n + a0 + a);
@@ -313,12 +311,14 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
     if (FAMILY == 1) p0 = c.pf[(base + al) * c.cap + be];
   }
   double hi = 0.0, lo = 0.0;
+  // balanced chunks of <= FW_CH nodes (65 nodes: 33 + 32, not 36 + 29 or 32 + 32 + 1)
   const int nchunk = (a_hi - a_lo + FW_CH - 1) / FW_CH;
-  if (nchunk > 0) stage(0, a_lo, min(FW_CH, a_hi - a_lo));
+  const int csz = nchunk > 0 ? (a_hi - a_lo + nchunk - 1) / nchunk : 0;
+  if (nchunk > 0) stage(0, a_lo, min(csz, a_hi - a_lo));
   for (int ci = 0; ci < nchunk; ++ci) {
-    const int a0 = a_lo + ci * FW_CH, cn = min(FW_CH, a_hi - a0);
+    const int a0 = a_lo + ci * csz, cn = min(csz, a_hi - a0);
     if (ci + 1 < nchunk) {
-      stage((ci + 1) & 1, a0 + FW_CH, min(FW_CH, a_hi - a0 - FW_CH));
+      stage((ci + 1) & 1, a0 + csz, min(csz, a_hi - a0 - csz));
       cp_async_wait_group<1>();
     } else {
       cp_async_wait_group<0>();
