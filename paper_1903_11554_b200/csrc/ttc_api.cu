@@ -72,6 +72,7 @@ struct ttc_ctx {
   bool greedy_cached = false;  // k_sweep keeps its rows' u / columns' v in shared memory
   size_t greedy_smem = 0;      // dynamic shared memory of k_sweep
   int greedy_threads = 256;    // CTA size of k_sweep (256: two CTAs per SM, 512: one)
+  int fw_ns = 0;               // k_fiber_wsum cluster size override (TTC_FW_NS; 0 = host rule)
   const void* greedy_fn = nullptr;   // k_sweep variant (one sweep)
   const void* sweeps_fn = nullptr;   // k_sweeps variant (persistent, world == 1)
   bool persistent = false;           // k_sweeps usable (all clusters resident)
@@ -192,6 +193,7 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false
       const long long tiles = (long long)ta * tb * njobs;
       int ns = 1;
       while (ns < 8 && tiles * ns < 16LL * c->sms && n / (2 * ns) >= 32) ns *= 2;
+      if (c->fw_ns > 0) ns = c->fw_ns;   // (experiments: TTC_FW_NS)
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(ta * tb, ns, njobs);
       lc.blockDim = dim3(FW_TA * FW_TB);
@@ -695,6 +697,10 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     if (const char* e = std::getenv("TTC_GREEDY_T")) {
       const int t = std::atoi(e);
       if (t == 256 || t == 512) { T = t; G = std::max(1, pick_g(t == 512 ? sms : 2LL * sms)); }
+    }
+    if (const char* e = std::getenv("TTC_FW_NS")) {
+      const int v = std::atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8) c->fw_ns = v;
     }
     if (const char* e = std::getenv("TTC_PHASE_JOB")) {   // profiling: superblock of the phase clocks
       const int j = std::atoi(e);

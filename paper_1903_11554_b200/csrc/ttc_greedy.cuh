@@ -123,6 +123,7 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
   const int* st = c.sbstate + job * 4;
   __shared__ ESum sS;
   __shared__ DDE sP;
+  __shared__ double sX[64];   // node values of the frozen tuple's first 64 coordinates
   const int* T;
   int lo, hi;  // coordinate range of the frozen tuple
   if (side == 0) {
@@ -144,7 +145,10 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
     const int lane = threadIdx.x;
     ESum s = esum_zero();
     DDE p = dde_one();
-    for (int q = lo + lane; q < hi; q += 32) esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
+    for (int q = lo + lane; q < hi; q += 32) {
+      esum_add(s, c.chi[q * n + T[q]], c.clo[q * n + T[q]]);
+      if (q - lo < 64) sX[q - lo] = c.u[q * n + T[q]];
+    }
     if (c.family == 1)
       for (int a = lo + lane; a < hi; a += 32) {
         const double ua = c.u[a * n + T[a]];
@@ -178,10 +182,11 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
     if (c.family == 1) {
       const double uo = c.u[mode_own * n + a], ux = c.u[mode_oth * n + a];
       DDE p = sP, q = dde_one();
+#pragma unroll 2
       for (int t = lo; t < hi; ++t) {
-        const double x = c.u[t * n + T[t]];
-        dde_mul_d(p, rho_ool(uo, x));
-        dde_mul_d(q, rho_ool(ux, x));
+        const double x = t - lo < 64 ? sX[t - lo] : c.u[t * n + T[t]];
+        dde_mul_d(p, rho(uo, x));   // (inline: the two chains and consecutive t overlap)
+        dde_mul_d(q, rho(ux, x));
       }
       if (side == 0) { c.PA[o + a] = p; c.QL1[o + a] = q; }
       else { c.PB[o + a] = p; c.QR0[o + a] = q; }
@@ -189,20 +194,33 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
   }
 }
 
-__device__ void sb_cx_table(const DevCtx& c, int job, int al, int be, int rl, int rr) {
+// CX[alpha][beta] by one warp: lanes split the k * (d-k-2) cross pairs (i < k, j > k+1), each
+// lane a partial double-double product, then the shuffle tree -- the product is rounded once
+// later, so any grouping gives the same entries (R3).  (A thread per entry ran the
+// whole chain alone: D_20's middle superblocks have ~80 pairs per entry, ~24k cycles.)
+__device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
   const int k = c.kb + job, d = c.d, n = c.n;
-  const int* st = c.sbstate + job * 4;
-  if (al >= rl || be >= rr || (al < st[0] && be < st[1])) return;
+  const int lane = threadIdx.x & 31;
   DDE p = dde_one();
   if (k > 0 && k < d - 2) {
     const int* TX = rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d;
     const int* TY = rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d;
-    for (int i = 0; i < k; ++i) {
-      const double ui = c.u[i * n + TX[i]];
-      for (int j = k + 2; j < d; ++j) dde_mul_d(p, rho_ool(ui, c.u[j * n + TY[j]]));
+    const int nj = d - k - 2, np = k * nj;
+    for (int q = lane; q < np; q += 32) {
+      const int i = q / nj, j = k + 2 + (q - i * nj);
+      dde_mul_d(p, rho_ool(c.u[i * n + TX[i]], c.u[j * n + TY[j]]));
     }
   }
-  c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    DDE y;
+    y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
+    y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
+    y.e = __shfl_xor_sync(0xffffffffu, p.e, o);
+    y.pad = 0;
+    dde_mul(p, y);
+  }
+  if (lane == 0) c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
 }
 
 // A_k(alpha, a; beta, b) from the tables (single rounding, R3)
@@ -830,13 +848,14 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
   }
   if (FAMILY == 1) {
-    // CX for the new pairs: new alpha x all beta, then old alpha x new beta
+    // CX for the new pairs: new alpha x all beta, then old alpha x new beta; a warp per pair
     const int na = (rl - rows_done) * rr, nb = rows_done * (rr - cols_done);
-    for (int e = cr * T + tid; e < na + nb; e += G * T) {
+    const int nw = G * (T >> 5);
+    for (int e = cr * (T >> 5) + (tid >> 5); e < na + nb; e += nw) {   // (warp-uniform)
       int al, be;
       if (e < na) { al = rows_done + (int)(e / rr); be = (int)(e % rr); }
       else { const int f = e - na; al = f / (rr - cols_done); be = cols_done + f % (rr - cols_done); }
-      sb_cx_table(c, job, al, be, rl, rr);
+      sb_cx_table_warp(c, job, al, be);
     }
   }
   TRACE(2);

@@ -109,6 +109,8 @@ def check_run(tt, prob, sweeps, check_fibers=True, check_evals=True):
     (FAMILY_D, 4, 41, 8.0, 16, 0.0, 1024, 1, 9, 16),      # tol = 0, max samples, one rook round
     (FAMILY_C, 4, 21, 6.0, 6, 1e-12, 16, 0, 10, 6),       # no rook rounds: the best sample
     (FAMILY_D, 3, 513, 24.0, 64, 1e-12, 32, 4, 11, 4),    # cap*n = 32832 rows: 4-CTA clusters
+    (FAMILY_D, 4, 65, 8.0, 24, 1e-14, 32, 4, 12, 24),     # ranks past one 16x16 fiber tile, ragged
+    (FAMILY_C, 5, 129, 10.0, 40, 1e-15, 32, 4, 13, 40),   # ranks 40: three tiles, ragged last one
 ])
 def test_parity_small(lib, family, d, n, L, cap, tol, ns, rook, seed, sweeps):
     tt, prob = make(family, d, n, L, cap, tol, ns, rook, seed)
