@@ -243,6 +243,13 @@ void tt_cross_destroy(ttc_ctx* ctx);
 /* Thread-local description of the last error (never NULL). */
 const char* tt_last_error(void);
 
+/* tt_selftest_division -- diagnostics for the division the u/v extension uses with a
+ * divisor known in advance (u_t(x_t)): q_pre[i] = the hoisted-reciprocal quotient,
+ * q_ieee[i] = __ddiv_rn(a[i], b[i]); the two must agree bit for bit.
+ * a, b, q_pre, q_ieee: DEVICE pointers to n doubles (caller-owned); synchronises the device.
+ * TTC_ERR_ARG on n < 0 or a NULL pointer, TTC_ERR_CUDA on a launch failure. */
+int tt_selftest_division(const double* a, const double* b, double* q_pre, double* q_ieee, int64_t n);
+
 /* Library build identifier (compile arch, version). */
 const char* tt_build_info(void);
 

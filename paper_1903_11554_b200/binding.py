@@ -30,7 +30,7 @@ EXPORTS = [
     "tt_integrate_read", "tt_integrate_local", "tt_integrate_partials_buffer", "tt_integrate_finish",
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
     "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info", "tt_cross_get_launch_shape",
-    "tt_cross_get_phase_times",
+    "tt_cross_get_phase_times", "tt_selftest_division",
 ]
 N_KERNELS = 13
 
@@ -94,6 +94,7 @@ def load(path: str = LIB_PATH):
         "tt_integrate_read": (i32, [P, ctypes.POINTER(f64), ctypes.POINTER(f64), ctypes.POINTER(i32)]),
         "tt_last_error": (ctypes.c_char_p, []),
         "tt_build_info": (ctypes.c_char_p, []),
+        "tt_selftest_division": (i32, [P, P, P, P, i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -534,6 +534,25 @@ int ttc_trace_read(unsigned long long* events, int* counts) {
 }
 #endif
 
+// diagnostics: q_pre[i] = div_pre(a[i], b[i], rcp_refined(b[i])), q_ieee[i] = __ddiv_rn(a[i], b[i])
+namespace ttc {
+__global__ void k_selftest_division(const double* a, const double* b, double* qp, double* qi, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    qp[i] = div_pre(a[i], b[i], rcp_refined(b[i]));
+    qi[i] = __ddiv_rn(a[i], b[i]);
+  }
+}
+}  // namespace ttc
+
+int tt_selftest_division(const double* a, const double* b, double* q_pre, double* q_ieee, int64_t n) {
+  if (n < 0 || (n > 0 && (!a || !b || !q_pre || !q_ieee))) return fail(TTC_ERR_ARG, "tt_selftest_division: bad arguments");
+  if (n == 0) return TTC_OK;
+  ttc::k_selftest_division<<<(unsigned)std::min<long long>(4096, (n + 255) / 256), 256>>>(a, b, q_pre, q_ieee, n);
+  if (int e = check_launch("k_selftest_division")) return e;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(TTC_ERR_CUDA, "tt_selftest_division: sync");
+  return TTC_OK;
+}
+
 const char* tt_build_info(void) {
   return "libttcross 0.2 (sm_100a, fp64, -fmad=false, dimension-parallel greedy cross, cluster rook search)";
 }

@@ -274,7 +274,8 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 
 template <int FAMILY>
 __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int side, int r, int x_lo, int x_hi,
-                            const int* p_al, const int* p_a, const double* pdiag, double* coef, double* tile,
+                            const int* p_al, const int* p_a, const double* pdiag, const double* prcp,
+                            double* coef, double* tile,
                             unsigned long long& ent, unsigned long long& upd) {
   const int n = c.n, cap = c.cap;
   const int sbn = (int)c.sbn;
@@ -369,7 +370,7 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
         for (int t = 0; t < r; ++t) {
           if (L > 1) __syncwarp(gmask);   // tile[t][j] final (updated at step t-1 by lane t mod L)
           double f = tile[t * TS + j];
-          if (side == 1) f = __ddiv_rn(f, pdiag[t]);  // v_t
+          if (side == 1) f = div_pre(f, pdiag[t], prcp[t]);  // v_t (= __ddiv_rn bits)
           const int q0 = t + 1 + ((ln - (t + 1)) & (L - 1));
           for (int q = q0; q < r; q += L)
             tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
@@ -382,7 +383,7 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
     for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
       const int s = e / nrow, j = e - s * nrow;
       const double f = tile[s * TS + j];
-      dst[s * sbn + x0 + j] = side == 1 ? __ddiv_rn(f, pdiag[s]) : f;
+      dst[s * sbn + x0 + j] = side == 1 ? div_pre(f, pdiag[s], prcp[s]) : f;
     }
     __syncthreads();
   }
@@ -866,7 +867,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   // ---- phase 2: u / v of the existing pivots on the new rows and columns
   {
     __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
-    __shared__ double pdiag[TTC_MAX_RANK_DEV];
+    __shared__ double pdiag[TTC_MAX_RANK_DEV], prcp[TTC_MAX_RANK_DEV];
     double* coef = dyn;
     double* tile = dyn + (long long)cap * cap;
     const int nr_new = (rl - rows_done) * n, nc_new = (rr - cols_done) * n;
@@ -884,7 +885,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       __syncthreads();
       const int lo = rows_done * n + rr_i * rchunk;
-      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, coef, tile,
+      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
                           ext_ent, ext_upd);
       __syncthreads();
     }
@@ -893,10 +894,11 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         p_al[tid] = S.xs[tid] / n;
         p_a[tid] = S.xs[tid] - (S.xs[tid] / n) * n;
         pdiag[tid] = first ? *c.p0val : U[tid * sbn + S.xs[tid]];
+        prcp[tid] = rcp_refined(pdiag[tid]);
       }
       __syncthreads();
       const int lo = cols_done * n + cc_i * cchunk;
-      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, coef, tile,
+      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
                           ext_ent, ext_upd);
     }
   }
