@@ -415,7 +415,29 @@ __device__ __forceinline__ bool cand_better(double v, long long f, double bv, lo
   return v > bv || (v == bv && f < bf);
 }
 
+// warp argmax of (v, f) with cand_better's order (largest v, then smallest f) on every lane.
+// Candidates are |E| >= 0 with an index < 2^31, or (-1, LLONG_MAX) for none; the bit pattern
+// of a non-negative double orders like its value, so three warp reductions (max of the high
+// words, max of the low words among those, min of the indices among the maxima: REDUX)
+// replace the five-round shuffle tree (tools/microbench.cu: warp_argmax probes).  NaN is
+// never chosen, as with cand_better.
 __device__ __forceinline__ void warp_argmax(double& v, long long& f) {
+  const bool has = v >= 0.0;
+  const unsigned hi = has ? (unsigned)__double2hiint(v) : 0u;
+  const unsigned lo = has ? (unsigned)__double2loint(v) : 0u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const unsigned mf = __reduce_min_sync(0xffffffffu, (has && hi == mh && lo == ml) ? (unsigned)f : 0xffffffffu);
+  if (mf == 0xffffffffu) {
+    v = -1.0;
+    f = LLONG_MAX;
+  } else {
+    v = __hiloint2double((int)mh, (int)ml);
+    f = (long long)mf;
+  }
+}
+// the five-round shuffle tree (kept for the microbenchmark comparison)
+__device__ __forceinline__ void warp_argmax_shfl(double& v, long long& f) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, v, o);

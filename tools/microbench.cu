@@ -6,6 +6,7 @@
 //       product, and one whole D-family superblock entry + 16-term u.v update (the rook step's
 //       per-row chain)
 //   (e) st.async + mbarrier candidate exchange round (the k_sweep cluster argmax)
+//   (f) warp argmax latency: REDUX (warp_argmax) vs the shuffle tree (warp_argmax_shfl)
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
 #include <cooperative_groups.h>
 #include <climits>
@@ -14,6 +15,7 @@
 #include <vector>
 namespace cg = cooperative_groups;
 #include "../paper_1903_11554_b200/csrc/ttc_common.cuh"
+#include "../paper_1903_11554_b200/csrc/ttc_greedy.cuh"
 using namespace ttc;
 
 // (d) dependent chains; kind: 0 dadd, 1 dmul, 2 ddiv, 3 rho, 4 dde_mul, 5 entry + 16-term update
@@ -153,6 +155,24 @@ __global__ void k_chase(const int* next, int iters, int* sink, unsigned long lon
   *sink = p;
 }
 
+// (f) one warp, dependent chain of warp argmaxes; kind 0 REDUX, 1 shuffle tree
+__global__ void k_warp_argmax(int kind, int iters, unsigned long long* out, double* sink) {
+  double v = 0.25 + 1e-3 * ((threadIdx.x * 7) & 31);
+  long long f = threadIdx.x;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    double bv = v;
+    long long bf = f;
+    if (kind == 0) warp_argmax(bv, bf);
+    else warp_argmax_shfl(bv, bf);
+    v = v + bv * 1e-30;   // depends on the result
+    f = (f + bf) & 31;
+  }
+  unsigned long long t1 = clock64();
+  sink[threadIdx.x] = v + f;
+  if (threadIdx.x == 0) *out = t1 - t0;
+}
+
 int main() {
   unsigned long long* d_out;
   cudaMalloc(&d_out, 8);
@@ -175,6 +195,19 @@ int main() {
     cudaDeviceSynchronize();
     cudaMemcpy(&h, d_out, 8, cudaMemcpyDeviceToHost);
     printf("{\"probe\": \"cluster_argmax_round\", \"G\": %d, \"cycles\": %.1f}\n", G, (double)h / iters);
+  }
+  {
+    double* sink;
+    cudaMalloc(&sink, 32 * sizeof(double));
+    for (int kind : {0, 1}) {
+      k_warp_argmax<<<1, 32>>>(kind, iters, d_out, sink);
+      k_warp_argmax<<<1, 32>>>(kind, iters, d_out, sink);
+      cudaDeviceSynchronize();
+      cudaMemcpy(&h, d_out, 8, cudaMemcpyDeviceToHost);
+      printf("{\"probe\": \"warp_argmax\", \"impl\": \"%s\", \"cycles\": %.1f}\n", kind ? "shfl_tree" : "redux",
+             (double)h / iters);
+    }
+    cudaFree(sink);
   }
   k_cta_rounds<<<64, 288>>>(iters, d_out);
   k_cta_rounds<<<64, 288>>>(iters, d_out);
