@@ -845,6 +845,17 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     S.xs[tid] = px;
     S.ys[tid] = py;
   }
+  // Alg. 2 line 1 sample positions of this sweep, drawn now (they depend only on the sweep,
+  // k and the superblock shape) by the warps after warp 0, which starts the tables; kept in
+  // S.f_node until the samples phase (the rook steps restage it afterwards)
+  int* smp = reinterpret_cast<int*>(S.f_node);
+  {
+    const uint64_t tag = 1ULL + (uint64_t)sweep;
+    for (int q = tid >= 32 ? tid - 32 : tid + T - 32; q < c.ns; q += T) {
+      smp[2 * q] = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
+      smp[2 * q + 1] = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
+    }
+  }
   const int rows_done = c.sbstate[job * 4 + 0], cols_done = c.sbstate[job * 4 + 1];
   const bool first = rows_done == 0 && cols_done == 0;
   __syncthreads();
@@ -985,12 +996,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     }
     // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically)
     {
-      const uint64_t tag = 1ULL + (uint64_t)sweep;
       double bv = -1.0;
       long long bf = LLONG_MAX;
       for (int q = tid; q < c.ns; q += T) {
-        const int sx = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
-        const int sy = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
+        const int sx = smp[2 * q], sy = smp[2 * q + 1];
         const int al = sx / n, a = sx - al * n;
         const int be = sy / n, b = sy - be * n;
         double e = sb_entry<FAMILY>(c, job, k, al, a, be, b);
@@ -1004,8 +1013,8 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       TRACE(7);
       argmax_step(&S, bv, bf, 1, 0);   // CTA-local: every CTA drew the same samples
       const int q = (int)S.best.idx;
-      xst = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q)) % (uint64_t)R);
-      yst = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
+      xst = smp[2 * q];
+      yst = smp[2 * q + 1];
       if (cr == 0 && tid == 0) {
         evals += c.ns;
         upd += (unsigned long long)c.ns * r;
