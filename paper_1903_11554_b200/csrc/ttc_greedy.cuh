@@ -797,7 +797,7 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
 // new pivot (if any) is written to the record Rn (slot r and rank); returns the new rank.
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
-                                          int rl, int rr, int* Rn, int& xstep) {
+                                          int rl, int rr, int* Rn, int& xstep, bool end_sync) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
@@ -1177,7 +1177,11 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
   }
   TRACE(40);
-  if (G > 1) cl.sync();  // no CTA may leave while another can still read its shared memory
+  // no CTA may leave while another can still read its shared memory; inside the persistent
+  // loop the next sweep's start barrier does this (nothing a CTA writes to its shared memory
+  // before that barrier is read remotely: the exchange slots alternate by step parity, S.pv
+  // is rewritten only in the next sweep's final phase)
+  if (G > 1 && end_sync) cl.sync();
   TRACE(41);
   phase(PH_END);
   if (timer) atomicAdd(&c.phase_ns[PH_LAUNCHES], 1ULL);
@@ -1214,7 +1218,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
-  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep);
+  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, true);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
     c.done[k] = sweep + 1;
@@ -1231,7 +1235,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
 template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
   __shared__ GreedySmem S;
-  __shared__ int s_abort, s_any;
+  __shared__ int s_abort[2];   // by sweep parity: one cluster barrier per sweep start
   extern __shared__ double dyn[];
   cg::cluster_group cl = cg::this_cluster();
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
@@ -1257,22 +1261,25 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         while (ld_acquire(&c.done[k + 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
         }
       if (abort) atomicOr(&c.flags[1], 1);
-      s_abort = abort;
+      s_abort[s & 1] = abort;
       if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) atomicAdd(&c.phase_ns[PH_START], gtimer() - w0);
     }
     TRACE(50);
     cl.sync();
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int i = 0; i < (int)cl.num_blocks(); ++i) any |= cl.map_shared_rank(&s_abort, i)[0];
-      s_any = any;
+    // every warp reads the cluster's abort flags (lane i: CTA i) -- no second barrier: slot
+    // s & 1 is rewritten two sweeps later, after this sweep's barriers
+    {
+      const int lane = threadIdx.x & 31;
+      const int mine = lane < (int)cl.num_blocks() ? cl.map_shared_rank(&s_abort[s & 1], lane)[0] : 0;
+      TRACE(51);
+      if (__any_sync(0xffffffffu, mine)) {   // (the same on every CTA of the cluster)
+        cl.sync();   // no CTA exits while another may still read its flags
+        break;
+      }
     }
-    cl.sync();  // s_abort may be rewritten only after every CTA has read it
-    TRACE(51);
-    if (s_any) break;
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
-    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep);
+    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, s + 1 == s0 + nsweeps);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
       c.rank_ring[k * 2 + (s & 1)] = r;
       st_release(&c.done[k], s + 1);  // the record writes above happen-before this release
