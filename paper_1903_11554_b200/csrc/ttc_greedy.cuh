@@ -120,19 +120,19 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride, int rl,
                                int rr) {
   const int k = c.kb + job, d = c.d, n = c.n;
-  const int* st = c.sbstate + job * 4;
   __shared__ ESum sS;
   __shared__ DDE sP;
   __shared__ double sX[64];   // node values of the frozen tuple's first 64 coordinates
   const int* T;
   int lo, hi;  // coordinate range of the frozen tuple
+  // (the callers pass only the slots that are new this sweep)
   if (side == 0) {
-    if (slot < st[0] || slot >= rl) return;
+    if (slot >= rl) return;
     T = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)slot * d : nullptr;
     lo = 0;
     hi = k;
   } else {
-    if (slot < st[1] || slot >= rr) return;
+    if (slot >= rr) return;
     T = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)slot * d : nullptr;
     lo = k + 2;
     hi = d;
@@ -154,8 +154,12 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
         const double ua = c.u[a * n + T[a]];
         for (int b = a + 1; b < hi; ++b) dde_mul_d(p, rho_ool(ua, c.u[b * n + T[b]]));
       }
+    // butterfly levels with offset >= the lanes holding data only combine identities (exact
+    // no-ops: +0, *1): skipped
+    const int act = min(32, hi - lo);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
+      if (o >= act) continue;
       s.h += __shfl_xor_sync(0xffffffffu, s.h, o);
       s.l += __shfl_xor_sync(0xffffffffu, s.l, o);
       DDE y;
@@ -202,10 +206,12 @@ __device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
   const int k = c.kb + job, d = c.d, n = c.n;
   const int lane = threadIdx.x & 31;
   DDE p = dde_one();
+  int act = 0;   // lanes holding a factor (the tree's levels beyond combine identities: skipped)
   if (k > 0 && k < d - 2) {
     const int* TX = rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d;
     const int* TY = rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d;
     const int nj = d - k - 2, np = k * nj;
+    act = min(32, np);
     for (int q = lane; q < np; q += 32) {
       const int i = q / nj, j = k + 2 + (q - i * nj);
       dde_mul_d(p, rho_ool(c.u[i * n + TX[i]], c.u[j * n + TY[j]]));
@@ -213,6 +219,7 @@ __device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
+    if (o >= act) continue;
     DDE y;
     y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
     y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
@@ -797,7 +804,8 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
 // new pivot (if any) is written to the record Rn (slot r and rank); returns the new rank.
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
-                                          int rl, int rr, int* Rn, int& xstep, bool end_sync) {
+                                          int rl, int rr, int* Rn, int& xstep, bool end_sync,
+                                          int rows_done, int cols_done, bool xy_known) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
@@ -839,7 +847,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       t_last = t;
     }
   };
-  if (tid < r) {
+  if (!xy_known && tid < r) {   // (the persistent loop keeps them in S.xs / S.ys: appended below)
     int px, py;
     pivot_pos(c, k, tid, px, py);
     S.xs[tid] = px;
@@ -856,7 +864,6 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       smp[2 * q + 1] = (int)(splitmix64(c.seed, draw_ctr(tag, d, k, 2 * q + 1)) % (uint64_t)C);
     }
   }
-  const int rows_done = c.sbstate[job * 4 + 0], cols_done = c.sbstate[job * 4 + 1];
   const bool first = rows_done == 0 && cols_done == 0;
   __syncthreads();
   TRACE(1);
@@ -1144,6 +1151,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   }
 
   phase(PH_FINAL);
+  if (added && tid == 0) {   // the new pivot's position, for the next sweep of a persistent loop
+    S.xs[r] = xst;
+    S.ys[r] = yst;
+  }
   if (cr == 0 && tid == 0) {
     if (added) {
       const int al = xst / n, a = xst - al * n, be = yst / n, b = yst - be * n;
@@ -1218,7 +1229,8 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
-  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, true);
+  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, true,
+                                            c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
     c.done[k] = sweep + 1;
@@ -1241,6 +1253,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   int* Rk = c.rec_cur + (long long)k * c.RS;
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
+  int rdone = c.sbstate[job * 4 + 0], cdone = c.sbstate[job * 4 + 1];
   int xstep = 0;
   TRACE_INIT();
   xbar_init(&S);  // ordered before remote use by the cluster barriers of the first sweep
@@ -1279,7 +1292,10 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     }
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
-    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, s + 1 == s0 + nsweeps);
+    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, s + 1 == s0 + nsweeps, rdone, cdone,
+                                   s > s0);
+    rdone = rl;   // (= the sbstate the sweep wrote)
+    cdone = rr;
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
       c.rank_ring[k * 2 + (s & 1)] = r;
       st_release(&c.done[k], s + 1);  // the record writes above happen-before this release
