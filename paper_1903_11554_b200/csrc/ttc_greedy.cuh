@@ -106,6 +106,52 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
   if (i == 0 && threadIdx.x == 0) c.flags[1] = 0;
 }
 
+// CX[alpha][beta] by one warp: lanes split the k * (d-k-2) cross pairs (i < k, j > k+1), each
+// lane a partial double-double product, then the shuffle tree -- the product is rounded once
+// later, so any grouping gives the same entries (DESIGN.md R3).  (A thread per entry ran the
+// whole chain alone: D_20's middle superblocks have ~80 pairs per entry, ~24k cycles.)
+__device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
+  const int k = c.kb + job, d = c.d, n = c.n;
+  const int lane = threadIdx.x & 31;
+  DDE p = dde_one();
+  int act = 0;   // lanes holding a factor (the tree's levels beyond combine identities: skipped)
+  if (k > 0 && k < d - 2) {
+    const int* TX = rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d;
+    const int* TY = rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d;
+    const int nj = d - k - 2, np = k * nj;
+    act = min(32, np);
+    for (int q = lane; q < np; q += 32) {
+      const int i = q / nj, j = k + 2 + (q - i * nj);
+      dde_mul_d(p, rho_ool(c.u[i * n + TX[i]], c.u[j * n + TY[j]]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    if (o >= act) continue;
+    DDE y;
+    y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
+    y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
+    y.e = __shfl_xor_sync(0xffffffffu, p.e, o);
+    y.pad = 0;
+    dde_mul(p, y);
+  }
+  if (lane == 0) c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
+}
+
+// this warp's share of the sweep's new CX pairs (new alpha x all beta, then old alpha x new
+// beta): warps 1.. of every CTA of the cluster, global warp index gw of nwg (warp 0 of each CTA
+// is busy with the frozen-tuple scalars of the side tables meanwhile)
+__device__ void sb_cx_share(const DevCtx& c, int job, int rows_done, int cols_done, int rl, int rr, int gw,
+                            int nwg) {
+  const int na = (rl - rows_done) * rr, nb = rows_done * (rr - cols_done);
+  for (int e = gw; e < na + nb; e += nwg) {   // (warp-uniform)
+    int al, be;
+    if (e < na) { al = rows_done + e / rr; be = e % rr; }
+    else { const int f = e - na; al = f / (rr - cols_done); be = cols_done + f % (rr - cols_done); }
+    sb_cx_table_warp(c, job, al, be);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // superblock factor tables (eq. (9)-(10) integrands split over the frozen parts)
 // ---------------------------------------------------------------------------------------
@@ -118,7 +164,7 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
 // blockIdx.z >= 2*jobs (family D): CX[alpha][beta] = prod_{i<k} prod_{j>k+1} rho(X_alpha,i, Y_beta,j)
 // for the new (alpha, beta) pairs, z = 2*jobs + job, y = alpha, x*128 + tid = beta.
 __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, int slot, int a0, int astride, int rl,
-                               int rr) {
+                               int rr, int cx_rows_done, int cx_cols_done, int cx_gw, int cx_nwg) {
   const int k = c.kb + job, d = c.d, n = c.n;
   __shared__ ESum sS;
   __shared__ DDE sP;
@@ -173,6 +219,8 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
       sS = s;
       sP = p;
     }
+  } else if (cx_nwg > 0) {   // family D, first new slot: the CX pairs overlap warp 0's scalars
+    sb_cx_share(c, job, cx_rows_done, cx_cols_done, rl, rr, cx_gw, cx_nwg);
   }
   __syncthreads();
   const long long o = ((long long)job * c.cap + slot) * n;
@@ -196,38 +244,6 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
       else { c.PB[o + a] = p; c.QR0[o + a] = q; }
     }
   }
-}
-
-// CX[alpha][beta] by one warp: lanes split the k * (d-k-2) cross pairs (i < k, j > k+1), each
-// lane a partial double-double product, then the shuffle tree -- the product is rounded once
-// later, so any grouping gives the same entries (DESIGN.md R3).  (A thread per entry ran the
-// whole chain alone: D_20's middle superblocks have ~80 pairs per entry, ~24k cycles.)
-__device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
-  const int k = c.kb + job, d = c.d, n = c.n;
-  const int lane = threadIdx.x & 31;
-  DDE p = dde_one();
-  int act = 0;   // lanes holding a factor (the tree's levels beyond combine identities: skipped)
-  if (k > 0 && k < d - 2) {
-    const int* TX = rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d;
-    const int* TY = rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d;
-    const int nj = d - k - 2, np = k * nj;
-    act = min(32, np);
-    for (int q = lane; q < np; q += 32) {
-      const int i = q / nj, j = k + 2 + (q - i * nj);
-      dde_mul_d(p, rho_ool(c.u[i * n + TX[i]], c.u[j * n + TY[j]]));
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    if (o >= act) continue;
-    DDE y;
-    y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
-    y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
-    y.e = __shfl_xor_sync(0xffffffffu, p.e, o);
-    y.pad = 0;
-    dde_mul(p, y);
-  }
-  if (lane == 0) c.CX[((long long)job * c.cap + al) * c.cap + be] = p;
 }
 
 // A_k(alpha, a; beta, b) from the tables (single rounding, R3)
@@ -877,27 +893,25 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     const int gl = G >= 2 ? G / 2 : 1;
     const bool do_l = G == 1 || cr < gl, do_r = G == 1 || cr >= gl;
     const int il = G == 1 ? 0 : cr, ir = G == 1 ? 0 : cr - gl;
+    // family D: the CX pairs of the new slots go to warps 1.. of every CTA, during the first
+    // side-table call (or on their own when this CTA has no new slot)
+    const int nwc = (T >> 5) - 1;
+    const int cx_gw = cr * nwc + (tid >> 5) - 1, cx_nwg = FAMILY == 1 ? G * nwc : 0;
+    bool cx_pending = FAMILY == 1;
     if (do_l)
       for (int slot = rows_done; slot < rl; ++slot) {
-        sb_side_tables(c, job, 0, slot, il * T, gl * T, rl, rr);
+        sb_side_tables(c, job, 0, slot, il * T, gl * T, rl, rr, rows_done, cols_done, cx_gw, cx_pending ? cx_nwg : 0);
+        cx_pending = false;
         __syncthreads();
       }
     if (do_r)
       for (int slot = cols_done; slot < rr; ++slot) {
-        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T, rl, rr);
+        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T, rl, rr, rows_done, cols_done, cx_gw,
+                       cx_pending ? cx_nwg : 0);
+        cx_pending = false;
         __syncthreads();
       }
-  }
-  if (FAMILY == 1) {
-    // CX for the new pairs: new alpha x all beta, then old alpha x new beta; a warp per pair
-    const int na = (rl - rows_done) * rr, nb = rows_done * (rr - cols_done);
-    const int nw = G * (T >> 5);
-    for (int e = cr * (T >> 5) + (tid >> 5); e < na + nb; e += nw) {   // (warp-uniform)
-      int al, be;
-      if (e < na) { al = rows_done + (int)(e / rr); be = (int)(e % rr); }
-      else { const int f = e - na; al = f / (rr - cols_done); be = cols_done + f % (rr - cols_done); }
-      sb_cx_table_warp(c, job, al, be);
-    }
+    if (cx_pending && tid >= 32) sb_cx_share(c, job, rows_done, cols_done, rl, rr, cx_gw, cx_nwg);
   }
   TRACE(2);
   cl.sync();  // tables visible to the whole cluster
