@@ -505,9 +505,21 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 // Layout: buf[stage][i][T] (conflict-free per warp).  Stage s = (row j, term block b), row-major.
 #define RING_P 4
 #define RING_MIN_ROWS 4   // rows per thread from which a step streams through the ring
+// L2 policy of the stream: the u/v factors of all superblocks exceed the
+// 126 MB L2 many times over (D_20 640 MB, C_200 840 MB), so no factor line survives in L2
+// until the superblock's next step anyway.  EVICT_FIRST loads them evict_first, so the stream
+// stops displacing the tables and records the steps reuse: C_200 -5.6%, but D_20 +1%
+// (profiles/r01n_l2_policy.log), so it is compiled in for the C family only.  (Keeping a
+// fraction of the lines with evict_last measured slower for every fraction tried, 0.15-0.5.)
+__device__ __forceinline__ void cp_async8_ef(void* smem, const void* gmem, unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
+}
+template <bool EVICT_FIRST>
 struct DotRing {
   double* buf;
   const double* F;
+  unsigned long long pol;   // L2 cache policy of the factor stream (EVICT_FIRST)
   int T, tid, tb, nb, sbn, r;
   int z0, total;          // first row of the thread, stages in all
   int is, irow, iblk;     // next stage to issue
@@ -515,6 +527,7 @@ struct DotRing {
   __device__ __forceinline__ void init(double* b, const double* f, int T_, int tid_, int tb_, int sbn_, int r_, int zb,
                                        int ze) {
     buf = b; F = f; T = T_; tid = tid_; tb = tb_; sbn = sbn_; r = r_;
+    if (EVICT_FIRST) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     nb = (r + tb - 1) / tb;
     z0 = zb + tid;
     const int rows = z0 < ze ? (ze - z0 + T - 1) / T : 0;
@@ -529,7 +542,10 @@ struct DotRing {
       const int t0 = iblk * tb, tn = min(tb, r - t0);
       const double* src = F + t0 * sbn + z0 + irow * T;
 #pragma unroll 1
-      for (int i = 0; i < tn; ++i) cp_async8(dst + i * T, src + i * sbn);
+      if (EVICT_FIRST)
+        for (int i = 0; i < tn; ++i) cp_async8_ef(dst + i * T, src + i * sbn, pol);
+      else
+        for (int i = 0; i < tn; ++i) cp_async8(dst + i * T, src + i * sbn);
       if (++iblk == nb) { iblk = 0; ++irow; }
     }
     ++is;
@@ -609,7 +625,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jrow = 0;
-  DotRing ring;
+  DotRing<FAMILY == 0> ring;
   const bool use_ring = !CACHED && xe - xb >= RING_MIN_ROWS * T;
   if (use_ring) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
   #pragma unroll 1
@@ -692,7 +708,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jcol = 0;
-  DotRing ring;
+  DotRing<FAMILY == 0> ring;
   const bool use_ring = !CACHED && ye - yb >= RING_MIN_ROWS * T;
   if (use_ring) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
   #pragma unroll 1
