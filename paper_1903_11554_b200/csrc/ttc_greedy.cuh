@@ -508,9 +508,9 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 // L2 policy of the stream: the u/v factors of all superblocks exceed the
 // 126 MB L2 many times over (D_20 640 MB, C_200 840 MB), so no factor line survives in L2
 // until the superblock's next step anyway.  EVICT_FIRST loads them evict_first, so the stream
-// stops displacing the tables and records the steps reuse: C_200 -5.6%, but D_20 +1%
-// (profiles/r01n_l2_policy.log), so it is compiled in for the C family only.  (Keeping a
-// fraction of the lines with evict_last measured slower for every fraction tried, 0.15-0.5.)
+// stops displacing the tables and records the steps reuse: C_200 -8%, D_20 -1%
+// (profiles/r01n_l2_policy.log); t-form families.  (Keeping a fraction of the lines with
+// evict_last measured slower for every fraction tried, 0.15-0.5.)
 __device__ __forceinline__ void cp_async8_ef(void* smem, const void* gmem, unsigned long long pol) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
@@ -541,7 +541,7 @@ struct DotRing {
       double* dst = buf + (is & (RING_P - 1)) * tb * T + tid;
       const int t0 = iblk * tb, tn = min(tb, r - t0);
       const double* src = F + t0 * sbn + z0 + irow * T;
-#pragma unroll 1
+      // (loops left to the compiler's unrolling: measured faster than unroll 1 on D_20)
       if (EVICT_FIRST)
         for (int i = 0; i < tn; ++i) cp_async8_ef(dst + i * T, src + i * sbn, pol);
       else
@@ -625,7 +625,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jrow = 0;
-  DotRing<FAMILY == 0> ring;
+  DotRing<FAMILY <= 1> ring;
   const bool use_ring = !CACHED && xe - xb >= RING_MIN_ROWS * T;
   if (use_ring) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
   #pragma unroll 1
@@ -708,7 +708,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   double bv = -1.0;
   long long bf = LLONG_MAX;
   int jcol = 0;
-  DotRing<FAMILY == 0> ring;
+  DotRing<FAMILY <= 1> ring;
   const bool use_ring = !CACHED && ye - yb >= RING_MIN_ROWS * T;
   if (use_ring) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
   #pragma unroll 1
