@@ -294,6 +294,9 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
+#ifndef EXT_ILP
+#define EXT_ILP 4   // raw entries per thread per iteration of the extension
+#endif
 
 template <int FAMILY>
 __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int side, int r, int x_lo, int x_hi,
@@ -345,36 +348,36 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
         else TS = nrow + 1;
       }
     }
-    // (1) raw entries of the tile, one per thread, two per iteration: the two independent
+    // (1) raw entries of the tile, one per thread, EXT_ILP per iteration: the independent
     // latency chains (table loads, double-double products, division) overlap
     {
-      auto raw_entry = [&](int e) {
+      const int ne = nrow * r, B = blockDim.x;
+      int e = threadIdx.x;
+#pragma unroll 1
+      for (; e + (EXT_ILP - 1) * B < ne; e += EXT_ILP * B) {
+        double v[EXT_ILP];
+        int at[EXT_ILP];
+#pragma unroll
+        for (int u = 0; u < EXT_ILP; ++u) {
+          const int eu = e + u * B;
+          const int s = eu / nrow, j = eu - s * nrow;
+          const int x = x0 + j;
+          const int al = x / n, a = x - al * n;
+          v[u] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                           : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+          at[u] = s * TS + j;
+        }
+#pragma unroll
+        for (int u = 0; u < EXT_ILP; ++u) tile[at[u]] = v[u];
+      }
+#pragma unroll 1
+      for (; e < ne; e += B) {
         const int s = e / nrow, j = e - s * nrow;
         const int x = x0 + j;
         const int al = x / n, a = x - al * n;
         tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
                                      : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
-      };
-      const int ne = nrow * r, B = blockDim.x;
-      int e = threadIdx.x;
-#pragma unroll 1
-      for (; e + B < ne; e += 2 * B) {
-        const int e1 = e + B;
-        const int s0 = e / nrow, j0 = e - s0 * nrow, s1 = e1 / nrow, j1 = e1 - s1 * nrow;
-        const int x0a = x0 + j0, x1a = x0 + j1;
-        const int al0 = x0a / n, a0 = x0a - al0 * n, al1 = x1a / n, a1 = x1a - al1 * n;
-        double v0, v1;
-        if (side == 0) {
-          v0 = sb_entry<FAMILY>(c, job, k, al0, a0, p_al[s0], p_a[s0]);
-          v1 = sb_entry<FAMILY>(c, job, k, al1, a1, p_al[s1], p_a[s1]);
-        } else {
-          v0 = sb_entry<FAMILY>(c, job, k, p_al[s0], p_a[s0], al0, a0);
-          v1 = sb_entry<FAMILY>(c, job, k, p_al[s1], p_a[s1], al1, a1);
-        }
-        tile[s0 * TS + j0] = v0;
-        tile[s1 * TS + j1] = v1;
       }
-      if (e < ne) raw_entry(e);
     }
     __syncthreads();
     clock_to(PH_EXT_RAW);

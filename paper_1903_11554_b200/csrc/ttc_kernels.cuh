@@ -497,17 +497,22 @@ __global__ void __launch_bounds__(256) k_solve(DevCtx c) {
   __syncthreads();
   for (int k = 0; k < r; ++k) {
     if (threadIdx.x < 32) {
+      // partial pivoting: first row of the largest |hi| (a warp argmax by REDUX: the bit
+      // pattern of a non-negative double orders like its value; rows with no candidate: none)
       double bv = -1.0;
       int bq = k;
       for (int q = k + threadIdx.x; q < r; q += 32) {
         const double v = fabs(A[perm[q] * cap + k].hi);
         if (v > bv) { bv = v; bq = q; }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-        if (ov > bv || (ov == bv && oq < bq)) { bv = ov; bq = oq; }
+      {
+        const bool has = bv >= 0.0;
+        const unsigned hi = has ? (unsigned)__double2hiint(bv) : 0u, lo = has ? (unsigned)__double2loint(bv) : 0u;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        const unsigned mq = __reduce_min_sync(0xffffffffu, (has && hi == mh && lo == ml) ? (unsigned)bq : 0xffffffffu);
+        bv = mq == 0xffffffffu ? -1.0 : __hiloint2double((int)mh, (int)ml);
+        bq = mq == 0xffffffffu ? k : (int)mq;
       }
       if (threadIdx.x == 0) {
         const int t = perm[k];
