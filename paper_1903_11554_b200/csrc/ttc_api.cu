@@ -58,6 +58,10 @@ struct ttc_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t ls = nullptr;          // launch stream: `stream`, or the capture stream while a graph is built
   cudaStream_t cap_stream = nullptr;  // private stream used to capture the solve graph
+  // quadrature branches that do not depend on each other (k_intersection, k_frozen_q) run on
+  // two side streams forked from / joined to ls by events -- concurrent branches of the graph
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int graph_sweeps = -1;
@@ -123,23 +127,42 @@ cudaEvent_t get_event(ttc_ctx* c) {
 struct Timed {
   ttc_ctx* c;
   int kid;
+  cudaStream_t s;
   cudaEvent_t a = nullptr;
-  Timed(ttc_ctx* c_, int kid_) : c(c_), kid(kid_) {
+  Timed(ttc_ctx* c_, int kid_, cudaStream_t s_ = nullptr) : c(c_), kid(kid_), s(s_ ? s_ : c_->ls) {
     c->launches++;
     c->klaunch[kid]++;
     if (c->timing) {
       a = get_event(c);
-      cudaEventRecord(a, c->ls);
+      cudaEventRecord(a, s);
     }
   }
   ~Timed() {
     if (c->timing) {
       cudaEvent_t b = get_event(c);
-      cudaEventRecord(b, c->ls);
+      cudaEventRecord(b, s);
       c->evs.push_back({a, b, kid});
     }
   }
 };
+
+// side stream i joins the work already issued on ls (fork) / ls waits for side stream i (join)
+int side_fork(ttc_ctx* c, int i) {
+  if (!c->side[i]) {
+    if (cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+      return fail(TTC_ERR_CUDA, "side stream / event creation failed");
+  }
+  if (cudaEventRecord(c->ev_fork[i], c->ls) != cudaSuccess || cudaStreamWaitEvent(c->side[i], c->ev_fork[i], 0) != cudaSuccess)
+    return fail(TTC_ERR_CUDA, "side stream fork failed");
+  return TTC_OK;
+}
+int side_join(ttc_ctx* c, int i) {
+  if (cudaEventRecord(c->ev_join[i], c->side[i]) != cudaSuccess || cudaStreamWaitEvent(c->ls, c->ev_join[i], 0) != cudaSuccess)
+    return fail(TTC_ERR_CUDA, "side stream join failed");
+  return TTC_OK;
+}
 
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -172,9 +195,12 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false
   }
   if (int e = check_launch("k_frozen_sides")) return e;
   if (dc.family == TTC_FAMILY_D) {
+    // k_frozen_q needs only the records: a concurrent branch (side stream 1), joined before
+    // the fiber kernel; k_frozen_lr follows k_frozen_sides on ls
+    if (int e = side_fork(c, 1)) return e;
     {
-      Timed t(c, K_FROZEN_Q);
-      k_frozen_q<<<dim3((n + 127) / 128, tup, 2 * njobs), 128, 0, c->ls>>>(dc, kind, jbase);
+      Timed t(c, K_FROZEN_Q, c->side[1]);
+      k_frozen_q<<<dim3((n + 127) / 128, tup, 2 * njobs), 128, 0, c->side[1]>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_q")) return e;
     {
@@ -182,6 +208,7 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false
       k_frozen_lr<<<dim3((tup + 63) / 64, tup, njobs), 64, 0, c->ls>>>(dc, kind, jbase);
     }
     if (int e = check_launch("k_frozen_lr")) return e;
+    if (int e = side_join(c, 1)) return e;
   }
   if (fused) {
     {
@@ -308,6 +335,16 @@ int do_integrate_local(ttc_ctx* c) {
   int m_lo = c->kb + 1, m_hi = c->ke;  // inclusive range
   if (rank == 0) m_lo = 0;
   const int nm = (c->n_owned > 0) ? (m_hi - m_lo + 1) : (rank == 0 ? 1 : 0);
+  // the intersection matrices need only the records: a concurrent branch (side stream 0)
+  // alongside the fibers, joined before k_solve
+  if (c->n_owned > 0) {
+    if (int e = side_fork(c, 0)) return e;
+    {
+      Timed t(c, K_INTERSECTION, c->side[0]);
+      k_intersection<<<dim3((cap + 63) / 64, cap, c->n_owned), 64, 0, c->side[0]>>>(dc, c->kb);
+    }
+    if (int e = check_launch("k_intersection")) return e;
+  }
   if (nm > 0) {
     const bool fused = dc.family < TTC_FAMILY_CX;
     if (int e = launch_fibers(c, JOB_INT, m_lo, nm, fused)) return e;
@@ -321,11 +358,7 @@ int do_integrate_local(ttc_ctx* c) {
   }
   CK(cudaMemsetAsync(dc.flags, 0, sizeof(int), c->ls));  // flags[1] (sweep timeout) stays
   if (c->n_owned > 0) {
-    {
-      Timed t(c, K_INTERSECTION);
-      k_intersection<<<dim3((cap + 63) / 64, cap, c->n_owned), 64, 0, c->ls>>>(dc, c->kb);
-    }
-    if (int e = check_launch("k_intersection")) return e;
+    if (int e = side_join(c, 0)) return e;
     {
       Timed t(c, K_SOLVE);
       // split the right-hand sides over 4 CTAs when the interfaces leave SMs idle
@@ -1069,6 +1102,11 @@ void tt_cross_destroy(ttc_ctx* c) {
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (c->side[i]) cudaStreamDestroy(c->side[i]);
+    if (c->ev_fork[i]) cudaEventDestroy(c->ev_fork[i]);
+    if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+  }
   for (void* p : c->allocs) cudaFree(p);
   if (c->out_host) cudaFreeHost(c->out_host);
   delete c;
