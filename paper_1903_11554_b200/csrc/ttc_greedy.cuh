@@ -486,6 +486,7 @@ struct GreedySmem {
   ESum fs;                           // SB[beta][b] (column step) or SA[alpha][a] (row step)
   DDE fp;                            // PB[beta][b] or PA[alpha][a]
   double pv;                         // E(x*, y*) of the final pivot (owner CTA of column y*)
+  double pa;                         // A(x*, y*) (CACHED: owner CTA of row x*)
 };
 
 // asynchronous global -> shared copies (LDGSTS): the whole cache fill is one round trip
@@ -837,10 +838,20 @@ __device__ __noinline__ void argmax_step(GreedySmem* S, double v, long long f, i
 // One Alg. 6 sweep of superblock `job` (all CTAs of its cluster): phases 1-3 with the ranks
 // r (own), rl / rr (neighbours, at the end of the previous sweep) given by the caller; the
 // new pivot (if any) is written to the record Rn (slot r and rank); returns the new rank.
+// release / acquire flags of the persistent sweep loop (global memory, gpu scope)
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
                                           int rl, int rr, int* Rn, int& xstep, bool end_sync,
-                                          int rows_done, int cols_done, bool xy_known) {
+                                          int rows_done, int cols_done, bool xy_known, bool release) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
   const int cr = (int)cl.block_rank();
@@ -990,6 +1001,33 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   int xst = 0, yst = 0;
   bool added = false;
   double raw_star = 0.0;
+  // the new pivot record (Alg. 6 line 4), the superblock state and -- persistent loop -- the
+  // rank ring and the release of done[k] for the neighbours, by thread 0 of CTA 0
+  auto publish = [&](bool add, double raw) {
+    if (cr != 0 || tid != 0) return;
+    if (add) {
+      const int al = xst / n, a = xst - al * n, be = yst / n, b = yst - be * n;
+      const int* TL = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d : nullptr;
+      const int* TR = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d : nullptr;
+      int* tup = Rn + 1 + (long long)r * d;
+      for (int q = 0; q < k; ++q) tup[q] = TL[q];
+      tup[k] = a;
+      tup[k + 1] = b;
+      for (int q = k + 2; q < d; ++q) tup[q] = TR[q];
+      int* par = Rn + 1 + (long long)cap * d + 2 * r;
+      par[0] = al;
+      par[1] = be;
+      Rn[0] = r + 1;
+      scale = fmax(scale, fabs(raw));
+    }
+    c.praw_max[job] = scale;
+    c.sbstate[job * 4 + 0] = rl;
+    c.sbstate[job * 4 + 1] = rr;
+    if (release) {
+      c.rank_ring[k * 2 + (sweep & 1)] = add ? r + 1 : r;
+      st_release(&c.done[k], sweep + 1);  // the record writes above happen-before this release
+    }
+  };
   const bool stage_n = n <= STAGE_N;
 
   if (active) {
@@ -1158,55 +1196,39 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         stage = 0;
       }
     }
+    // the pivot value E(x*, y*) from the shared memory of the CTA owning column y* (cached:
+    // also A(x*, y*) from the owner of row x*), read through DSMEM after the barrier
+    const int own = (int)(yst / cpc);
+    if (cr == own && tid == 0) S.pv = CACHED ? Erow[yst - yb] : V[r * sbn + yst];
+    if (CACHED && cr == (int)(xst / rpc) && tid == 0) S.pa = Acol[xst - xb];
+    TRACE(8);
+    if (G > 1) cl.sync();  // S.pv, S.pa (non-cached: U[r][:], V[r][:], Araw) visible cluster-wide
+    else __syncthreads();
+    TRACE(9);
+    const double pv = G > 1 ? cl.map_shared_rank(&S.pv, own)[0] : S.pv;
+    raw_star = CACHED ? (G > 1 ? cl.map_shared_rank(&S.pa, (int)(xst / rpc))[0] : S.pa) : Araw[xst];
+    added = fabs(pv) > c.tol * scale;
+    // publish first (the neighbours wait for it), then the copy-out / rescale of v_r
+    publish(added, raw_star);
     if (CACHED) {   // the final column / row leave the chip once
       for (int x = xb + tid; x < xe; x += T) {
         U[r * sbn + x] = Ecol[x - xb];
         Araw[x] = Acol[x - xb];
       }
 #pragma unroll 1
-      for (int y = yb + tid; y < ye; y += T) V[r * sbn + y] = Erow[y - yb];
-    }
-    // the pivot value E(x*, y*) is read from the shared memory of the CTA owning column y*,
-    // not from V[r][y*]: that CTA rescales V[r][:] in place right after the barrier
-    const int own = (int)(yst / cpc);
-    if (cr == own && tid == 0) S.pv = CACHED ? Erow[yst - yb] : V[r * sbn + yst];
-    TRACE(8);
-    if (G > 1) cl.sync();  // U[r][:], V[r][:], Araw, S.pv visible to the whole cluster
-    else __syncthreads();
-    TRACE(9);
-    const double pv = G > 1 ? cl.map_shared_rank(&S.pv, own)[0] : S.pv;
-    raw_star = Araw[xst];
-    if (fabs(pv) > c.tol * scale) {
-      added = true;
+      for (int y = yb + tid; y < ye; y += T) V[r * sbn + y] = added ? __ddiv_rn(Erow[y - yb], pv) : Erow[y - yb];
+    } else if (added) {
 #pragma unroll 1
       for (int y = yb + tid; y < ye; y += T) V[r * sbn + y] = __ddiv_rn(V[r * sbn + y], pv);
     }
+  } else {
+    publish(false, 0.0);
   }
 
   phase(PH_FINAL);
   if (added && tid == 0) {   // the new pivot's position, for the next sweep of a persistent loop
     S.xs[r] = xst;
     S.ys[r] = yst;
-  }
-  if (cr == 0 && tid == 0) {
-    if (added) {
-      const int al = xst / n, a = xst - al * n, be = yst / n, b = yst - be * n;
-      const int* TL = k > 0 ? rec_piv(c.rec_cur, c.RS, k - 1) + (long long)al * d : nullptr;
-      const int* TR = k < d - 2 ? rec_piv(c.rec_cur, c.RS, k + 1) + (long long)be * d : nullptr;
-      int* tup = Rn + 1 + (long long)r * d;
-      for (int q = 0; q < k; ++q) tup[q] = TL[q];
-      tup[k] = a;
-      tup[k + 1] = b;
-      for (int q = k + 2; q < d; ++q) tup[q] = TR[q];
-      int* par = Rn + 1 + (long long)cap * d + 2 * r;
-      par[0] = al;
-      par[1] = be;
-      Rn[0] = r + 1;
-      scale = fmax(scale, fabs(raw_star));
-    }
-    c.praw_max[job] = scale;
-    c.sbstate[job * 4 + 0] = rl;
-    c.sbstate[job * 4 + 1] = rr;
   }
   if (c.counters && tid == 0) {
     evals += ext_ent;
@@ -1234,14 +1256,6 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
 
 // neighbour ranks published at the end of each sweep (a ring of two: a neighbour can be at
 // most one sweep ahead) and the sweeps each superblock has completed
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // single sweep (any world size): ranks from the current records, the updated record goes to
 // rec_next (the multi-process exchange buffer)
@@ -1263,7 +1277,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
   const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, true,
-                                            c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false);
+                                            c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false, false);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
     c.done[k] = sweep + 1;
@@ -1325,14 +1339,11 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     }
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
+    // (sweep_body publishes rank_ring[k] and releases done[k] as soon as the pivot is known)
     r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, s + 1 == s0 + nsweeps, rdone, cdone,
-                                   s > s0);
+                                   s > s0, true);
     rdone = rl;   // (= the sbstate the sweep wrote)
     cdone = rr;
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-      c.rank_ring[k * 2 + (s & 1)] = r;
-      st_release(&c.done[k], s + 1);  // the record writes above happen-before this release
-    }
   }
   TRACE_FLUSH();
 }
