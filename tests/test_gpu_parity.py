@@ -321,3 +321,30 @@ def test_perturbed_timing_same_pivots(lib):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_trace_build.py"), "C10", "D5"],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("name", ["D5", "C10"])
+def test_fiber_kernel_cluster_splits_agree(lib, name, monkeypatch):
+    """The quadrature fiber kernel splits each tile's nodes over a (1, NS, 1) cluster and adds
+    the partial double-double sums through DSMEM in range order: every split (NS = 1, 2, 4, 8,
+    forced with TTC_FW_NS) gives the same integral to double-double rounding, and the oracle's
+    within the parity bar."""
+    from paper_1903_11554_b200 import TTCross
+    wl = WORKLOADS[name]
+    u, w = wl.grid()
+    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed)
+    st = X.initial_state(prob)
+    for _ in range(wl.alg6_sweeps):
+        st = X.sweep(prob, st)
+    ref, *_ = X.integrate_exact(prob, st)
+    vals = []
+    for ns in ("1", "2", "4", "8"):
+        monkeypatch.setenv("TTC_FW_NS", ns)
+        tt = TTCross(wl.family, u, w, wl.rank_cap, wl.tol, n_samples=wl.n_samples, rook_iters=wl.rook_iters,
+                     seed=wl.seed)
+        tt.sweep(wl.alg6_sweeps)
+        vals.append(tt.integrate()[0])
+        tt.close()
+    for v in vals:
+        assert abs(v - vals[0]) <= 1e-14 * abs(vals[0]), vals
+        assert abs(v - ref) <= INT_RTOL * abs(ref), (v, ref)
