@@ -44,10 +44,26 @@ from workloads import FAMILY_NAMES, WORKLOADS, X_FAMILIES, X_WORKLOADS  # noqa: 
 
 ALL_WORKLOADS = {**WORKLOADS, **X_WORKLOADS}
 
-DEFAULT_WORKLOAD = "D5"   # BASELINE.json configs[1]
+DEFAULT_WORKLOAD = "D20"   # BASELINE.json configs[3]: the largest single-GPU config
 L2_FLUSH_BYTES = 256 << 20
-# fp64 peak: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz (max SM clock)
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# fp64 peak: MEASURED on this pool's B200 by tools/fp64_peak.cu (DFMA chains
+# on every SM, CUDA events; profiles/fp64_peak.json), else the nominal 148 SMs x 64 FP64 FMA
+# lanes x 2 flop x 1.965 GHz
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def fp64_peak(mode="burst"):
+    """(TFLOP/s, source): the measured DFMA throughput ('burst': a kernel timed alone;
+    'sustained': back to back for seconds), or the nominal figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            e = json.load(f)
+        return float(e[f"dfma_{mode}_tflops"]), f"measured DFMA {mode} (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return FP64_NOMINAL_TFLOPS, "nominal: 148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz (no measurement committed)"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
 
 
 def parse():
@@ -135,25 +151,32 @@ def flops_per_entry(family, m):
     return {2: 4 * m + 2, 3: 4 * m + 3 + pairs, 4: pairs}[family]
 
 
+# algorithmic fp64 flops per entry of the fused quadrature fiber kernel, an
+# FMA counted as 2 and an IEEE division or reciprocal as 1:  rounding of the exact sum S (2),
+# S*S (1);  D only: two double-double products (10 each: p, err FMA, two FMAs, s, l), hi+lo
+# (1), the division (1);  C: the reciprocal (1);  the double-double accumulation of w_a*A
+# (14: product + error FMA, two-sum, renormalisation).  C 18, D 39.  (ncu's executed fp64
+# operations are higher -- C 27.2, D 53.3 per entry, profiles/r01n_ncu_fiber_wsum_*_flops.csv
+# -- because the IEEE division expands into a reciprocal and Newton steps.)
+FIBER_FLOPS_PER_ENTRY = {0: 18, 1: 39}
+
+
 def fiber_roofline(kt, stats, family, modes, peaks):
     """The quadrature fiber kernel: the throughput-mode batched integrand evaluation.
-    t-form (k_fiber_wsum, fused with the weighted sum, nothing written per entry): fp64 flops
-    per entry as executed, DADD + DMUL + 2 DFMA from ncu's sass op counters (C 27.2 on C_200,
-    D 53.3 on D_20: profiles/r01n_ncu_fiber_wsum_*_flops.csv) -- the exact-limb sum and its
-    rounding, the double-double products, the IEEE division (reciprocal + Newton steps) and
-    the double-double accumulation of w_a * A; x-form (k_fiber_x, 8 B written per entry):
-    flops_per_entry."""
+    t-form (k_fiber_wsum, fused with the weighted sum, nothing written per entry):
+    FIBER_FLOPS_PER_ENTRY; x-form (k_fiber_x, 8 B written per entry): flops_per_entry."""
     launches, ms = kt.get("k_fiber", (0, 0.0))
     if not launches or ms <= 0:
         return None
     avg_s = ms / launches / 1e3
     ent = stats["fiber_entries"] / launches
     fused = family in (0, 1)
-    fpe = {0: 27.2, 1: 53.3}[family] if fused else flops_per_entry(family, modes)
+    fpe = FIBER_FLOPS_PER_ENTRY[family] if fused else flops_per_entry(family, modes)
     tf = ent * fpe / avg_s / 1e12
     gbs = 0.0 if fused else ent * 8 / avg_s / 1e9
     return {"kernel": "k_fiber_wsum" if fused else "k_fiber_x", "avg_us": avg_s * 1e6, "entries_per_launch": ent,
-            "achieved_tflops": tf, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS,
+            "achieved_tflops": tf, "frac_fp64_peak": tf / FP64_PEAK_TFLOPS, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+            "fp64_peak_source": FP64_PEAK_SOURCE,
             "write_GBs": gbs, "frac_hbm": gbs / peaks["hbm_gbs"],
             "per_unit": f"{fpe} flop / entry" + ("" if fused else " + 8 B written")}
 
@@ -200,7 +223,7 @@ def roofline(kt, stats, family, peaks, peak_src, modes=0, workload=None, cached=
     alu = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
            "frac": tf / FP64_PEAK_TFLOPS,
            "per_unit": f"{fpe} fp64 flop/entry + 2 flop/update term",
-           "peak_source": "derived fp64 FMA peak: 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §6)"}
+           "peak_source": FP64_PEAK_SOURCE}
     out.update({"entries_per_launch": ent, "updates_per_launch": upd})
     if name == "k_sweep" and not cached:
         # memory side: every u_t(x) v_t(y) term streams one factor (the other is staged),
@@ -222,44 +245,84 @@ def roofline(kt, stats, family, peaks, peak_src, modes=0, workload=None, cached=
 # --------------------------------------------------------------------------------------
 # oracle leg (cpu_baseline and --impl reference)
 # --------------------------------------------------------------------------------------
-def oracle_sample(wl, budget_s):
-    """Run the oracle on a bounded sample of the workload; returns (evals, seconds, what).
+_ORACLE_PROB = None
 
-    Small workloads (a whole solve fits a few seconds): whole solves (init + sweeps +
-    quadrature), repeated while the budget lasts.  Large ones: sweeps from the rank-1 start,
-    superblock by superblock (each = LU of the existing cross + one Alg. 2 step), stopped
-    when the budget is spent.
-    """
-    from threadpoolctl import threadpool_limits
+
+def _oracle_init(name):
+    global _ORACLE_PROB
     from oracle import cross as X
+    wl = ALL_WORKLOADS[name]
     u, w = wl.grid()
-    prob = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed, wl.fold)
+    _ORACLE_PROB = X.Problem(wl.family, u, w, wl.rank_cap, wl.tol, wl.n_samples, wl.rook_iters, wl.seed, wl.fold)
+
+
+def _oracle_solve(nsw):
+    from oracle import cross as X
+    st, val, _ = X.run(_ORACLE_PROB, nsw)
+    return st.n_evals
+
+
+def _oracle_update(args):
+    from oracle import cross as X
+    st, k = args
+    piv, par, info = X.superblock_update(_ORACLE_PROB, st, k)
+    return k, piv, par, info["evals"]
+
+
+def oracle_sample(wl, budget_s, cores=None):
+    """Run the oracle (test infrastructure, as it stands) on a bounded sample of the workload
+    on `cores` host processes (numpy, one thread each); returns (evals, seconds, what, cores,
+    solve_s or None).
+
+    Small workloads (a whole solve takes ~1 s on one core): whole solves, one per process,
+    repeated while the budget lasts.  Large ones: Alg. 6 sweeps from the rank-1 start, the
+    superblock updates of a sweep spread over the processes (each = LU of the existing
+    cross + one Alg. 2 step, Alg. 6), stopped after the sweep in
+    which the budget runs out.
+    """
+    import multiprocessing as mp
+    from oracle import cross as X
+    cores = cores or os.cpu_count() or 1
+    _oracle_init(wl.name)
+    prob = _ORACLE_PROB
     nsw = wl.alg6_sweeps
     evals, t0 = 0, time.perf_counter()
-    with threadpool_limits(1):
-        if wl.d <= 8 and budget_s >= 1.5:   # a whole solve of these takes ~1 s on one core
-            solves = 0
-            while True:
-                st, val, _ = X.run(prob, nsw)
-                evals += st.n_evals
-                solves += 1
-                if time.perf_counter() - t0 > budget_s:
-                    break
-            return evals, time.perf_counter() - t0, f"{solves} full solve(s) ({nsw} Alg. 6 sweeps + quadrature)"
-        st = X.initial_state(prob)
-        done = 0
-        while time.perf_counter() - t0 <= budget_s:
-            new = st.copy()
-            for k in range(wl.d - 1):
-                piv, par, info = X.superblock_update(prob, st, k)
-                new.piv[k], new.par[k] = piv, par
-                evals += info["evals"]
-                done += 1
-                if time.perf_counter() - t0 > budget_s:
-                    break
-            new.sweep = st.sweep + 1
-            st = new
-        return evals, time.perf_counter() - t0, f"{done} superblock update(s) from the rank-1 start"
+    env = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env:
+        os.environ[k] = "1"
+    try:
+        with mp.get_context("fork").Pool(cores, initializer=_oracle_init, initargs=(wl.name,)) as pool:
+            t0 = time.perf_counter()
+            if wl.d <= 8:
+                solves = 0
+                while True:
+                    for e in pool.imap_unordered(_oracle_solve, [nsw] * cores):
+                        evals += e
+                        solves += 1
+                    if time.perf_counter() - t0 > budget_s:
+                        break
+                s = time.perf_counter() - t0
+                return (evals, s, f"{solves} full solve(s) ({nsw} Alg. 6 sweeps + quadrature), {cores} at a time",
+                        cores, s / solves * cores)
+            st = X.initial_state(prob)
+            sweeps = 0
+            while time.perf_counter() - t0 <= budget_s and sweeps < nsw:
+                new = st.copy()
+                for k, piv, par, ev in pool.imap_unordered(_oracle_update, [(st, k) for k in range(wl.d - 1)]):
+                    new.piv[k], new.par[k] = piv, par
+                    evals += ev
+                new.sweep = st.sweep + 1
+                st = new
+                sweeps += 1
+            return (evals, time.perf_counter() - t0,
+                    f"the first {sweeps} Alg. 6 sweeps from the rank-1 start (ranks up to {max(st.ranks)}), "
+                    f"superblocks spread over {cores} processes", cores, None)
+    finally:
+        for k, v in env.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def run_reference(args):
@@ -270,9 +333,9 @@ def run_reference(args):
     budget = max(0.5, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(wl, budget)
-    tot_e, tot_s, what = 0, 0.0, ""
+    tot_e, tot_s, what, cores = 0, 0.0, "", 1
     for _ in range(args.steps):
-        e, s, what = oracle_sample(wl, budget)
+        e, s, what, cores, _ = oracle_sample(wl, budget)
         tot_e += e
         tot_s += s
     v = tot_e / tot_s
@@ -281,8 +344,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(wl, args.gpus),
-        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": 1, "kind": "oracle",
-                         "sample": f"per step: {what} of {wl.name} (numpy fp64, 1 thread)"},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                         "sample": f"per step: {what} of {wl.name} (numpy fp64, one thread per process)"},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -300,11 +363,41 @@ def workload_config(wl, n):
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
+def spawn_ranks(args):
+    """--gpus N > 1 without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and pass their output through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def nccl_summary(path_glob):
+    """One stderr line from the NCCL_DEBUG=INFO logs of this job: communicator ranks, channels,
+    whether NVLS (in-switch reduction) was set up."""
+    import glob
+    lines = []
+    for p in glob.glob(path_glob):
+        with open(p, errors="replace") as f:
+            lines += f.readlines()
+    nvls = any("NVLS" in ln for ln in lines)
+    ranks = sorted({ln.split("rank ")[1].split()[0] for ln in lines if "Init COMPLETE" in ln and "rank " in ln})
+    chans = sum(1 for ln in lines if "via P2P" in ln or "via NVLS" in ln)
+    print(f"[bench] NCCL: {len(lines)} log lines, comm ranks {ranks}, {chans} P2P/NVLS channel lines, "
+          f"NVLS {'seen' if nvls else 'not seen'} ({path_glob})", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -315,7 +408,12 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
+        # communicator ranks / channels / NVLS visible without polluting stdout (the JSON line)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        nccl_log = os.path.join(tempfile.gettempdir(), f"ttc_nccl_{os.environ.get('MASTER_PORT', '0')}")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log + ".%h.%p.log")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_1903_11554_b200 import TTCross
@@ -448,9 +546,10 @@ def main():
     # ---- oracle on the host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        e, s, what = oracle_sample(wl, args.cpu_seconds)
-        cpu = {"value": e / s, "unit": "evals/s", "cores": 1, "kind": "oracle",
-               "sample": f"{what} of {wl.name} (numpy fp64, 1 thread), {s:.1f} s"}
+        e, s, what, cores, solve_s = oracle_sample(wl, args.cpu_seconds)
+        cpu = {"value": e / s, "unit": "evals/s", "cores": cores, "kind": "oracle",
+               "sample": f"{what} of {wl.name} (numpy fp64, one thread per process), {s:.1f} s",
+               "solve_s_per_core": solve_s}
 
     if rank == 0:
         line = {
@@ -468,6 +567,8 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+        if rank == 0 and nccl_log:
+            nccl_summary(nccl_log + ".*.log")
     core.close()
 
 

@@ -84,19 +84,23 @@ typedef struct ttc_stats {
   int64_t rook_steps;      /* column+row rounds of the rook searches                        */
   int64_t ext_entries;     /* ... of which by the u/v extension phase (batched fibers)      */
   int64_t ext_updates;     /* multiply-subtract terms of the extension phase                */
+  int64_t ring_steps;      /* (CTA, rook step) pairs that streamed the u/v factors from HBM
+                              through the shared-memory ring (the non-cached launch shape)  */
 } ttc_stats;
 
 /*
  * tt_cross_init -- create a context, upload the grid, precompute the per-node tables and draw
- * the seed-fixed rank-1 start (R5; 64 entry evaluations, part of loading the
- * problem -- not counted in the per-solve statistics, which tt_cross_reset zeroes).
+ * the seed-fixed rank-1 start (R5; 64 entry evaluations, redrawn by every reset /
+ * solve -- not counted in the per-solve statistics, which tt_cross_reset zeroes).
  *   out      : receives the context (owned by the caller; free with tt_cross_destroy)
  *   cfg      : problem configuration (copied)
  *   nodes_u  : d*n doubles, row-major [mode][node], > 0: u-nodes (u = e^t, R1) for
  *              the t-form families, x-nodes in (0,1) for the x-form families
  *   weights  : d*n doubles, quadrature weights [mode][node]
  *   mem_kind : TTC_MEM_HOST (pageable/pinned host arrays, copied H2D on `stream`) or
- *              TTC_MEM_DEVICE (device arrays, copied D2D)
+ *              TTC_MEM_DEVICE (device arrays, copied D2D).  The copies are asynchronous:
+ *              the caller keeps nodes_u / weights alive and unmodified until the stream
+ *              has completed them (any synchronising call of this library does that).
  *   stream   : cudaStream_t to issue all work on (may be NULL)
  * Errors: TTC_ERR_ARG for out-of-range sizes or non-positive host nodes, TTC_ERR_CUDA.
  */
@@ -111,8 +115,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u,
  */
 int tt_cross_load_grid(ttc_ctx* ctx, const double* nodes_u, const double* weights, int32_t mem_kind);
 
-/* tt_cross_reset -- restore the rank-1 start of the loaded grid (device kernel, asynchronous)
- * and zero the statistics.  Lets a benchmark time repeated solves from the same seed. */
+/* tt_cross_reset -- draw the rank-1 start of the loaded grid again (k_init_pivot: first argmax
+ * |A| over the seeded samples) and reset every interface to it (device kernels, asynchronous),
+ * zero the statistics.  Lets a benchmark time repeated whole solves from the same seed. */
 int tt_cross_reset(ttc_ctx* ctx);
 
 /*
@@ -124,7 +129,9 @@ int tt_cross_reset(ttc_ctx* ctx);
  * starts sweep s as soon as superblocks k-1 and k+1 have published sweep s-1 (the
  * neighbour-only exchange of Alg. 6 lines 6-8, through release/acquire flags); otherwise one
  * launch per sweep.  Results are identical either way.  A neighbour wait longer than ~2 s
- * (clusters not co-resident) is reported by the next tt_integrate* as TTC_ERR_CUDA.
+ * (clusters not co-resident, e.g. under MPS or beside concurrent kernels) abandons the launch
+ * and is reported as TTC_ERR_CUDA by the next synchronising call (tt_integrate*,
+ * tt_cross_get_state, tt_cross_get_stats); the cross is then incomplete.
  * Fully asynchronous on the context stream.
  */
 int tt_cross_sweep(ttc_ctx* ctx, int32_t n_sweeps);
@@ -138,13 +145,15 @@ int tt_cross_sweep_local(ttc_ctx* ctx);
 int tt_cross_commit(ttc_ctx* ctx);
 
 /*
- * tt_cross_exchange_buffer -- device pointer of the "next" record buffer: world*chunk
- * records of (1 + rank_cap*d + 2*rank_cap) int32 (record k = [r_k, PIV[k][0..cap)[0..d),
- * PAR[k][0..cap)[0..2)]), where chunk = ceil((d-1)/world) interfaces are owned by each rank,
- * rank p owning records [p*chunk, (p+1)*chunk).  *bytes_per_rank = chunk*(1+cap*d+2*cap)*4.
- * An in-place all-gather of this buffer completes a sweep (Alg. 6 lines 6-8).
- * For world > 1 the buffer stays at the same address for the life of the context
- * (tt_cross_commit copies it into the current records); for world == 1 commit swaps the
+ * tt_cross_exchange_buffer -- device pointer of the exchange buffer of one sweep.  A record is
+ * (1 + rank_cap*d + 2*rank_cap) int32: [r_k, PIV[k][0..cap)[0..d), PAR[k][0..cap)[0..2)].
+ * Interfaces are partitioned in balanced contiguous blocks (Alg. 6 line 1): with
+ * q = (d-1) / world, m = (d-1) % world, rank p owns [kb_p, kb_{p+1}), kb_p = p*q + min(p, m).
+ * world > 1: world slots of chunk = ceil((d-1)/world) records; tt_cross_sweep_local writes
+ * this rank's records of [kb_p, kb_{p+1}) to the start of slot p; an in-place all-gather of
+ * the slots (*bytes_per_rank = chunk*record bytes) followed by tt_cross_commit completes the
+ * sweep (Alg. 6 lines 6-8).  The buffer stays at the same address for the life of the context.
+ * world == 1: the "next" records of all d-1 interfaces (no exchange needed); commit swaps the
  * two record buffers, so re-query the pointer after every commit.
  */
 int tt_cross_exchange_buffer(ttc_ctx* ctx, void** dev_ptr, int64_t* bytes_total,
@@ -199,7 +208,9 @@ int tt_integrate_finish(ttc_ctx* ctx, double* value, double* log10_abs, int32_t*
  *   tt_cross_get_state : ranks_out[d-1]; piv_out[(d-1)*rank_cap*d] (slots >= r_k are -1);
  *                        par_out[(d-1)*rank_cap*2] (may be NULL)
  *   tt_cross_get_fiber : fiber A(I_{<=m-1}, i_m, I_{>m}) of mode m of the current cross,
- *                        evaluated on demand (the same entries the quadrature contracts),
+ *                        evaluated on demand by the quadrature's own fiber kernel
+ *                        (k_fiber_wsum storing the entries it contracts; it also refreshes
+ *                        W_m, see tt_cross_get_wsum),
  *                        out[rx*ry*n] as [alpha][beta][a]; capacity in doubles; out NULL:
  *                        only rx, ry.  TTC_ERR_STATE while a local sweep is uncommitted.
  *   tt_cross_get_stats : counters and (if enabled) device times.
@@ -208,6 +219,18 @@ int tt_cross_get_state(ttc_ctx* ctx, int32_t* ranks_out, int32_t* piv_out, int32
 int tt_cross_get_fiber(ttc_ctx* ctx, int32_t mode, double* out, int64_t capacity,
                        int32_t* rx, int32_t* ry);
 int tt_cross_get_stats(ttc_ctx* ctx, ttc_stats* out);
+
+/*
+ * tt_cross_get_wsum -- the weighted fiber sums W_m[alpha][beta] = sum_a w_{m,a}
+ * A(I_{<=m-1}[alpha], a, I_{>m}[beta]) (§4.1) of mode m as the last
+ * tt_integrate / tt_integrate_local / tt_cross_get_fiber of this context computed them, in
+ * double-double: hi_out[rx*ry], lo_out[rx*ry] row-major [alpha][beta] (value = hi + lo).
+ * capacity in doubles per array; hi_out NULL: only rx, ry.  Synchronises the stream.
+ * Only modes this rank contracts are defined (world > 1: modes kb+1..ke, and 0 on rank 0).
+ * Errors: TTC_ERR_ARG (mode out of range, buffer too small), TTC_ERR_STATE (pending sweep).
+ */
+int tt_cross_get_wsum(ttc_ctx* ctx, int32_t mode, double* hi_out, double* lo_out, int64_t capacity,
+                      int32_t* rx, int32_t* ry);
 
 /* tt_cross_get_kernel_time -- per-kernel launch count and accumulated device time (ms,
  * timing enabled) since the last reset, for kernel id kid in [0, 13): 0 k_prep_nodes,

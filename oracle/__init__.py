@@ -15,9 +15,11 @@ Modules
                 configs in the (4/d!) t-form), the per-entry definition of the tensor A,
                 full-grid brute force (§4.1 eq. (5)).
   cross      -- counter-based initial pivots, fibers A(I_{<=k-1}, i_k, I_{>k}), the
-                rank-revealing cross (complete pivoting, §2.4) + maxvol swaps
-                (Alg. 1), the dimension-parallel half-sweeps (Alg. 6 / §3.4 relaxation),
-                and the TT quadrature (§4.1 product of (2d-1) matrices).
+                greedy pivot search of Alg. 2 (random samples, then rook search on the
+                cross error), the dimension-parallel sweeps of
+                Alg. 6 (every superblock appends at most one pivot per sweep from the index
+                sets of the previous sweep, lines 624-641), and the TT quadrature (§4.1
+                product of (2d-1) matrices, lines 689-693).
 
 Parity status: every function is pinned by ``tests/test_oracle_*.py`` against closed
 forms, brute force, mpmath or determinant/volume identities (DESIGN.md §"Oracle pins").

@@ -250,6 +250,7 @@ def superblock_update(prob: Problem, st: State, k: int):
         e[np.isin(sx, xs) | np.isin(sy, ys)] = 0.0
         q = int(np.argmax(np.abs(e)))
         xst, yst = int(sx[q]), int(sy[q])
+        start = (xst, yst)
         # Alg. 2 lines 2-5: rook search -- column partial pivoting, then row partial pivoting,
         # until the row step keeps the column (rook condition eq. (2)) or the budget is spent
         c_at = g_at = -1
@@ -278,7 +279,8 @@ def superblock_update(prob: Problem, st: State, k: int):
         new_t.append(sb.tuples(np.array([xst]), np.array([yst]))[0])
         new_p.append((xst // n, yst // n))
         info["added"] += 1
-        info["adds"].append({"x": xst, "y": yst, "pivot": float(pv), "converged": bool(c_at == yst and g_at == xst),
+        info["adds"].append({"x": xst, "y": yst, "start": start, "pivot": float(pv),
+                             "converged": bool(c_at == yst and g_at == xst),
                              "xs_before": list(xs[:-1]), "ys_before": list(ys[:-1])})
         break
     info["evals"] = sb.evals

@@ -12,7 +12,8 @@ Definitions (readings R1-R3):
   tests/test_oracle_integrand.py pins the two forms against each other.
 
 * The tensor whose TT cross is built is the raw integrand on the grid (no weights folded,
-  PAPER.md §4.1; the folded variant of lines 701-706 is out of scope):
+  PAPER.md §4.1; the folded variant of lines 701-706 is offered for the
+  x-form families only, oracle.cross.Problem(fold=True), R2):
       A(i_1..i_d) = f(u_{1,i_1}, ..., u_{d,i_d}),   f = P / S^2,
       S = sum_j (u_j + 1/u_j),      P = prod_{i<j} rho(u_i, u_j)  (P = 1 for family C),
       rho(x, y) = q*q,  q = (max(x,y) - min(x,y)) / (max(x,y) + min(x,y)).

@@ -30,7 +30,7 @@ EXPORTS = [
     "tt_integrate_read", "tt_integrate_local", "tt_integrate_partials_buffer", "tt_integrate_finish",
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
     "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info", "tt_cross_get_launch_shape",
-    "tt_cross_get_phase_times", "tt_selftest_division",
+    "tt_cross_get_phase_times", "tt_selftest_division", "tt_cross_get_wsum",
 ]
 N_KERNELS = 13
 
@@ -50,7 +50,7 @@ class TtcStats(ctypes.Structure):
         ("ms_fiber", ctypes.c_double), ("ms_cross", ctypes.c_double), ("ms_quad", ctypes.c_double),
         ("ms_other", ctypes.c_double), ("fiber_entries", ctypes.c_int64), ("sb_entries", ctypes.c_int64),
         ("sb_updates", ctypes.c_int64), ("rook_steps", ctypes.c_int64), ("ext_entries", ctypes.c_int64),
-        ("ext_updates", ctypes.c_int64),
+        ("ext_updates", ctypes.c_int64), ("ring_steps", ctypes.c_int64),
     ]
 
 
@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
         "tt_cross_get_state": (i32, [P, P, P, P]),
         "tt_cross_get_fiber": (i32, [P, i32, P, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "tt_cross_get_stats": (i32, [P, ctypes.POINTER(TtcStats)]),
+        "tt_cross_get_wsum": (i32, [P, i32, P, P, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "tt_cross_set_timing": (i32, [P, i32]),
         "tt_cross_destroy": (None, [P]),
         "tt_cross_load_grid": (i32, [P, P, P, i32]),
@@ -150,6 +151,9 @@ class TTCross:
         if ku != kw:
             raise TypeError("nodes and weights must both be host or both be device arrays")
         self._h = ctypes.c_void_p()
+        # the library copies the grid asynchronously on its stream: the source buffers stay
+        # referenced here until a synchronising call (include/ttcross.h, tt_cross_init)
+        self._inflight = [keep_u, keep_w]
         sp = ctypes.c_void_p(int(stream)) if stream else ctypes.c_void_p()
         _check(self.lib, self.lib.tt_cross_init(ctypes.byref(self._h), ctypes.byref(self.cfg), pu, pw, ku, sp),
                "tt_cross_init")
@@ -186,6 +190,7 @@ class TTCross:
         v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
         _check(self.lib, self.lib.tt_integrate(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
                "tt_integrate")
+        self._synced()
         return v.value, l10.value, sg.value
 
     def load_grid(self, u, w):
@@ -193,7 +198,12 @@ class TTCross:
         pw, kw, keep_w = _ptr_and_kind(w)
         if ku != kw:
             raise TypeError("nodes and weights must both be host or both be device arrays")
+        self._inflight += [keep_u, keep_w]
         _check(self.lib, self.lib.tt_cross_load_grid(self._h, pu, pw, ku), "tt_cross_load_grid")
+
+    def _synced(self):
+        """The library's stream has completed everything enqueued so far."""
+        self._inflight = []
 
     def solve_launch(self, n_sweeps, graph=True):
         _check(self.lib, self.lib.tt_solve_launch(self._h, int(n_sweeps), 1 if graph else 0), "tt_solve_launch")
@@ -205,6 +215,7 @@ class TTCross:
         v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
         _check(self.lib, self.lib.tt_integrate_read(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
                "tt_integrate_read")
+        self._synced()
         return v.value, l10.value, sg.value
 
     def integrate_local(self):
@@ -214,6 +225,7 @@ class TTCross:
         v, l10, sg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
         _check(self.lib, self.lib.tt_integrate_finish(self._h, ctypes.byref(v), ctypes.byref(l10), ctypes.byref(sg)),
                "tt_integrate_finish")
+        self._synced()
         return v.value, l10.value, sg.value
 
     # -- buffers for the multi-process exchange (zero-copy device views)
@@ -238,6 +250,7 @@ class TTCross:
         _check(self.lib, self.lib.tt_cross_get_state(self._h, ranks.ctypes.data_as(ctypes.c_void_p),
                                                      piv.ctypes.data_as(ctypes.c_void_p),
                                                      par.ctypes.data_as(ctypes.c_void_p)), "tt_cross_get_state")
+        self._synced()
         P = [piv[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
         if parents:
             return ranks, P, [par[i, :ranks[i]].astype(np.int64) for i in range(self.d - 1)]
@@ -253,9 +266,24 @@ class TTCross:
                "tt_cross_get_fiber")
         return out
 
+    def wsum(self, mode):
+        """W_m = sum_a w_{m,a} F_m[:, :, a] in double-double as (hi, lo), each (r_{m-1}, r_m), as the
+        last quadrature (or fiber()) computed it."""
+        rx, ry = ctypes.c_int32(), ctypes.c_int32()
+        _check(self.lib, self.lib.tt_cross_get_wsum(self._h, int(mode), None, None, 0, ctypes.byref(rx),
+                                                    ctypes.byref(ry)), "tt_cross_get_wsum")
+        hi = np.empty((rx.value, ry.value))
+        lo = np.empty((rx.value, ry.value))
+        _check(self.lib, self.lib.tt_cross_get_wsum(self._h, int(mode), hi.ctypes.data_as(ctypes.c_void_p),
+                                                    lo.ctypes.data_as(ctypes.c_void_p), hi.size, ctypes.byref(rx),
+                                                    ctypes.byref(ry)), "tt_cross_get_wsum")
+        self._synced()
+        return hi, lo
+
     def stats(self):
         s = TtcStats()
         _check(self.lib, self.lib.tt_cross_get_stats(self._h, ctypes.byref(s)), "tt_cross_get_stats")
+        self._synced()
         return {f: getattr(s, f) for f, _ in TtcStats._fields_ if f != "pad"}
 
 

@@ -46,6 +46,9 @@ const char* const kKernelName[K_COUNT] = {
 const int kKernelClass[K_COUNT] = {KC_OTHER, KC_OTHER, KC_OTHER, KC_CROSS, KC_FIBER, KC_FIBER, KC_FIBER,
                                    KC_FIBER, KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD,  KC_QUAD};
 
+const char* const kWaveTimeout =
+    "k_sweeps: a superblock waited > 2 s for a neighbour (clusters not co-resident); the sweeps are incomplete";
+
 struct EvRec {
   cudaEvent_t a, b;
   int kid;
@@ -68,6 +71,7 @@ struct ttc_ctx {
   long long graph_launches = 0;
   DevCtx dc{};
   int chunk = 0, kb = 0, ke = 0, n_owned = 0, slots = 0, nrec = 0;
+  int* xbuf = nullptr;  // world > 1: exchange buffer [world][chunk][RS] (rank p's records in slot p)
   int sweeps = 0;
   int pending = 0;  // a local sweep waits for commit
   int* t0buf = nullptr;
@@ -171,11 +175,12 @@ int check_launch(const char* what) {
 }
 
 // ------------------------------------------------------------------ launch sequences
-// quadrature fibers: frozen parts + entries for modes [jbase, jbase+njobs).  fused (t-form
-// families only): the entries are not stored, k_fiber_wsum contracts them with the weights
-// into W directly (the product path of tt_integrate); otherwise k_fiber writes dc.fib
-// (tt_cross_get_fiber) and the caller runs k_wsum.
-int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false, bool count = true) {
+// quadrature fibers: frozen parts + entries for modes [jbase, jbase+njobs).  t-form
+// families: k_fiber_wsum contracts the entries with the weights into W directly, nothing
+// stored per entry (the product path of tt_integrate); emit (tt_cross_get_fiber): the same
+// kernel also writes every entry to dc.fib.  x-form: k_fiber_x writes dc.fib and the caller
+// runs k_wsum.
+int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool emit = false, bool count = true) {
   DevCtx dc = c->dc;
   if (!count) dc.counters = nullptr;   // (tt_cross_get_fiber: not part of the method's work)
   const int n = dc.n, tup = dc.cap;
@@ -210,50 +215,38 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool fused = false
     if (int e = check_launch("k_frozen_lr")) return e;
     if (int e = side_join(c, 1)) return e;
   }
-  if (fused) {
-    {
-      Timed t(c, K_FIBER);
-      // tiles of FW_TA x FW_TB fibers (the grid covers rank = cap; tiles beyond the actual
-      // ranks exit at once) x NS node ranges, NS (the cluster size) doubled up to 8 while
-      // the grid has fewer than 4 waves of 4 CTAs per SM and the ranges keep >= 32 nodes
-      const int ta = (tup + FW_TA - 1) / FW_TA, tb = (tup + FW_TB - 1) / FW_TB;
-      const long long tiles = (long long)ta * tb * njobs;
-      int ns = 1;
-      while (ns < 8 && tiles * ns < 16LL * c->sms && n / (2 * ns) >= 32) ns *= 2;
-      if (c->fw_ns > 0) ns = c->fw_ns;   // (experiments: TTC_FW_NS)
-      cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3(ta * tb, ns, njobs);
-      lc.blockDim = dim3(FW_TA * FW_TB);
-      lc.dynamicSmemBytes = fw_smem_bytes();
-      lc.stream = c->ls;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 1;
-      at[0].val.clusterDim.y = ns;
-      at[0].val.clusterDim.z = 1;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      cudaError_t e = dc.family == TTC_FAMILY_C ? cudaLaunchKernelEx(&lc, k_fiber_wsum<0>, dc, kind, jbase, tb)
-                                                : cudaLaunchKernelEx(&lc, k_fiber_wsum<1>, dc, kind, jbase, tb);
-      if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_fiber_wsum launch: ") + cudaGetErrorString(e));
-    }
-    return check_launch("k_fiber_wsum");
-  }
   {
     Timed t(c, K_FIBER);
-    // large fibers: a thread per (alpha, a) walking beta; small ones: an entry per thread
-    const bool loop = (long long)tup * tup * n * njobs >= (1LL << 22);
-    if (loop) {
-      const dim3 g((n + 255) / 256, tup, njobs);
-      if (dc.family == TTC_FAMILY_C) k_fiber<0, true><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
-      else k_fiber<1, true><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
-    } else {
-      const dim3 g(std::min(4096, (tup * n + 255) / 256), tup, njobs);
-      if (dc.family == TTC_FAMILY_C) k_fiber<0, false><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
-      else k_fiber<1, false><<<g, 256, 0, c->ls>>>(dc, kind, jbase);
-    }
+    // tiles of FW_TA x FW_TB fibers (the grid covers rank = cap; tiles beyond the actual
+    // ranks exit at once) x NS node ranges, NS (the cluster size) doubled up to 8 while
+    // the grid has fewer than 4 waves of 4 CTAs per SM and the ranges keep >= 32 nodes
+    const int ta = (tup + FW_TA - 1) / FW_TA, tb = (tup + FW_TB - 1) / FW_TB;
+    const long long tiles = (long long)ta * tb * njobs;
+    int ns = 1;
+    while (ns < 8 && tiles * ns < 16LL * c->sms && n / (2 * ns) >= 32) ns *= 2;
+    if (c->fw_ns > 0) ns = c->fw_ns;   // (experiments: TTC_FW_NS)
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(ta * tb, ns, njobs);
+    lc.blockDim = dim3(FW_TA * FW_TB);
+    lc.dynamicSmemBytes = fw_smem_bytes();
+    lc.stream = c->ls;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = ns;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t e;
+    if (dc.family == TTC_FAMILY_C)
+      e = emit ? cudaLaunchKernelEx(&lc, k_fiber_wsum<0, true>, dc, kind, jbase, tb)
+               : cudaLaunchKernelEx(&lc, k_fiber_wsum<0, false>, dc, kind, jbase, tb);
+    else
+      e = emit ? cudaLaunchKernelEx(&lc, k_fiber_wsum<1, true>, dc, kind, jbase, tb)
+               : cudaLaunchKernelEx(&lc, k_fiber_wsum<1, false>, dc, kind, jbase, tb);
+    if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_fiber_wsum launch: ") + cudaGetErrorString(e));
   }
-  return check_launch("k_fiber");
+  return check_launch("k_fiber_wsum");
 }
 
 // one Alg. 6 sweep over the owned superblocks -> rec_next
@@ -282,6 +275,9 @@ int do_sweep_local(ttc_ctx* c) {
     if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweep launch: ") + cudaGetErrorString(e));
     if (int e2 = check_launch("k_sweep")) return e2;
   }
+  if (c->cfg.world > 1 && c->n_owned > 0)   // own records -> own slot of the exchange buffer
+    CK(cudaMemcpyAsync(c->xbuf + (long long)c->cfg.rank * c->chunk * c->dc.RS, c->dc.rec_next + (long long)c->kb * c->dc.RS,
+                       sizeof(int32_t) * c->n_owned * c->dc.RS, cudaMemcpyDeviceToDevice, c->ls));
   c->pending = 1;
   return TTC_OK;
 }
@@ -318,9 +314,10 @@ int do_commit(ttc_ctx* c) {
   if (c->cfg.world == 1) {
     std::swap(c->dc.rec_cur, c->dc.rec_next);
   } else {
-    // keep the exchange buffer at a fixed address for the caller's collectives
-    CK(cudaMemcpyAsync(c->dc.rec_cur, c->dc.rec_next, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToDevice,
-                       c->ls));
+    // every rank's slot of the all-gathered exchange buffer -> the current records
+    k_unpack_records<<<c->cfg.world, 256, 0, c->ls>>>(c->xbuf, c->dc.rec_cur, c->dc.d - 1, c->cfg.world, c->chunk,
+                                                      c->dc.RS);
+    if (int e = check_launch("k_unpack_records")) return e;
   }
   c->pending = 0;
   c->sweeps++;
@@ -346,9 +343,8 @@ int do_integrate_local(ttc_ctx* c) {
     if (int e = check_launch("k_intersection")) return e;
   }
   if (nm > 0) {
-    const bool fused = dc.family < TTC_FAMILY_CX;
-    if (int e = launch_fibers(c, JOB_INT, m_lo, nm, fused)) return e;
-    if (!fused) {
+    if (int e = launch_fibers(c, JOB_INT, m_lo, nm)) return e;
+    if (dc.family >= TTC_FAMILY_CX) {
       {
         Timed t(c, K_WSUM);
         k_wsum<<<dim3((cap + 7) / 8, cap, nm), 256, 0, c->ls>>>(dc, m_lo);
@@ -430,7 +426,7 @@ int do_integrate_read(ttc_ctx* c, double* value, double* log10_abs, int32_t* sig
   int flag = 0, flag2[2] = {0, 0};
   std::memcpy(flag2, c->out_host + 2, 2 * sizeof(int));
   flag = flag2[0];
-  if (flag2[1]) return fail(TTC_ERR_CUDA, "k_sweeps: a superblock waited > 2 s for a neighbour (clusters not co-resident)");
+  if (flag2[1]) return fail(TTC_ERR_CUDA, kWaveTimeout);
   if (flag) return fail(TTC_ERR_SINGULAR, "an intersection matrix A(I_{<=k}, I_{>k}) is singular");
   const double core = c->out_host[0];
   const double lg2 = c->out_host[1];
@@ -478,9 +474,15 @@ int resolve_timing(ttc_ctx* c) {
   return TTC_OK;
 }
 
-// device part of a reset (async, capturable): rank-1 start, superblock state, counters
+// device part of a reset (async, capturable): rank-1 start (the seeded first pivot, DESIGN.md
+// R5 -- part of every timed solve), superblock state, counters
 int reset_device(ttc_ctx* c) {
   CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
+  {
+    Timed t(c, K_INIT_PIVOT);
+    k_init_pivot<<<1, N_INIT, 0, c->ls>>>(c->dc, c->t0buf);
+  }
+  if (int e = check_launch("k_init_pivot")) return e;
   {
     Timed t(c, K_INIT_RECORDS);
     k_init_records<<<std::max(std::max(c->nrec, c->n_owned), c->dc.d - 1), 128, 0, c->ls>>>(c->dc, c->t0buf, c->nrec,
@@ -629,10 +631,11 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.seed = k.seed;
   dc.world = k.world;
   dc.rank = k.rank;
-  c->chunk = (d - 1 + k.world - 1) / k.world;
+  // balanced partition (part_begin): D_20 on 8 ranks owns 3,3,3,2,2,2,2,2 superblocks
+  c->chunk = (d - 1 + k.world - 1) / k.world;   // the largest share: exchange slot size
   dc.chunk = c->chunk;
-  c->kb = std::min(d - 1, k.rank * c->chunk);
-  c->ke = std::min(d - 1, (k.rank + 1) * c->chunk);
+  c->kb = part_begin(d - 1, k.world, k.rank);
+  c->ke = part_begin(d - 1, k.world, k.rank + 1);
   c->n_owned = c->ke - c->kb;
   dc.kb = c->kb;
   dc.ke = c->ke;
@@ -640,7 +643,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.sbn = (long long)cap * n;
   dc.G = 1;  // cluster size of k_sweep, chosen below once the device is known
   c->slots = d;
-  c->nrec = k.world * c->chunk;
+  c->nrec = d - 1;   // record i = interface i
   c->rec_ints = (long long)c->nrec * dc.RS;
   dc.fib_stride = (long long)cap * cap * n;
   const int nj = std::max(1, c->n_owned);
@@ -664,6 +667,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   const size_t tab = (size_t)nj * cap * n;
   if ((e = dalloc(c, &dc.rec_cur, (size_t)c->rec_ints)) || (e = dalloc(c, &dc.rec_next, (size_t)c->rec_ints)) ||
       (e = dalloc(c, &c->t0buf, (size_t)d)) ||
+      (k.world > 1 && (e = dalloc(c, &c->xbuf, (size_t)k.world * c->chunk * dc.RS))) ||
       (e = dalloc(c, &dc.SA, tab)) || (e = dalloc(c, &dc.SB, tab)) ||
       (e = dalloc(c, &dc.U, (size_t)nj * cap * dc.sbn)) || (e = dalloc(c, &dc.V, (size_t)nj * cap * dc.sbn)) ||
       (e = dalloc(c, &dc.Araw, (size_t)nj * dc.sbn)) || (e = dalloc(c, &dc.praw_max, (size_t)nj)) ||
@@ -720,8 +724,10 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     allow((const void*)k_sweep<1, false, 512>, 180 * 1024);
     allow((const void*)k_sweep<0, true, 512>, 180 * 1024);
     allow((const void*)k_sweep<1, true, 512>, 180 * 1024);
-    allow((const void*)k_fiber_wsum<0>, fw_smem_bytes());
-    allow((const void*)k_fiber_wsum<1>, fw_smem_bytes());
+    allow((const void*)k_fiber_wsum<0, false>, fw_smem_bytes());
+    allow((const void*)k_fiber_wsum<1, false>, fw_smem_bytes());
+    allow((const void*)k_fiber_wsum<0, true>, fw_smem_bytes());
+    allow((const void*)k_fiber_wsum<1, true>, fw_smem_bytes());
     const int quad_smem = 2 * cap * cap * (int)sizeof(DD);
     if (ce == cudaSuccess) ce = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, quad_smem);
     if (ce != cudaSuccess) return bail(fail(TTC_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(ce)));
@@ -788,7 +794,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       }
     };
     // resident clusters for (G, cached)
-    auto resident = [&](int g, bool cached) -> int {
+    auto resident_of = [&](const void* fn, int g, bool cached) -> int {
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(g);
       lc.blockDim = dim3(T);
@@ -801,12 +807,13 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       lc.attrs = at;
       lc.numAttrs = 1;
       int nclus = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclus, fn_for(cached), &lc) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&nclus, fn, &lc) != cudaSuccess) {
         cudaGetLastError();
         return 0;
       }
       return nclus;
     };
+    auto resident = [&](int g, bool cached) -> int { return resident_of(fn_for(cached), g, cached); };
     // prefer: all nj clusters resident; cached rows when they fit; then the largest G
     bool cached = false;
     for (;; G >>= 1) {
@@ -849,7 +856,10 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
         default: c->sweeps_fn = big ? (const void*)k_sweeps<4, false, 512> : (const void*)k_sweeps<4, false, 256>; break;
       }
       // the wavefront needs every cluster resident at once
-      c->persistent = k.world == 1 && resident(G, cached) >= nj && !std::getenv("TTC_NO_PERSISTENT");
+      // (queried for the persistent kernel itself: its register / shared-memory footprint
+      // differs from the single-sweep kernel's)
+      c->persistent = k.world == 1 && resident_of(c->sweeps_fn, G, cached) >= nj && resident(G, cached) >= nj &&
+                      !std::getenv("TTC_NO_PERSISTENT");
     }
   }
   int rc = tt_cross_load_grid(c, nodes_u, weights, mem_kind);
@@ -881,11 +891,6 @@ int tt_cross_load_grid(ttc_ctx* c, const double* nodes_u, const double* weights,
                                                              const_cast<long long*>(c->dc.clo), d * n);
   }
   if (int e = check_launch("k_prep_nodes")) return e;
-  {
-    Timed t(c, K_INIT_PIVOT);
-    k_init_pivot<<<1, N_INIT, 0, c->stream>>>(c->dc, c->t0buf);
-  }
-  if (int e = check_launch("k_init_pivot")) return e;
   return tt_cross_reset(c);
 }
 
@@ -920,8 +925,14 @@ int tt_cross_sweep(ttc_ctx* c, int32_t n_sweeps) {
 
 int tt_cross_exchange_buffer(ttc_ctx* c, void** dev_ptr, int64_t* bytes_total, int64_t* bytes_per_rank) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
-  if (dev_ptr) *dev_ptr = c->dc.rec_next;
-  if (bytes_total) *bytes_total = c->rec_ints * (int64_t)sizeof(int32_t);
+  if (c->cfg.world == 1) {
+    if (dev_ptr) *dev_ptr = c->dc.rec_next;
+    if (bytes_total) *bytes_total = c->rec_ints * (int64_t)sizeof(int32_t);
+    if (bytes_per_rank) *bytes_per_rank = c->rec_ints * (int64_t)sizeof(int32_t);
+    return TTC_OK;
+  }
+  if (dev_ptr) *dev_ptr = c->xbuf;
+  if (bytes_total) *bytes_total = (int64_t)c->cfg.world * c->chunk * c->dc.RS * (int64_t)sizeof(int32_t);
   if (bytes_per_rank) *bytes_per_rank = (int64_t)c->chunk * c->dc.RS * (int64_t)sizeof(int32_t);
   return TTC_OK;
 }
@@ -992,8 +1003,11 @@ int tt_cross_get_state(ttc_ctx* c, int32_t* ranks_out, int32_t* piv_out, int32_t
   if (!c) return fail(TTC_ERR_ARG, "null context");
   const int d = c->dc.d, cap = c->dc.cap, RS = c->dc.RS;
   std::vector<int32_t> rec(c->rec_ints);
+  int32_t flags[2] = {0, 0};
   CK(cudaMemcpyAsync(rec.data(), c->dc.rec_cur, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(flags, c->dc.flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (flags[1]) return fail(TTC_ERR_CUDA, kWaveTimeout);
   for (int i = 0; i < d - 1; ++i) {
     const int32_t* R = rec.data() + (long long)i * RS;
     if (ranks_out) ranks_out[i] = R[0];
@@ -1023,18 +1037,53 @@ int tt_cross_get_fiber(ttc_ctx* c, int32_t mode, double* out, int64_t capacity, 
     if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
     // evaluated on demand from the current index sets (the quadrature pass contracts the
     // t-form fibers without storing them)
-    if (int e = launch_fibers(c, JOB_INT, mode, 1, false, false)) return e;
+    if (int e = launch_fibers(c, JOB_INT, mode, 1, true, false)) return e;
+    if (c->dc.family >= TTC_FAMILY_CX) {   // (x-form: W from the stored entries, as tt_integrate)
+      Timed t(c, K_WSUM);
+      k_wsum<<<dim3((c->dc.cap + 7) / 8, c->dc.cap, 1), 256, 0, c->ls>>>(c->dc, mode);
+    }
+    if (int e = check_launch("k_wsum")) return e;
     CK(cudaMemcpyAsync(out, c->dc.fib + (long long)mode * c->dc.fib_stride, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
   return TTC_OK;
 }
 
+int tt_cross_get_wsum(ttc_ctx* c, int32_t mode, double* hi_out, double* lo_out, int64_t capacity, int32_t* rx,
+                      int32_t* ry) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  const int d = c->dc.d, cap = c->dc.cap, RS = c->dc.RS;
+  if (mode < 0 || mode >= d) return fail(TTC_ERR_ARG, "mode out of range");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  int32_t a = 1, b = 1;
+  if (mode > 0) CK(cudaMemcpyAsync(&a, c->dc.rec_cur + (long long)(mode - 1) * RS, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if (mode < d - 1) CK(cudaMemcpyAsync(&b, c->dc.rec_cur + (long long)mode * RS, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (rx) *rx = a;
+  if (ry) *ry = b;
+  if (!hi_out) return TTC_OK;
+  if (!lo_out) return fail(TTC_ERR_ARG, "lo_out is NULL");
+  if (capacity < (int64_t)a * b) return fail(TTC_ERR_ARG, "wsum buffer too small");
+  std::vector<DD> W((size_t)cap * cap);
+  CK(cudaMemcpyAsync(W.data(), c->dc.W + (long long)mode * cap * cap, sizeof(DD) * cap * cap, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < a; ++i)
+    for (int j = 0; j < b; ++j) {
+      hi_out[(long long)i * b + j] = W[(size_t)i * cap + j].hi;
+      lo_out[(long long)i * b + j] = W[(size_t)i * cap + j].lo;
+    }
+  return TTC_OK;
+}
+
 int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
   if (!c || !out) return fail(TTC_ERR_ARG, "null argument");
   unsigned long long cnt[TTC_NCOUNTERS] = {};
+  int32_t flags[2] = {0, 0};
   CK(cudaMemcpyAsync(cnt, c->dc.counters, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(flags, c->dc.flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (flags[1]) return fail(TTC_ERR_CUDA, kWaveTimeout);
   if (int e = resolve_timing(c)) return e;
   std::memset(out, 0, sizeof(*out));
   out->evals = (int64_t)cnt[CNT_EVALS];
@@ -1050,6 +1099,7 @@ int tt_cross_get_stats(ttc_ctx* c, ttc_stats* out) {
   out->rook_steps = (int64_t)cnt[CNT_ROOK_STEPS];
   out->ext_entries = (int64_t)cnt[CNT_EXT_ENTRIES];
   out->ext_updates = (int64_t)cnt[CNT_EXT_UPDATES];
+  out->ring_steps = (int64_t)cnt[CNT_RING_STEPS];
   return TTC_OK;
 }
 

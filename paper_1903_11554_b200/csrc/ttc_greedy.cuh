@@ -106,6 +106,23 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
   if (i == 0 && threadIdx.x == 0) c.flags[1] = 0;
 }
 
+// Balanced superblock partition (Alg. 6 line 1): rank p owns the interfaces
+// [kb_p, ke_p), the first (d-1) mod world ranks one more than the others.
+__host__ __device__ __forceinline__ int part_begin(int nif, int world, int p) {
+  const int base = nif / world, rem = nif % world;
+  return p * base + (p < rem ? p : rem);
+}
+
+// multi-process commit: rank p's slot of the all-gathered exchange buffer (its records of
+// interfaces [kb_p, ke_p), slot stride `chunk` records) -> the current records; one block per rank
+__global__ void k_unpack_records(const int* xbuf, int* rec_cur, int nif, int world, int chunk, int RS) {
+  const int p = blockIdx.x;
+  const int kb = part_begin(nif, world, p), ke = part_begin(nif, world, p + 1);
+  const int* src = xbuf + (long long)p * chunk * RS;
+  int* dst = rec_cur + (long long)kb * RS;
+  for (long long t = threadIdx.x; t < (long long)(ke - kb) * RS; t += blockDim.x) dst[t] = src[t];
+}
+
 // CX[alpha][beta] by one warp: lanes split the k * (d-k-2) cross pairs (i < k, j > k+1), each
 // lane a partial double-double product, then the shuffle tree -- the product is rounded once
 // later, so any grouping gives the same entries (R3).  (A thread per entry ran the
@@ -996,7 +1013,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   if (p0 == 0.0) active = false;  // singular first pivot: leave the interface (R8)
   double scale = c.praw_max[job];
   if (scale < 0.0) scale = fabs(p0);
-  unsigned long long evals = 0, upd = 0;
+  unsigned long long evals = 0, upd = 0, ring_steps = 0;
   int steps = 0;
   int xst = 0, yst = 0;
   bool added = false;
@@ -1093,6 +1110,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       const int q = (int)S.best.idx;
       xst = smp[2 * q];
       yst = smp[2 * q + 1];
+      // smp aliases S.f_node, which the first column step (family D, staged) overwrites
+      // before its own barrier: every thread must have read the winner first
+      if (FAMILY == 1 && stage_n) __syncthreads();
       if (cr == 0 && tid == 0) {
         evals += c.ns;
         upd += (unsigned long long)c.ns * r;
@@ -1129,6 +1149,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       if (tid == 0) {
         evals += (unsigned long long)max(0, xe - xb);
         upd += (unsigned long long)max(0, xe - xb) * r;
+        ring_steps += !CACHED && xe - xb >= RING_MIN_ROWS * T;   // (column_eval's use_ring)
       }
       if (!search) {
         __syncthreads();
@@ -1151,6 +1172,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       if (tid == 0) {
         evals += (unsigned long long)max(0, ye - yb);
         upd += (unsigned long long)max(0, ye - yb) * r;
+        ring_steps += !CACHED && ye - yb >= RING_MIN_ROWS * T;   // (row_eval's use_ring)
       }
       if (!search) {
         __syncthreads();
@@ -1241,6 +1263,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (ext_ent) atomicAdd(&c.counters[CNT_EXT_ENTRIES], ext_ent);
     if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
+    if (ring_steps) atomicAdd(&c.counters[CNT_RING_STEPS], ring_steps);
   }
   TRACE(40);
   // no CTA may leave while another can still read its shared memory; inside the persistent

@@ -130,76 +130,6 @@ __global__ void k_fill(double* p, double v, long long count) {
     p[t] = v;
 }
 
-// ---------------------------------------------------------------------------------------
-// fiber entries: grid x = flat (beta*n + a) chunks, y = alpha, z = job
-// ---------------------------------------------------------------------------------------
-// Quadrature fiber entries, two launch shapes:
-//  LOOP = false (small fibers, latency-bound): one entry per thread, grid x = flat
-//          (beta*n + a) chunks, y = alpha, z = job;
-//  LOOP = true (large fibers): grid x = chunk of 256 nodes a, y = alpha, z = job; a thread
-//          keeps its (alpha, a) factors -- S_L + c_m[a] and P_LL * Q_L[alpha][a] -- in
-//          registers and walks beta: per entry only Q_R[beta][a] streams (coalesced over
-//          a), S_R / Pf are warp broadcasts, the stores F[alpha][beta][a] are coalesced.
-//          (Prefetching 4 or 8 betas per iteration raised registers and ran slower.)
-template <int FAMILY, bool LOOP>
-__global__ void __launch_bounds__(256) k_fiber(DevCtx c, int kind, int jbase) {
-  const int j = jbase + blockIdx.z, al = blockIdx.y;
-  Job jb = make_job(c, kind, j);
-  if (al >= jb.rx) return;
-  const int n = c.n, m = jb.m;
-  const long long base = (long long)j * c.cap;
-  if (!LOOP) {
-    const int total = jb.ry * n;
-    const ESum sl = c.sl[base + al];
-    double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n;
-    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-      const int be = f / n;
-      const int a = f - be * n;
-      ESum s = sl;
-      esum_add(s, c.sr[base + be]);
-      esum_add(s, c.chi[m * n + a], c.clo[m * n + a]);
-      const double S = esum_round(s);
-      const double SS = __dmul_rn(S, S);
-      double v;
-      if (FAMILY == 0) {
-        v = __drcp_rn(SS);
-      } else {
-        DDE p = c.pf[(base + al) * c.cap + be];
-        dde_mul(p, c.ql[(base + al) * n + a]);
-        dde_mul(p, c.qr[(base + be) * n + a]);
-        v = dde_div(p, SS);
-      }
-      F[f] = v;
-    }
-    return;
-  }
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  ESum sa = c.sl[base + al];
-  esum_add(sa, c.chi[m * n + a], c.clo[m * n + a]);
-  DDE pa;
-  if (FAMILY == 1) pa = c.ql[(base + al) * n + a];
-  double* F = c.fib + (long long)j * c.fib_stride + (long long)al * jb.ry * n + a;
-  const DDE* pf = c.pf + (base + al) * c.cap;
-  const int ry = jb.ry;
-  for (int be = 0; be < ry; ++be) {
-    ESum s = sa;
-    esum_add(s, c.sr[base + be]);
-    const double S = esum_round(s);
-    const double SS = __dmul_rn(S, S);
-    double v;
-    if (FAMILY == 0) {
-      v = __drcp_rn(SS);
-    } else {
-      DDE p = pf[be];
-      dde_mul(p, pa);
-      dde_mul(p, c.qr[(base + be) * n + a]);
-      v = dde_div(p, SS);
-    }
-    F[(long long)be * n] = v;
-  }
-}
-
 __device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, double yl) {
   const double p = __dmul_rn(h, yh);
   const double err = fma(h, yh, -p);
@@ -250,7 +180,10 @@ __device__ __forceinline__ void cp_async8g(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-template <int FAMILY>
+// EMIT = true (tt_cross_get_fiber): the same kernel also stores every entry it contracts,
+// F[alpha][beta][a] -> c.fib, so the fiber entries checked against the oracle are the product
+// path's own (the stores are uncoalesced; diagnostics only).
+template <int FAMILY, bool EMIT>
 __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int kind, int jbase, int tiles_b) {
   extern __shared__ __align__(16) unsigned char fw_dyn[];
   FwBuf* buf = reinterpret_cast<FwBuf*>(fw_dyn);
@@ -311,6 +244,7 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
     if (FAMILY == 1) p0 = c.pf[(base + al) * c.cap + be];
   }
   double hi = 0.0, lo = 0.0;
+  double* F = EMIT ? c.fib + (long long)j * c.fib_stride + ((long long)al * jb.ry + be) * n : nullptr;
   // balanced chunks of <= FW_CH nodes (65 nodes: 33 + 32, not 36 + 29 or 32 + 32 + 1)
   const int nchunk = (a_hi - a_lo + FW_CH - 1) / FW_CH;
   const int csz = nchunk > 0 ? (a_hi - a_lo + nchunk - 1) / nchunk : 0;
@@ -341,6 +275,7 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
           dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
           v = dde_div(DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0}, SS);
         }
+        if (EMIT) F[a0 + a] = v;
         const double wa = B.w[a];
         const double pr = __dmul_rn(wa, v);
         const double pe = fma(wa, v, -pr);

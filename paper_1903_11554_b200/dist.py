@@ -1,10 +1,11 @@
 """Multi-GPU plumbing of the dimension-parallel TT cross (Alg. 6).
 
-One process per GPU.  Interfaces (superblocks) are partitioned into contiguous chunks,
-rank p owning [p*chunk, min(d-1, (p+1)*chunk)) with chunk = ceil((d-1)/world) (Alg. 6
-line 1 "Deduce the range [k_beg, k_end) of superblocks belonging to the process p").
-After every sweep each rank has the new pivots of its own interfaces in its slice of
-the library's record buffer; an all-gather of that buffer gives every rank the complete
+One process per GPU.  Interfaces (superblocks) are partitioned into balanced contiguous
+blocks, rank p owning [kb_p, kb_{p+1}) with kb_p = p*q + min(p, m), q = (d-1) // world,
+m = (d-1) % world (Alg. 6 line 1 "Deduce the range [k_beg, k_end) of superblocks belonging
+to the process p"): D_20 on 8 ranks owns 3,3,3,2,2,2,2,2.  After every sweep each rank has
+the new pivots of its own interfaces in its slot of the library's exchange buffer (slots of
+chunk = ceil((d-1)/world) records); an all-gather of the slots gives every rank the complete
 new index sets (the paper exchanges only neighbour pivots, Alg. 6 lines 6-8; an all-gather
 over NVSwitch costs one latency-bound collective of a few KB, and every rank needs the full
 sets at the quadrature).  The quadrature all-gathers the per-rank partial chain products
@@ -23,12 +24,17 @@ import torch.distributed as dist
 from .binding import TTCross
 
 
+def part_begin(nif: int, world: int, p: int) -> int:
+    """First interface of rank p in the balanced partition of ``nif`` interfaces."""
+    q, m = divmod(nif, world)
+    return p * q + min(p, m)
+
+
 def owned_interfaces(d: int, rank: int, world: int):
-    """[kb, ke) of the interfaces owned by ``rank`` (same rule as libttcross)."""
+    """[kb, ke) of the interfaces owned by ``rank`` and the exchange slot size ``chunk``
+    (records per rank slot = the largest share), the rule of libttcross (part_begin)."""
     chunk = (d - 1 + world - 1) // world
-    kb = min(d - 1, rank * chunk)
-    ke = min(d - 1, (rank + 1) * chunk)
-    return kb, ke, chunk
+    return part_begin(d - 1, world, rank), part_begin(d - 1, world, rank + 1), chunk
 
 
 def record_stride(d: int, cap: int) -> int:
@@ -62,6 +68,28 @@ def unpack_records(buf, d: int, cap: int, n_interfaces: int):
     return piv, par
 
 
+def pack_slots(rec, d: int, cap: int, world: int):
+    """Exchange-buffer layout from interface-indexed records (host emulation of what
+    tt_cross_sweep_local writes): slot p (``chunk`` records) starts with rank p's records."""
+    rs = record_stride(d, cap)
+    chunk = (d - 1 + world - 1) // world
+    out = torch.full((world * chunk * rs,), -1, dtype=torch.int32)
+    for p in range(world):
+        kb, ke, _ = owned_interfaces(d, p, world)
+        out[p * chunk * rs: (p * chunk + ke - kb) * rs] = rec[kb * rs: ke * rs]
+    return out
+
+
+def unpack_slots(xbuf, rec, d: int, cap: int, world: int):
+    """Inverse of pack_slots into interface-indexed records (what tt_cross_commit does)."""
+    rs = record_stride(d, cap)
+    chunk = (d - 1 + world - 1) // world
+    for p in range(world):
+        kb, ke, _ = owned_interfaces(d, p, world)
+        rec[kb * rs: ke * rs] = xbuf[p * chunk * rs: (p * chunk + ke - kb) * rs]
+    return rec
+
+
 def allgather_slices(buf: torch.Tensor, per_rank: int, group=None):
     """In-place all-gather: rank p's elements buf[p*per_rank:(p+1)*per_rank] are copied to
     every rank.  ``buf`` must hold world*per_rank elements (1-D)."""
@@ -69,8 +97,6 @@ def allgather_slices(buf: torch.Tensor, per_rank: int, group=None):
     rank = dist.get_rank(group)
     if buf.numel() != world * per_rank:
         raise ValueError(f"buffer has {buf.numel()} elements, expected {world}*{per_rank}")
-    if world == 1:
-        return buf
     mine = buf[rank * per_rank:(rank + 1) * per_rank].clone()
     dist.all_gather_into_tensor(buf, mine, group=group)
     return buf

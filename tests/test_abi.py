@@ -84,7 +84,7 @@ def test_config_struct_layout_matches_header():
     from paper_1903_11554_b200 import binding
     assert ctypes.sizeof(binding.TtcConfig) == 6 * 4 + 8 + 8 + 3 * 4 + 4  # trailing pad to 8
     assert binding.TtcConfig.tol.offset == 24 and binding.TtcConfig.seed.offset == 32
-    assert ctypes.sizeof(binding.TtcStats) == 8 + 8 + 4 + 4 + 4 * 8 + 6 * 8
+    assert ctypes.sizeof(binding.TtcStats) == 8 + 8 + 4 + 4 + 4 * 8 + 7 * 8
 
 
 def test_c_demo_links_against_the_library(lib):

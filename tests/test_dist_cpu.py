@@ -16,8 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import cross as X
-from paper_1903_11554_b200.dist import (allgather_slices, owned_interfaces, pack_records, record_stride,
-                                        unpack_records)
+from paper_1903_11554_b200.dist import (allgather_slices, owned_interfaces, pack_records, pack_slots,
+                                        record_stride, unpack_records, unpack_slots)
 from workloads import FAMILY_C, FAMILY_D, ising_grid
 
 
@@ -37,6 +37,19 @@ def test_partition_covers_every_interface_once(d, world):
         assert 0 <= kb <= ke <= d - 1 and ke - kb <= chunk
         seen += list(range(kb, ke))
     assert seen == list(range(d - 1))
+
+
+def test_partition_is_balanced():
+    """Alg. 6 line 1 with balanced blocks: shares differ by at most one, larger first."""
+    shares = [owned_interfaces(20, r, 8)[1] - owned_interfaces(20, r, 8)[0] for r in range(8)]
+    assert shares == [3, 3, 3, 2, 2, 2, 2, 2]
+    shares = [owned_interfaces(200, r, 8)[1] - owned_interfaces(200, r, 8)[0] for r in range(8)]
+    assert shares == [25, 25, 25, 25, 25, 25, 25, 24]
+    assert [owned_interfaces(3, r, 4)[1] - owned_interfaces(3, r, 4)[0] for r in range(4)] == [1, 1, 0, 0]
+    for d in (2, 5, 20, 201):
+        for world in (1, 2, 3, 8):
+            sh = [owned_interfaces(d, r, world)[1] - owned_interfaces(d, r, world)[0] for r in range(world)]
+            assert max(sh) - min(sh) <= 1 and sh == sorted(sh, reverse=True) and max(sh) <= owned_interfaces(d, 0, world)[2]
 
 
 def test_record_roundtrip():
@@ -63,11 +76,11 @@ def _worker(rank, world, port, d, n, cap, sweeps, q):
         st = X.initial_state(prob)
         for _ in range(sweeps):
             mine = X.sweep(prob, st, range(kb, ke))          # this rank's superblocks only
-            buf = pack_records(st.piv, st.par, d, cap, world * chunk)
-            local = pack_records(mine.piv, mine.par, d, cap, world * chunk)
-            buf[kb * rs: ke * rs] = local[kb * rs: ke * rs]
-            allgather_slices(buf, chunk * rs)                 # the exchange of Alg. 6 lines 6-8
-            piv, par = unpack_records(buf, d, cap, d - 1)
+            local = pack_records(mine.piv, mine.par, d, cap, d - 1)
+            xbuf = pack_slots(local, d, cap, world)          # own records -> own slot
+            allgather_slices(xbuf, chunk * rs)                # the exchange of Alg. 6 lines 6-8
+            rec = unpack_slots(xbuf, pack_records(st.piv, st.par, d, cap, d - 1), d, cap, world)
+            piv, par = unpack_records(rec, d, cap, d - 1)
             st = X.State([p.numpy() for p in piv], [p.numpy() for p in par], st.sweep + 1, 0)
         if rank == 0:
             q.put([p.tolist() for p in st.piv])
@@ -75,7 +88,7 @@ def _worker(rank, world, port, d, n, cap, sweeps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("d,world", [(6, 2), (5, 2)])
+@pytest.mark.parametrize("d,world", [(6, 2), (5, 2), (7, 3)])
 def test_two_process_sweeps_equal_single_process(d, world):
     n, cap, sweeps = 7, 5, 4
     ctx = mp.get_context("spawn")

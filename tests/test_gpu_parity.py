@@ -61,6 +61,21 @@ def gpu_sweep_evals(prob, before, after, prev_rows, prev_cols):
     return total, rows_done, cols_done
 
 
+WSUM_RTOL = 1e-28
+
+
+def assert_wsum_matches(got, F, w, m):
+    """W_m = sum_a w_a F[:, :, a] (§4.1) from the fused fiber kernel in
+    double-double against the oracle's double-double sum of the oracle's fibers: every term
+    w_a A >= 0, so both are within ~n 2^-104 relative of the exact sum; bar 1e-28 relative."""
+    hi, lo = got
+    rh, rl = X._dd_weighted_sum(F, w)
+    assert hi.shape == rh.shape, (m, hi.shape, rh.shape)
+    diff = np.abs((hi - rh) + (lo - rl))
+    bad = diff > WSUM_RTOL * np.abs(rh)
+    assert not np.any(bad), f"W_{m}: {int(bad.sum())} entries beyond 1e-28, worst {np.max(diff / np.maximum(np.abs(rh), 1e-300))}"
+
+
 def quad_evals(prob, st):
     d, n = prob.d, prob.n
     r = [1] + st.ranks + [1]
@@ -84,8 +99,11 @@ def check_run(tt, prob, sweeps, check_fibers=True, check_evals=True):
     fibers = X.tt_fibers(prob, st)
     ref, rlog10, rsign = X.integrate_exact(prob, st, fibers)
     if check_fibers:
+        # the weighted sums the product kernel contracted (read before fiber() refreshes them)
         for m in range(prob.d):
-            g = tt.fiber(m)
+            assert_wsum_matches(tt.wsum(m), fibers[m], prob.qw[m], m)
+        for m in range(prob.d):
+            g = tt.fiber(m)   # the entries of the same kernel (k_fiber_wsum, EMIT)
             assert g.shape == fibers[m].shape
             assert np.array_equal(g, fibers[m]), f"fiber {m} differs"
     assert sign == rsign

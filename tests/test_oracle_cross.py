@@ -90,6 +90,44 @@ def test_added_pivots_follow_alg2(fam, d, n, cap, rook):
         st = new
 
 
+@pytest.mark.parametrize("fam,d,n,cap,ns,rook", [(FAMILY_C, 3, 9, 6, 16, 4), (FAMILY_D, 4, 7, 5, 24, 0),
+                                                 (FAMILY_D, 3, 11, 8, 8, 1), (FAMILY_C, 4, 6, 6, 40, 2)])
+def test_search_starts_at_largest_sample_error(fam, d, n, cap, ns, rook):
+    """Alg. 2 line 1: the rook search starts at the sample with the
+    largest cross error |E| among the n_samples random superblock entries, pivot rows and
+    columns excluded (E vanishes there).  The samples are
+    re-drawn here from the counter-based stream (splitmix64, pinned by its published vector)
+    and E is the numpy.linalg cross error of eq. (1), not the oracle's incomplete-LU factors.
+    With rook = 0 the start is the added pivot itself."""
+    prob = make_problem(fam, d, n, 3.0, cap, ns=ns, rook=rook)
+    st = X.initial_state(prob)
+    checked = 0
+    for sweep in range(6):
+        new = X.sweep(prob, st)
+        for k in range(d - 1):
+            info = new.log[-1][1][k]
+            sb, Asb = superblock_dense(prob, st, k)
+            scale = np.max(np.abs(Asb))
+            R, C = Asb.shape
+            for add in info["adds"]:
+                tag = 1 + sweep
+                sx = [X.splitmix64(prob.seed, ((tag * (d + 1) + k) << 20) + 2 * q) % R for q in range(ns)]
+                sy = [X.splitmix64(prob.seed, ((tag * (d + 1) + k) << 20) + 2 * q + 1) % C for q in range(ns)]
+                I, J = add["xs_before"], add["ys_before"]
+                E = cross_error(Asb, I, J)
+                e = np.array([0.0 if (x in I or y in J) else abs(E[x, y]) for x, y in zip(sx, sy)])
+                x0, y0 = add["start"]
+                q0 = next(q for q in range(ns) if (sx[q], sy[q]) == (x0, y0))
+                assert e[q0] >= e.max() - 1e-9 * scale          # a largest |E| sample (up to rounding)
+                if e.max() > 1e-6 * scale:
+                    assert x0 not in I and y0 not in J          # pivot rows / columns excluded
+                if rook == 0:
+                    assert (add["x"], add["y"]) == (x0, y0)
+                checked += 1
+        st = new
+    assert checked >= 3
+
+
 def test_aca_form_equals_cross_formula():
     """The u/v factors rebuilt by the LU init reproduce A(:, J) A(I, J)^{-1} A(I, :)."""
     prob = make_problem(FAMILY_D, 4, 9, 3.0, 6)
