@@ -287,15 +287,23 @@ class TTCross:
         return {f: getattr(s, f) for f, _ in TtcStats._fields_ if f != "pad"}
 
 
-    def phase_times(self):
+    def phase_times(self, per_sweep=False):
         """k_sweep phase clocks (us, CTA 0 of superblock TTC_PHASE_JOB, default the first) accumulated
-        while timing is on."""
-        out = np.zeros(14)
-        _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), 14),
+        while timing is on; per_sweep=True also returns the per-sweep log (a list of dicts)."""
+        nw = 14 + 8 * 256
+        out = np.zeros(nw)
+        _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), nw),
                "tt_cross_get_phase_times")
         names = ["prologue", "tables", "extend", "samples", "rook", "final", "exit", "launches",
                  "col_eval", "col_argmax", "row_eval", "row_argmax", "ext_raw", "ext_rec"]
-        return dict(zip(names, out.tolist()))
+        tot = dict(zip(names, out[:14].tolist()))
+        if not per_sweep:
+            return tot
+        log = out[14:].reshape(256, 8)
+        rows = [dict(zip(names[:7] + ["steps"], [round(x, 2) for x in r.tolist()])) for r in log]
+        while rows and not any(rows[-1].values()):
+            rows.pop()
+        return tot, rows
 
     def launch_shape(self):
         g, t, ca, sm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()

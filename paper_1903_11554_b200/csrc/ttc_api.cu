@@ -680,7 +680,7 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
       (e = dalloc(c, &dc.rank_ring, (size_t)2 * d)) || (e = dalloc(c, &dc.done, (size_t)d)) ||
-      (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_NPHASES)) ||
+      (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_PHASE_WORDS)) ||
       (e = dalloc(c, &c->partials, (size_t)k.world * chain_record_size(cap))) || (e = dalloc(c, &c->out_dev, 4)) ||
       (e = dalloc(c, &c->chainA, (size_t)(nj + 1) * cap * cap)) || (e = dalloc(c, &c->chainB, (size_t)(nj + 1) * cap * cap)) ||
       (e = dalloc(c, &c->chainAd, (size_t)(nj + 1) * 3)) || (e = dalloc(c, &c->chainBd, (size_t)(nj + 1) * 3)))
@@ -1127,17 +1127,21 @@ int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   c->timing = enable != 0;
   c->dc.phase_ns = c->timing ? c->phase_buf : nullptr;
-  if (c->timing) CK(cudaMemsetAsync(c->phase_buf, 0, TTC_NPHASES * sizeof(unsigned long long), c->stream));
+  if (c->timing) CK(cudaMemsetAsync(c->phase_buf, 0, TTC_PHASE_WORDS * sizeof(unsigned long long), c->stream));
   return TTC_OK;
 }
 
 int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
   if (!c || !us_out) return fail(TTC_ERR_ARG, "null argument");
   if (count < 12) return fail(TTC_ERR_ARG, "need 12 slots");
-  unsigned long long v[TTC_NPHASES] = {};
-  CK(cudaMemcpyAsync(v, c->phase_buf, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<unsigned long long> v(TTC_PHASE_WORDS);
+  CK(cudaMemcpyAsync(v.data(), c->phase_buf, sizeof(unsigned long long) * TTC_PHASE_WORDS, cudaMemcpyDeviceToHost,
+                     c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (int i = 0; i < TTC_NPHASES && i < count; ++i) us_out[i] = i == PH_LAUNCHES ? (double)v[i] : v[i] * 1e-3;
+  for (int i = 0; i < TTC_PHASE_WORDS && i < count; ++i) {
+    const bool is_count = i == PH_LAUNCHES || (i >= TTC_NPHASES && (i - TTC_NPHASES) % 8 == 7);
+    us_out[i] = is_count ? (double)v[i] : v[i] * 1e-3;
+  }
   return TTC_OK;
 }
 

@@ -548,7 +548,6 @@ struct DotRing {
   __device__ __forceinline__ void init(double* b, const double* f, int T_, int tid_, int tb_, int sbn_, int r_, int zb,
                                        int ze) {
     buf = b; F = f; T = T_; tid = tid_; tb = tb_; sbn = sbn_; r = r_;
-    if (EVICT_FIRST) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     nb = (r + tb - 1) / tb;
     z0 = zb + tid;
     const int rows = z0 < ze ? (ze - z0 + T - 1) / T : 0;
@@ -563,8 +562,14 @@ struct DotRing {
       const int t0 = iblk * tb, tn = min(tb, r - t0);
       const double* src = F + t0 * sbn + z0 + irow * T;
       // (loops left to the compiler's unrolling: measured faster than unroll 1 on D_20)
-      if (EVICT_FIRST)
+      if (EVICT_FIRST) {
+        // the policy is created right before its copies: LDGSTS takes it from a uniform
+        // register, and a policy created once in init() and carried across the out-of-line
+        // calls of the step reached the copies as garbage in some builds (SASS
+        // `LDGSTS desc[UR]` -> "illegal instruction", found with cuda-gdb)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         for (int i = 0; i < tn; ++i) cp_async8_ef(dst + i * T, src + i * sbn, pol);
+      }
       else
         for (int i = 0; i < tn; ++i) cp_async8(dst + i * T, src + i * sbn);
       if (++iblk == nb) { iblk = 0; ++irow; }
@@ -907,6 +912,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (timer) {
       const unsigned long long t = gtimer();
       atomicAdd(&c.phase_ns[ph], t - t_last);
+      if (sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * 8 + ph] += t - t_last;
       t_last = t;
     }
   };
@@ -1263,6 +1269,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (ext_ent) atomicAdd(&c.counters[CNT_EXT_ENTRIES], ext_ent);
     if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
+    if (timer && sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * 8 + 7] += (unsigned long long)steps;
     if (ring_steps) atomicAdd(&c.counters[CNT_RING_STEPS], ring_steps);
   }
   TRACE(40);
@@ -1345,7 +1352,11 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         }
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort[s & 1] = abort;
-      if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) atomicAdd(&c.phase_ns[PH_START], gtimer() - w0);
+      if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) {
+        const unsigned long long dw = gtimer() - w0;
+        atomicAdd(&c.phase_ns[PH_START], dw);
+        if (s < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + s * 8 + PH_START] += dw;
+      }
     }
     TRACE(50);
     cl.sync();

@@ -14,7 +14,7 @@ import torch  # noqa: E402
 from paper_1903_11554_b200 import TTCross  # noqa: E402
 from workloads import WORKLOADS  # noqa: E402
 
-for name in sys.argv[1:] or ["D5"]:
+for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["D5"]:
     wl = WORKLOADS[name]
     job = int(os.environ.get("TTC_PHASE_JOB", (wl.d - 1) // 2))
     os.environ["TTC_PHASE_JOB"] = str(job)
@@ -29,12 +29,15 @@ for name in sys.argv[1:] or ["D5"]:
     tt.set_timing(True)
     tt.solve_launch(wl.alg6_sweeps, graph=False)
     tt.integrate_read()
-    ph = tt.phase_times()
+    ph, log = tt.phase_times(per_sweep=True)
     kt = tt.kernel_times()
     tt.set_timing(False)
     nl = max(1.0, ph.pop("launches"))
     per = {k: round(v / nl, 2) for k, v in ph.items()}
     print(json.dumps({"workload": name, "job": job, "shape": tt.launch_shape(), "k_sweep_us": kt["k_sweep"][1] * 1e3 / kt["k_sweep"][0],
                       "phase_us_per_launch": per, "rook_steps": tt.stats()["rook_steps"]}), flush=True)
+    if "--log" in sys.argv:
+        for s, row in enumerate(log):
+            print(json.dumps({"workload": name, "job": job, "sweep": s, **row}), flush=True)
     tt.close()
     os.environ.pop("TTC_PHASE_JOB")

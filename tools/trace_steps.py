@@ -66,6 +66,42 @@ def analyse(ev, cnt, G, njobs):
     return out
 
 
+def per_sweep(ev, cnt, G, job, sweeps):
+    """CTA 0 of `job`: one row per sweep, us from the sweep's loop point (49) to each phase
+    boundary: nbr wait, tables, extension, samples, rook search, final, and the column/row
+    steps (count, us)."""
+    b = job * G
+    m = min(int(cnt[b]), ev.shape[1])
+    pts = (ev[b, :m] >> np.uint64(56)).astype(int)
+    ts = (ev[b, :m] & np.uint64((1 << 56) - 1)).astype(np.int64)
+    rows, cur = [], None
+    for i in range(m):
+        p, t = pts[i], ts[i]
+        if p == 49:
+            if cur:
+                rows.append(cur)
+            cur = {"t0": t, "marks": {}, "steps": 0, "step_us": 0.0, "last_step": None}
+        elif cur is not None:
+            cur["marks"].setdefault(p, t)
+            if p in (10, 20):
+                cur["last_step"] = t
+            elif p == 34 and cur["last_step"] is not None:
+                cur["steps"] += 1
+                cur["step_us"] += (t - cur["last_step"]) / MHZ
+                cur["last_step"] = None
+    if cur:
+        rows.append(cur)
+    out = []
+    for s, r in enumerate(rows):
+        mk = r["marks"]
+        def at(p):
+            return (mk[p] - r["t0"]) / MHZ if p in mk else None
+        out.append({"sweep": s, "wait": at(51), "tables": at(3), "extend": at(5), "samples": at(7),
+                    "rook": at(8), "final": at(9), "end": at(40), "steps": r["steps"],
+                    "step_us": round(r["step_us"], 1)})
+    return out
+
+
 def main():
     args = sys.argv[1:]
     light = "--heavy" not in args
@@ -107,6 +143,11 @@ def main():
         print(json.dumps({"workload": name, "shape": shape, "events_cta0": int(cnt[0]), "span_us": total,
                           "per_job_us": {j: dict(list(v.items())[:24]) for j, v in res.items() if j < 4}}),
               flush=True)
+        for job in sorted({0, njobs // 2, njobs - 1}):
+            for row in per_sweep(ev, cnt, G, job, wl.alg6_sweeps):
+                print(json.dumps({"workload": name, "job": job,
+                                  **{k: (round(v, 1) if isinstance(v, float) else v) for k, v in row.items()}}),
+                      flush=True)
         tt.close()
 
 
