@@ -252,8 +252,8 @@ int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, 
  * column/row + append, exit barrier], us_out[7] = sweeps measured, us_out[8..11] = [column
  * evaluation, column argmax (CTA + cluster), row evaluation, row argmax] summed over the search
  * steps, us_out[12..13] = [raw entries, recurrence] of the extension's row tiles (written when
- * count >= 14); with count >= 14 + 8*256 also a per-sweep log: us_out[14 + 8*s + p] = phase p
- * (0..6 as above) of sweep s < 256, us_out[14 + 8*s + 7] = its rook steps.  count >= 12.
+ * count >= 14); with count >= 14 + 16*256 also a per-sweep log: us_out[14 + 16*s + p] = slot p
+ * (0..13 as above) for sweep s < 256 alone, except slot 7 = the sweep's rook rounds.  count >= 12.
  * Reset by tt_cross_set_timing(1). */
 int tt_cross_get_phase_times(ttc_ctx* ctx, double* us_out, int32_t count);
 

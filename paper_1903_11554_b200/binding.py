@@ -290,7 +290,7 @@ class TTCross:
     def phase_times(self, per_sweep=False):
         """k_sweep phase clocks (us, CTA 0 of superblock TTC_PHASE_JOB, default the first) accumulated
         while timing is on; per_sweep=True also returns the per-sweep log (a list of dicts)."""
-        nw = 14 + 8 * 256
+        nw = 14 + 16 * 256
         out = np.zeros(nw)
         _check(self.lib, self.lib.tt_cross_get_phase_times(self._h, out.ctypes.data_as(ctypes.c_void_p), nw),
                "tt_cross_get_phase_times")
@@ -299,8 +299,8 @@ class TTCross:
         tot = dict(zip(names, out[:14].tolist()))
         if not per_sweep:
             return tot
-        log = out[14:].reshape(256, 8)
-        rows = [dict(zip(names[:7] + ["steps"], [round(x, 2) for x in r.tolist()])) for r in log]
+        log = out[14:].reshape(256, 16)[:, :14]
+        rows = [dict(zip(names[:7] + ["rounds"] + names[8:], [round(x, 2) for x in r.tolist()])) for r in log]
         while rows and not any(rows[-1].values()):
             rows.pop()
         return tot, rows

@@ -1,5 +1,7 @@
 // ttc_api.cu -- host side of libttcross: context, memory, launch sequences, C-ABI
 // (include/ttcross.h).  One translation unit; compiled for sm_100a only.
+#include <cuda.h>          // CUtensorMap and its enums (types only: the driver entry point is
+#include <cudaTypedefs.h>  // fetched at run time, libcuda is not linked)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -569,11 +571,15 @@ int ttc_trace_read(unsigned long long* events, int* counts) {
 }
 #endif
 
-// diagnostics: q_pre[i] = div_pre(a[i], b[i], rcp_refined(b[i])), q_ieee[i] = __ddiv_rn(a[i], b[i])
+// diagnostics: q_pre[i] = div_pre_fast (when its test passes) else div_pre, both with
+// rcp_refined(b[i]); q_ieee[i] = __ddiv_rn(a[i], b[i])
 namespace ttc {
 __global__ void k_selftest_division(const double* a, const double* b, double* qp, double* qi, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    qp[i] = div_pre(a[i], b[i], rcp_refined(b[i]));
+    const double r2 = rcp_refined(b[i]);
+    bool ok;
+    const double q = div_pre_fast(a[i], b[i], r2, ok);   // (the extension's branch-free path)
+    qp[i] = ok ? q : div_pre(a[i], b[i], r2);
     qi[i] = __ddiv_rn(a[i], b[i]);
   }
 }
@@ -640,7 +646,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   dc.kb = c->kb;
   dc.ke = c->ke;
   dc.RS = 1 + cap * d + 2 * cap;
-  dc.sbn = (long long)cap * n;
+  // row / column capacity of a superblock, padded to an even count: the u/v factor rows
+  // (stride sbn doubles) then start 16-byte aligned, as the TMA tensor maps need
+  dc.sbn = ((long long)cap * n + 1) & ~1LL;
   dc.G = 1;  // cluster size of k_sweep, chosen below once the device is known
   c->slots = d;
   c->nrec = d - 1;   // record i = interface i
@@ -764,9 +772,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       const int j = std::atoi(e);
       dc.phase_job = (j >= 0 && j < nj) ? j : 0;
     }
-    if (const char* e = std::getenv("TTC_GREEDY_G")) {
+    if (const char* e = std::getenv("TTC_GREEDY_G")) {   // (experiments: any cluster size 1..16)
       const int g = std::atoi(e);
-      if (g >= 1 && g <= 16 && (g & (g - 1)) == 0) G = g;
+      if (g >= 1 && g <= 16) G = g;
     }
     auto cache_for = [&](int g) -> size_t {
       const long long rpcap = (dc.sbn + g - 1) / g;
@@ -775,8 +783,10 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     const size_t ext_bytes = (size_t)extend_smem_doubles(cap) * sizeof(double);
     const size_t smem_lim = 180 * 1024;
     // the non-cached variant also holds the rook steps' DotRing (at least 4 terms per stage)
+    // (TTC_RING_KB: experiments with a larger ring in the non-cached shape)
+    const size_t ring_min = std::getenv("TTC_RING_KB") ? (size_t)std::atoi(std::getenv("TTC_RING_KB")) * 1024 : 0;
     auto smem_for = [&](int g, bool cached) -> size_t {
-      return std::max(ext_bytes, cached ? cache_for(g) : (size_t)RING_P * 4 * T * sizeof(double));
+      return std::max(ext_bytes, cached ? cache_for(g) : std::max(ring_min, (size_t)RING_P * 4 * T * sizeof(double)));
     };
     // T = threads per CTA; kernels are compiled for 256 (two CTAs per SM) and 512 (one)
     auto fn_for = [&](bool cached) -> const void* {
@@ -838,6 +848,18 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     c->greedy_cached = cached;
     c->greedy_smem = smem_for(G, cached);
     dc.ring_tb = (int)std::min<size_t>(8, c->greedy_smem / (sizeof(double) * RING_P * T));
+    // TMA ring: 16 terms per stage when two stages per warp fit (D_20: 20.8 ms vs 24.0 with 8
+    // terms x 4 stages, C_200 5.39 vs 6.01; profiles/r02_ring_shape.log)
+    if (TTC_TMA && !cached && c->greedy_smem >= 2 * 16 * (size_t)T * sizeof(double)) dc.ring_tb = 16;
+    if (const char* e = std::getenv("TTC_RING_TB")) {   // (experiments: terms per ring stage)
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= 64 && (size_t)v * 2 * T * sizeof(double) <= c->greedy_smem) dc.ring_tb = v;
+    }
+    // TMA ring (non-cached shape): stages of T rows x ring_tb terms in the same dynamic shared
+    // memory, as many as fit (<= TMA_PMAX); TTC_NO_TMA=1 keeps the cp.async DotRing (A/B)
+    dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / (T / 32)),
+                                      c->greedy_smem / (sizeof(double) * (size_t)T * dc.ring_tb));
+    dc.tma = TTC_TMA && !cached && dc.ring_p >= 2;
     dc.ext_tile = extend_tile_rows(cap);
     c->greedy_fn = fn_for(c->greedy_cached);
     {
@@ -861,6 +883,37 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       c->persistent = k.world == 1 && resident_of(c->sweeps_fn, G, cached) >= nj && resident(G, cached) >= nj &&
                       !std::getenv("TTC_NO_PERSISTENT");
     }
+  }
+  if (dc.tma) {
+    // 2-D tensor maps of U and V: dims {sbn (x, fastest), jobs * cap (t of job j at j*cap + t)},
+    // boxes of {32, ring_tb} doubles: a warp's rows (see TmaRing)
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return bail(fail(TTC_ERR_CUDA, "cuTensorMapEncodeTiled: driver entry point not found"));
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    CUtensorMap maps[2];
+    const int T = c->greedy_threads;
+    const cuuint32_t bw = 32;   // a warp's rows (TmaRing: one ring per warp)
+    const cuuint64_t dims[2] = {(cuuint64_t)dc.sbn, (cuuint64_t)nj * cap};
+    const cuuint64_t strides[1] = {(cuuint64_t)dc.sbn * sizeof(double)};
+    const cuuint32_t box[2] = {bw, (cuuint32_t)dc.ring_tb};
+    const cuuint32_t estr[2] = {1, 1};
+    double* bases[2] = {dc.U, dc.V};
+    for (int i = 0; i < 2; ++i) {
+      const CUresult cr = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, bases[i], dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS)
+        return bail(fail(TTC_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)cr) + ")"));
+    }
+    unsigned char* dmaps = nullptr;
+    if ((e = dalloc(c, &dmaps, sizeof(maps)))) return bail(e);
+    if (cudaMemcpy(dmaps, maps, sizeof(maps), cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(TTC_ERR_CUDA, "tensor map upload failed"));
+    dc.tmapU = dmaps;
+    dc.tmapV = dmaps + sizeof(CUtensorMap);
   }
   int rc = tt_cross_load_grid(c, nodes_u, weights, mem_kind);
   if (rc) return bail(rc);
@@ -1139,7 +1192,7 @@ int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
                      c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int i = 0; i < TTC_PHASE_WORDS && i < count; ++i) {
-    const bool is_count = i == PH_LAUNCHES || (i >= TTC_NPHASES && (i - TTC_NPHASES) % 8 == 7);
+    const bool is_count = i == PH_LAUNCHES || (i >= TTC_NPHASES && (i - TTC_NPHASES) % TTC_LOG_W == PH_LAUNCHES);
     us_out[i] = is_count ? (double)v[i] : v[i] * 1e-3;
   }
   return TTC_OK;

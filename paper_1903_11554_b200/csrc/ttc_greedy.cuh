@@ -251,11 +251,23 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
     if (c.family == 1) {
       const double uo = c.u[mode_own * n + a], ux = c.u[mode_oth * n + a];
       DDE p = sP, q = dde_one();
+      bool ok = true;
 #pragma unroll 2
-      for (int t = lo; t < hi; ++t) {
+      for (int t = lo; t < hi; ++t) {   // (branch-free rho: the two chains and consecutive t overlap)
         const double x = t - lo < 64 ? sX[t - lo] : c.u[t * n + T[t]];
-        dde_mul_d(p, rho(uo, x));   // (inline: the two chains and consecutive t overlap)
-        dde_mul_d(q, rho(ux, x));
+        bool o1, o2;
+        dde_mul_d(p, rho_fast(uo, x, o1));
+        dde_mul_d(q, rho_fast(ux, x, o2));
+        ok = ok && o1 && o2;
+      }
+      if (!ok) {   // (a division off its fast path: the chains again with the IEEE division)
+        p = sP;
+        q = dde_one();
+        for (int t = lo; t < hi; ++t) {
+          const double x = t - lo < 64 ? sX[t - lo] : c.u[t * n + T[t]];
+          dde_mul_d(p, rho(uo, x));
+          dde_mul_d(q, rho(ux, x));
+        }
       }
       if (side == 0) { c.PA[o + a] = p; c.QL1[o + a] = q; }
       else { c.PB[o + a] = p; c.QR0[o + a] = q; }
@@ -290,6 +302,35 @@ __device__ __forceinline__ double sb_entry(const DevCtx& c, int job, int k, int 
   return dde_div(p, SS);
 }
 
+// sb_entry with the divisions on their branch-free fast paths (ok: the bits of sb_entry; !ok:
+// the caller recomputes with sb_entry, out of its hot loop)
+template <int FAMILY>
+__device__ __forceinline__ double sb_entry_fast(const DevCtx& c, int job, int k, int al, int a, int be, int b,
+                                                bool& ok) {
+  if (FAMILY >= 2) {
+    ok = true;
+    return sb_entry<FAMILY>(c, job, k, al, a, be, b);
+  }
+  const int n = c.n;
+  const long long oa = ((long long)job * c.cap + al) * n;
+  const long long ob = ((long long)job * c.cap + be) * n;
+  ESum s = c.SA[oa + a];
+  esum_add(s, c.SB[ob + b]);
+  const double S = esum_round(s);
+  const double SS = __dmul_rn(S, S);
+  if (FAMILY == 0) return div_pre_fast(1.0, SS, rcp_refined(SS), ok);   // = __drcp_rn(SS) when ok
+  DDE p = c.PA[oa + a];
+  dde_mul(p, c.PB[ob + b]);
+  dde_mul(p, c.CX[((long long)job * c.cap + al) * c.cap + be]);
+  dde_mul(p, c.QL1[oa + b]);
+  dde_mul(p, c.QR0[ob + a]);
+  bool o1, o2;
+  dde_mul_d(p, rho_fast(c.u[k * n + a], c.u[(k + 1) * n + b], o1));
+  const double v = dde_div_fast(p, SS, o2);
+  ok = o1 && o2;
+  return v;
+}
+
 // pivot positions of interface k: xs = alpha_s*n + a_s, ys = beta_s*n + b_s
 __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x, int& y) {
   const int* T = rec_piv(c.rec_cur, c.RS, k) + (long long)s * c.d;
@@ -311,12 +352,16 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
+#ifndef EXT_WARP
+#define EXT_WARP 0   // 1: phase 2 in registers, a warp per row group (extend_side_warp; measured
+                     // D_20 -1..+3%, C_200 +25%: off)
+#endif
 #ifndef EXT_ILP
 #define EXT_ILP 4   // raw entries per thread per iteration of the extension
 #endif
 
 template <int FAMILY>
-__device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int side, int r, int x_lo, int x_hi,
+__device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo, int x_hi,
                             const int* p_al, const int* p_a, const double* pdiag, const double* prcp,
                             double* coef, double* tile,
                             unsigned long long& ent, unsigned long long& upd) {
@@ -342,7 +387,7 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
   auto clock_to = [&](int ph) {
     if (timer) {
       const unsigned long long t = gtimer();
-      atomicAdd(&c.phase_ns[ph], t - tm);
+      ph_add(c.phase_ns, sweep, ph, t - tm);
       tm = t;
     }
   };
@@ -374,18 +419,29 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
       for (; e + (EXT_ILP - 1) * B < ne; e += EXT_ILP * B) {
         double v[EXT_ILP];
         int at[EXT_ILP];
+        bool ok[EXT_ILP];
 #pragma unroll
-        for (int u = 0; u < EXT_ILP; ++u) {
+        for (int u = 0; u < EXT_ILP; ++u) {   // (branch-free: the EXT_ILP chains interleave)
           const int eu = e + u * B;
           const int s = eu / nrow, j = eu - s * nrow;
           const int x = x0 + j;
           const int al = x / n, a = x - al * n;
-          v[u] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
-                           : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+          v[u] = side == 0 ? sb_entry_fast<FAMILY>(c, job, k, al, a, p_al[s], p_a[s], ok[u])
+                           : sb_entry_fast<FAMILY>(c, job, k, p_al[s], p_a[s], al, a, ok[u]);
           at[u] = s * TS + j;
         }
 #pragma unroll
-        for (int u = 0; u < EXT_ILP; ++u) tile[at[u]] = v[u];
+        for (int u = 0; u < EXT_ILP; ++u) {
+          if (!ok[u]) {
+            const int eu = e + u * B;
+            const int s = eu / nrow, j = eu - s * nrow;
+            const int x = x0 + j;
+            const int al = x / n, a = x - al * n;
+            v[u] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                             : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+          }
+          tile[at[u]] = v[u];
+        }
       }
 #pragma unroll 1
       for (; e < ne; e += B) {
@@ -434,6 +490,167 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int job, int k, int si
   upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
 }
 
+// Phase 2, register variant (EXT_WARP), in batches of nw * EXT_RW rows:
+//   (1) the raw entries A(x, y_s) (A(x_s, y)) of the batch, spread over all threads of the CTA
+//       (EXT_ILP independent entry chains per thread) into the tile [s][TS] -- the batched
+//       fiber evaluation;
+//   (2) a warp per EXT_RW rows runs the recurrence in registers, lane l holding s = l and
+//       s = l + 32 (cap <= 64): for t = 0..r-1 the owner lane of t (t mod 32) has the final
+//       value of s = t (u_t; columns: v_t = acc_t / u_t(x_t), div_pre in every lane) -> warp
+//       shuffle -> every lane subtracts f * coef[t][s] from its s > t.  The rows are
+//       independent chains, interleaved (the division's slow-path test is warp-uniform, so the
+//       fast path is branch-free across rows).  Per s: the same subtractions in the same t
+//       order as the oracle's u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s), hence the same bits;
+//   (3) the final values (columns: acc_s / u_s(x_s)) back to the tile, then coalesced stores.
+#ifndef EXT_RW
+#define EXT_RW 4   // rows per warp per batch
+#endif
+template <int FAMILY>
+__device__ __noinline__ void extend_side_warp(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
+                                              int x_hi,
+                                              const int* p_al, const int* p_a, const double* pdiag,
+                                              const double* prcp, double* coef, double* tile,
+                                              unsigned long long& ent, unsigned long long& upd) {
+  const int n = c.n, cap = c.cap;
+  const int sbn = (int)c.sbn;
+  double* U = c.U + (long long)job * cap * sbn;
+  double* V = c.V + (long long)job * cap * sbn;
+  if (x_lo >= x_hi) return;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int t = e / r, s = e - t * r;
+    double v = 0.0;
+    if (t < s) {
+      const int q = p_al[s] * n + p_a[s];
+      v = side == 0 ? V[t * sbn + q] : U[t * sbn + q];
+    }
+    coef[t * cap + s] = v;
+  }
+  double* dst = side == 0 ? U : V;
+  const bool timer = c.phase_ns && job == c.phase_job && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0;
+  unsigned long long tm = timer ? gtimer() : 0;
+  auto clock_to = [&](int ph) {
+    if (timer) {
+      const unsigned long long t = gtimer();
+      ph_add(c.phase_ns, sweep, ph, t - tm);
+      tm = t;
+    }
+  };
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int s0 = lane, s1 = lane + 32;
+  const bool h0 = s0 < r, h1 = s1 < r;
+  const int BR = min(nw * EXT_RW, c.ext_tile), TS = BR + 1;   // batch rows (<= the tile capacity), stride
+#pragma unroll 1
+  for (int x0 = x_lo; x0 < x_hi; x0 += BR) {
+    const int nrow = min(BR, x_hi - x0);
+    // (1) raw entries of the batch, EXT_ILP per thread per iteration
+    {
+      const int ne = nrow * r, B = blockDim.x;
+      int e = threadIdx.x;
+#pragma unroll 1
+      for (; e + (EXT_ILP - 1) * B < ne; e += EXT_ILP * B) {
+        double v[EXT_ILP];
+        int at[EXT_ILP];
+        bool ok[EXT_ILP];
+#pragma unroll
+        for (int u = 0; u < EXT_ILP; ++u) {   // (branch-free: the EXT_ILP chains interleave)
+          const int eu = e + u * B;
+          const int s = eu / nrow, j = eu - s * nrow;
+          const int x = x0 + j;
+          const int al = x / n, a = x - al * n;
+          v[u] = side == 0 ? sb_entry_fast<FAMILY>(c, job, k, al, a, p_al[s], p_a[s], ok[u])
+                           : sb_entry_fast<FAMILY>(c, job, k, p_al[s], p_a[s], al, a, ok[u]);
+          at[u] = s * TS + j;
+        }
+#pragma unroll
+        for (int u = 0; u < EXT_ILP; ++u) {
+          if (!ok[u]) {
+            const int eu = e + u * B;
+            const int s = eu / nrow, j = eu - s * nrow;
+            const int x = x0 + j;
+            const int al = x / n, a = x - al * n;
+            v[u] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                             : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+          }
+          tile[at[u]] = v[u];
+        }
+      }
+#pragma unroll 1
+      for (; e < ne; e += B) {
+        const int s = e / nrow, j = e - s * nrow;
+        const int x = x0 + j;
+        const int al = x / n, a = x - al * n;
+        tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
+                                     : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
+      }
+    }
+    __syncthreads();
+    clock_to(PH_EXT_RAW);
+    // (2) the recurrence, EXT_RW rows per warp in registers
+    const int j0 = warp * EXT_RW;
+    if (j0 < nrow) {   // (warp-uniform)
+      double v0[EXT_RW], v1[EXT_RW];
+#pragma unroll
+      for (int i = 0; i < EXT_RW; ++i) {
+        const int j = min(j0 + i, nrow - 1);   // (a ragged group repeats its last row; not written back)
+        v0[i] = h0 ? tile[s0 * TS + j] : 0.0;
+        v1[i] = h1 ? tile[s1 * TS + j] : 0.0;
+      }
+#pragma unroll 1
+      for (int t = 0; t < r; ++t) {
+        const int owner = t & 31;
+        const bool hi = t >= 32;
+        const double c0 = h0 ? coef[t * cap + s0] : 0.0;
+        const double c1 = h1 ? coef[t * cap + s1] : 0.0;
+        const bool u0 = h0 && s0 > t, u1 = h1 && s1 > t;
+        double f[EXT_RW];
+#pragma unroll
+        for (int i = 0; i < EXT_RW; ++i) f[i] = __shfl_sync(0xffffffffu, hi ? v1[i] : v0[i], owner);
+        if (side == 1) {   // v_t = acc_t / u_t(x_t): div_pre, its slow path taken warp-uniformly
+          const double dg = pdiag[t], rc = prcp[t];
+          bool ok = true;
+#pragma unroll
+          for (int i = 0; i < EXT_RW; ++i) {
+            bool o;
+            const double q = div_pre_fast(f[i], dg, rc, o);
+            ok &= o;
+            f[i] = q;
+          }
+          if (!__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int i = 0; i < EXT_RW; ++i) {
+              const double a = __shfl_sync(0xffffffffu, hi ? v1[i] : v0[i], owner);
+              f[i] = div_pre(a, dg, rc);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < EXT_RW; ++i) {
+          if (u0) v0[i] = __dsub_rn(v0[i], __dmul_rn(f[i], c0));
+          if (u1) v1[i] = __dsub_rn(v1[i], __dmul_rn(f[i], c1));
+        }
+      }
+      // (3) final values back to the tile (columns: acc_s / u_s(x_s))
+#pragma unroll
+      for (int i = 0; i < EXT_RW; ++i) {
+        const int j = j0 + i;
+        if (j < nrow) {
+          if (h0) tile[s0 * TS + j] = side == 1 ? div_pre(v0[i], pdiag[s0], prcp[s0]) : v0[i];
+          if (h1) tile[s1 * TS + j] = side == 1 ? div_pre(v1[i], pdiag[s1], prcp[s1]) : v1[i];
+        }
+      }
+    }
+    __syncthreads();
+    clock_to(PH_EXT_REC);
+    for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
+      const int s = e / nrow, j = e - s * nrow;
+      dst[s * sbn + x0 + j] = tile[s * TS + j];
+    }
+    __syncthreads();
+  }
+  ent += (unsigned long long)(x_hi - x_lo) * r;
+  upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
+}
+
 // phase-2 tile rows and dynamic shared memory: coef [cap][cap] + tile [cap][rows + 1]
 __host__ __device__ __forceinline__ int extend_tile_rows(int cap) {
   const long long rows = (EXT_SMEM_DOUBLES - (long long)cap * cap) / cap - 1;
@@ -447,6 +664,8 @@ __host__ __device__ __forceinline__ long long extend_smem_doubles(int cap) {
 // k_sweep phase 3 (Alg. 2): helpers
 // ---------------------------------------------------------------------------------------
 #define GREEDY_MAX_THREADS 512
+#define TMA_PMAX 16   // stages of the TMA ring (at most)
+#define TMA_NBAR 128  // TMA ring barriers: warps x stages
 #define STAGE_N 1024  // n up to which the n-indexed factor of a step is staged in shared memory
 
 struct Cand {
@@ -504,6 +723,7 @@ struct GreedySmem {
   DDE fp;                            // PB[beta][b] or PA[alpha][a]
   double pv;                         // E(x*, y*) of the final pivot (owner CTA of column y*)
   double pa;                         // A(x*, y*) (CACHED: owner CTA of row x*)
+  unsigned long long rfull[TMA_NBAR];   // TMA ring: stage landed (1 arrival + the box bytes), [warp][P]
 };
 
 // asynchronous global -> shared copies (LDGSTS): the whole cache fill is one round trip
@@ -526,6 +746,17 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 // Layout: buf[stage][i][T] (conflict-free per warp).  Stage s = (row j, term block b), row-major.
 #define RING_P 4
 #define RING_MIN_ROWS 4   // rows per thread from which a step streams through the ring
+// L2 evict_first hint on the factor stream (TMA ring only).  For cp.async with
+// .L2::cache_hint, ptxas 12.9 (sm_100a) emits LDGSTS whose cache-policy operand names uniform
+// registers the policy was never written to (SASS in profiles/r02_illegal_instruction.txt): a
+// garbage descriptor, "illegal instruction" in some builds -- the DotRing therefore streams
+// without a hint.  UTMALDG takes the policy registers correctly.
+#ifndef TTC_TMA
+#define TTC_TMA 1   // the rook steps stream through the TMA ring (0: the per-thread cp.async DotRing)
+#endif
+#ifndef TTC_EVICT_FIRST
+#define TTC_EVICT_FIRST 1
+#endif
 // L2 policy of the stream: the u/v factors of all superblocks exceed the
 // 126 MB L2 many times over (D_20 640 MB, C_200 840 MB), so no factor line survives in L2
 // until the superblock's next step anyway.  EVICT_FIRST loads them evict_first, so the stream
@@ -592,6 +823,105 @@ struct DotRing {
   }
 };
 
+// TMA ring of the non-cached rook steps (c.tma), one ring per warp: a warp's u/v factor
+// stream F[t][x] (its 32 rows x of each row block, t = 0..r-1) is cut into stages of tb terms,
+// each one 2-D box {32, tb} of F's tensor map (dims {sbn, jobs * cap}: x fastest, one row per
+// (job, t)), landing as [tb][32] in the warp's part of the shared-memory ring.  Lane 0 issues
+// stage q + P - 1 (cp.async.bulk.tensor, complete_tx on the warp's rfull[slot], L2 evict_first
+// for the t-form families) when the warp starts consuming stage q -- the slot of stage q - 1,
+// which every lane finished reading before the __syncwarp that ends it; every lane waits on
+// rfull and reads back its own row's terms.  Warps never wait for each other (the cp.async
+// DotRing's property, without its 8-byte copy per thread and term).  The ring position
+// (slot, phase) is the same in every thread and persists across steps and sweeps (RingPos).
+struct RingPos {
+  int slot;
+  unsigned phase;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(const unsigned long long* b, unsigned parity) {
+  const unsigned a = smem_u32(b);
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred q;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, q;\n}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void tma_ring_init(GreedySmem* S) {
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < TMA_NBAR; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S->rfull[q])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // (ordered before any use by the kernel's first cluster barrier)
+}
+
+template <bool EVICT_FIRST>
+struct TmaRing {
+  double* wbuf;               // this warp's P stages of [tb][32]
+  const void* tmap;
+  unsigned long long* full;   // this warp's P barriers
+  int lane, tb, P, nb, r, ybase, x0, T;
+  int total, is;              // stages of this step, issued (lane 0)
+  RingPos pos, ipos;          // consumption / issue position
+  __device__ __forceinline__ void start(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
+                                        int P_, int r_, int ybase_, int xb, int xe, RingPos p) {
+    const int warp = tid >> 5;
+    lane = tid & 31;
+    tmap = tmap_; T = T_; tb = tb_; P = P_; r = r_; ybase = ybase_;
+    wbuf = buf + (long long)warp * P * tb * 32;
+    full = &S->rfull[warp * P];
+    x0 = xb + warp * 32;
+    nb = (r + tb - 1) / tb;
+    total = xe > xb ? ((xe - xb + T - 1) / T) * nb : 0;
+    pos = p;
+    ipos = p;
+    is = 0;
+    if (lane == 0)
+      for (int q = 0; q < P - 1 && is < total; ++q) issue();
+  }
+  __device__ __forceinline__ void issue() {   // lane 0: stage `is` into slot ipos
+    const int jb = is / nb, b = is - jb * nb;
+    const unsigned fa = smem_u32(&full[ipos.slot]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fa), "r"(tb * 256) : "memory");
+    const unsigned dst = smem_u32(wbuf + ipos.slot * tb * 32);
+    const int x = x0 + jb * T, y = ybase + b * tb;
+    if (EVICT_FIRST) {
+      unsigned long long pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(fa), "l"(pol)
+          : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(fa)
+          : "memory");
+    }
+    ++is;
+    if (++ipos.slot == P) { ipos.slot = 0; ipos.phase ^= 1u; }
+  }
+  // e -= F[t][row] * vec[t], t = 0 .. r-1 in order, for this thread's row of the next row
+  // block (every lane of the warp calls this for every row block)
+  __device__ __forceinline__ double dot_sub(double e, const double* vec) {
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      if (lane == 0 && is < total) issue();
+      mbar_wait(&full[pos.slot], pos.phase);
+      const double* src = wbuf + pos.slot * tb * 32 + lane;
+      const int t0 = b * tb, tn = min(tb, r - t0);
+      for (int i = 0; i < tn; ++i) e = __dsub_rn(e, __dmul_rn(src[i * 32], vec[t0 + i]));
+      __syncwarp();   // (the slot is refilled two issues later, by lane 0 of this warp)
+      if (++pos.slot == P) { pos.slot = 0; pos.phase ^= 1u; }
+    }
+    return e;
+  }
+};
+
 // dynamic shared memory of the CACHED variant (phase 3): own rows' U[t][x], SA, PA and own
 // columns' V[t][y], SB, PB stay on chip for the whole rook search, plus the E / raw values of
 // the last steps.  Phase 2 uses the same buffer first.
@@ -615,8 +945,11 @@ struct StepCtx {
   bool stage_n;
   unsigned long long rowmask, colmask;  // bit j: this thread's j-th row / column is a pivot's
   bool timer;                           // phase clock owner (tt_cross_get_phase_times)
-  double* ring;                         // non-cached: DotRing buffer (dyn, RING_P * ring_tb * T doubles)
+  double* ring;                         // non-cached: DotRing / TmaRing buffer (dyn)
   int ring_tb;                          // terms per ring stage
+  int ring_p;                           // TMA ring stages
+  bool tma;                             // stream through the TMA ring (else the cp.async DotRing)
+  RingPos* rpos;                        // TMA ring position (persists across steps and sweeps)
 };
 
 // column step E(:, y) on this CTA's rows -> U[r][:] (or the row cache), raw values; returns
@@ -650,12 +983,33 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   TRACE(11);
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  int jrow = 0;
-  DotRing<FAMILY <= 1> ring;
-  const bool use_ring = !CACHED && xe - xb >= RING_MIN_ROWS * T;
+  const bool stream = !CACHED && xe - xb >= RING_MIN_ROWS * T;
+#if TTC_TMA
+  // (one ring kind per build: both live at once cost ~1 KB of spills per thread)
+  constexpr bool use_ring = false;
+  const bool use_tma = stream && X.tma;   // (else plain loads)
+  TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> ring;
+  if (use_tma) ring.start(X.ring, c.tmapU, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, xb, xe, *X.rpos);
+#else
+  constexpr bool use_tma = false;
+  const bool use_ring = stream;
+  DotRing<false> ring;   // (no cache hint: see TTC_EVICT_FIRST)
   if (use_ring) ring.init(X.ring, X.U, T, tid, X.ring_tb, sbn, r, xb, xe);
+#endif
+#if TTC_TMA
+  // (the TMA ring's barriers count every warp: all threads run every row block, a thread
+  // past the last row computes a clamped duplicate and stores nothing)
+  const int nblk = xe > xb ? (xe - xb + T - 1) / T : 0;
+  #pragma unroll 1
+  for (int jrow = 0; jrow < nblk; ++jrow) {
+    const bool valid = xb + jrow * T + tid < xe;
+    const int x = valid ? xb + jrow * T + tid : xe - 1;
+#else
+  int jrow = 0;
   #pragma unroll 1
   for (int x = xb + tid; x < xe; x += T, ++jrow) {
+    constexpr bool valid = true;
+#endif
     const int al = x / n, a = x - al * n;
     const double ua = X.uk[a];
     double raw;
@@ -666,7 +1020,9 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       esum_add(s, S.fs);
       const double Sd = esum_round(s);
       const double SS = __dmul_rn(Sd, Sd);
-      raw = __drcp_rn(SS);
+      bool ok;
+      raw = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
+      if (!ok) raw = __drcp_rn(SS);
     } else {
       ESum s = CACHED ? X.SAc[x - xb] : c.SA[jo + x];
       esum_add(s, S.fs);
@@ -676,16 +1032,23 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[al]);
       dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + be * n + a]);
-      dde_mul_d(p, rho(ua, ub));
-      raw = dde_div(p, SS);
+      bool o1, o2;
+      DDE pr = p;
+      dde_mul_d(pr, rho_fast(ua, ub, o1));
+      raw = dde_div_fast(pr, SS, o2);
+      if (!(o1 && o2)) {
+        dde_mul_d(p, rho(ua, ub));
+        raw = dde_div(p, SS);
+      }
     }
     double e = raw;
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.Uc[t * rpcap + (x - xb)], S.vec[t]));
-    else if (use_ring)
+    else if (use_tma || use_ring)
       e = ring.dot_sub(e, S.vec);
     else
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(X.U[t * sbn + x], S.vec[t]));
+    if (!valid) continue;
     bool piv = jrow < 64 && ((X.rowmask >> jrow) & 1ULL);   // a pivot row (E is exactly 0 there)
     if (jrow >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.xs[t] == x);
@@ -699,6 +1062,9 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
     }
     if (cand_better(fabs(e), x, bv, bf)) { bv = fabs(e); bf = x; }
   }
+#if TTC_TMA
+  if (use_tma) *X.rpos = ring.pos;
+#endif
   bv_out = bv;
   bf_out = bf;
 }
@@ -733,12 +1099,31 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   TRACE(21);
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  int jcol = 0;
-  DotRing<FAMILY <= 1> ring;
-  const bool use_ring = !CACHED && ye - yb >= RING_MIN_ROWS * T;
+  const bool stream = !CACHED && ye - yb >= RING_MIN_ROWS * T;
+#if TTC_TMA
+  // (one ring kind per build: both live at once cost ~1 KB of spills per thread)
+  constexpr bool use_ring = false;
+  const bool use_tma = stream && X.tma;   // (else plain loads)
+  TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> ring;
+  if (use_tma) ring.start(X.ring, c.tmapV, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, yb, ye, *X.rpos);
+#else
+  constexpr bool use_tma = false;
+  const bool use_ring = stream;
+  DotRing<false> ring;   // (no cache hint: see TTC_EVICT_FIRST)
   if (use_ring) ring.init(X.ring, X.V, T, tid, X.ring_tb, sbn, r, yb, ye);
+#endif
+#if TTC_TMA
+  const int nblk = ye > yb ? (ye - yb + T - 1) / T : 0;
+  #pragma unroll 1
+  for (int jcol = 0; jcol < nblk; ++jcol) {
+    const bool valid = yb + jcol * T + tid < ye;
+    const int y = valid ? yb + jcol * T + tid : ye - 1;
+#else
+  int jcol = 0;
   #pragma unroll 1
   for (int y = yb + tid; y < ye; y += T, ++jcol) {
+    constexpr bool valid = true;
+#endif
     const int be = y / n, b = y - be * n;
     const double ub = X.uk1[b];
     double e;
@@ -749,7 +1134,9 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       esum_add(s, S.fs);
       const double Sd = esum_round(s);
       const double SS = __dmul_rn(Sd, Sd);
-      e = __drcp_rn(SS);
+      bool ok;
+      e = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
+      if (!ok) e = __drcp_rn(SS);
     } else {
       ESum s = CACHED ? X.SBc[y - yb] : c.SB[jo + y];
       esum_add(s, S.fs);
@@ -759,15 +1146,22 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[be]);
       dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + al * n + b]);
-      dde_mul_d(p, rho(ua, ub));
-      e = dde_div(p, SS);
+      bool o1, o2;
+      DDE pr = p;
+      dde_mul_d(pr, rho_fast(ua, ub, o1));
+      e = dde_div_fast(pr, SS, o2);
+      if (!(o1 && o2)) {
+        dde_mul_d(p, rho(ua, ub));
+        e = dde_div(p, SS);
+      }
     }
     if (CACHED)
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.Vc[t * rpcap + (y - yb)]));
-    else if (use_ring)
+    else if (use_tma || use_ring)
       e = ring.dot_sub(e, S.vec);   // (S.vec[t] * V[t][y]: the product commutes bitwise)
     else
       for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(S.vec[t], X.V[t * sbn + y]));
+    if (!valid) continue;
     bool piv = jcol < 64 && ((X.colmask >> jcol) & 1ULL);   // a pivot column
     if (jcol >= 64)
       for (int t = 0; t < r; ++t) piv |= (S.ys[t] == y);
@@ -776,6 +1170,9 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
     else X.V[r * sbn + y] = e;
     if (cand_better(fabs(e), y, bv, bf)) { bv = fabs(e); bf = y; }
   }
+#if TTC_TMA
+  if (use_tma) *X.rpos = ring.pos;
+#endif
   bv_out = bv;
   bf_out = bf;
 }
@@ -872,7 +1269,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
-                                          int rl, int rr, int* Rn, int& xstep, bool end_sync,
+                                          int rl, int rr, int* Rn, int& xstep, RingPos& rpos, bool end_sync,
                                           int rows_done, int cols_done, bool xy_known, bool release) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = c.G;
@@ -883,7 +1280,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   const int R = rl * n, C = rr * n;
   // rows / columns of this CTA (contiguous blocks); the cached variant's shared-memory
   // stride is the capacity block rpcap >= rpc, cpc
-  const int rpc = (R + G - 1) / G, cpc = (C + G - 1) / G;
+  // (TMA ring: even block sizes, so every CTA's first row starts a 16-byte aligned TMA box --
+  // an odd start raised "illegal instruction", tools/tma_probe.cu)
+  const int rpc = c.tma ? (((R + G - 1) / G + 1) & ~1) : (R + G - 1) / G;
+  const int cpc = c.tma ? (((C + G - 1) / G + 1) & ~1) : (C + G - 1) / G;
   const int rpcap = (int)((c.sbn + G - 1) / G);
   const int xb = cr * rpc, xe = min(R, xb + rpc);
   const int yb = cr * cpc, ye = min(C, yb + cpc);
@@ -911,8 +1311,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   auto phase = [&](int ph) {
     if (timer) {
       const unsigned long long t = gtimer();
-      atomicAdd(&c.phase_ns[ph], t - t_last);
-      if (sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * 8 + ph] += t - t_last;
+      ph_add(c.phase_ns, sweep, ph, t - t_last);
       t_last = t;
     }
   };
@@ -992,8 +1391,13 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       __syncthreads();
       const int lo = rows_done * n + rr_i * rchunk;
-      extend_side<FAMILY>(c, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
+#if EXT_WARP
+      extend_side_warp<FAMILY>(c, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
+                               ext_ent, ext_upd);
+#else
+      extend_side<FAMILY>(c, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
                           ext_ent, ext_upd);
+#endif
       __syncthreads();
     }
     if (do_cols) {   // columns: fixed index = pivot rows x_s, divisors u_s(x_s) (A(t0) at first)
@@ -1005,11 +1409,19 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       __syncthreads();
       const int lo = cols_done * n + cc_i * cchunk;
-      extend_side<FAMILY>(c, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
+#if EXT_WARP
+      extend_side_warp<FAMILY>(c, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
+                               ext_ent, ext_upd);
+#else
+      extend_side<FAMILY>(c, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
                           ext_ent, ext_upd);
+#endif
     }
   }
   TRACE(4);
+  // (the rook steps read U / V through the TMA engine -- the async proxy: order this thread's
+  // generic-proxy stores before the barrier that publishes them)
+  if (c.tma) asm volatile("fence.proxy.async.global;" ::: "memory");
   cl.sync();  // u / v of the new rows and columns visible to the whole cluster
   TRACE(5);
   phase(PH_EXTEND);
@@ -1145,7 +1557,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     }
     StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
               U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
-              timer, dyn, c.ring_tb};
+              timer, dyn, c.ring_tb, c.ring_p, c.tma != 0, &rpos};
     auto column = [&](int y, bool search) -> int {
       double bv;
       long long bf;
@@ -1163,8 +1575,8 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       argmax_step(&S, bv, bf, G, xstep);
       if (timer) {
-        atomicAdd(&c.phase_ns[PH_COL_EVAL], t1 - t0);
-        atomicAdd(&c.phase_ns[PH_COL_ARGMAX], gtimer() - t1);
+        ph_add(c.phase_ns, sweep, PH_COL_EVAL, t1 - t0);
+        ph_add(c.phase_ns, sweep, PH_COL_ARGMAX, gtimer() - t1);
       }
       ++xstep;
       return (int)S.best.idx;
@@ -1186,8 +1598,8 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       argmax_step(&S, bv, bf, G, xstep);
       if (timer) {
-        atomicAdd(&c.phase_ns[PH_ROW_EVAL], t1 - t0);
-        atomicAdd(&c.phase_ns[PH_ROW_ARGMAX], gtimer() - t1);
+        ph_add(c.phase_ns, sweep, PH_ROW_EVAL, t1 - t0);
+        ph_add(c.phase_ns, sweep, PH_ROW_ARGMAX, gtimer() - t1);
       }
       ++xstep;
       return (int)S.best.idx;
@@ -1253,6 +1665,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     publish(false, 0.0);
   }
 
+  if (c.tma) asm volatile("fence.proxy.async.global;" ::: "memory");   // (U[r], V[r] for the next sweep's TMA reads)
   phase(PH_FINAL);
   if (added && tid == 0) {   // the new pivot's position, for the next sweep of a persistent loop
     S.xs[r] = xst;
@@ -1269,7 +1682,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     if (ext_ent) atomicAdd(&c.counters[CNT_EXT_ENTRIES], ext_ent);
     if (ext_upd) atomicAdd(&c.counters[CNT_EXT_UPDATES], ext_upd);
     if (cr == 0 && steps) atomicAdd(&c.counters[CNT_ROOK_STEPS], (unsigned long long)steps);
-    if (timer && sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * 8 + 7] += (unsigned long long)steps;
+    if (timer && sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * TTC_LOG_W + PH_LAUNCHES] += (unsigned long long)steps;
     if (ring_steps) atomicAdd(&c.counters[CNT_RING_STEPS], ring_steps);
   }
   TRACE(40);
@@ -1292,7 +1705,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
 template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int sweep) {
   __shared__ GreedySmem S;
-  extern __shared__ double dyn[];
+  extern __shared__ __align__(1024) double dyn[];
   cg::cluster_group cl = cg::this_cluster();
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   const int r = rec_rank(c.rec_cur, c.RS, k);
@@ -1302,11 +1715,13 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   const int* Rc = c.rec_cur + (long long)k * c.RS;
   TRACE_INIT();
   xbar_init(&S);
+  tma_ring_init(&S);
   if (cl.block_rank() == 0)
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
-  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, true,
+  RingPos rpos{0, 0u};
+  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, rpos, true,
                                             c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false, false);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
@@ -1325,15 +1740,17 @@ template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
   __shared__ GreedySmem S;
   __shared__ int s_abort[2];   // by sweep parity: one cluster barrier per sweep start
-  extern __shared__ double dyn[];
+  extern __shared__ __align__(1024) double dyn[];
   cg::cluster_group cl = cg::this_cluster();
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   int* Rk = c.rec_cur + (long long)k * c.RS;
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
   int rdone = c.sbstate[job * 4 + 0], cdone = c.sbstate[job * 4 + 1];
   int xstep = 0;
+  RingPos rpos{0, 0u};
   TRACE_INIT();
   xbar_init(&S);  // ordered before remote use by the cluster barriers of the first sweep
+  tma_ring_init(&S);
   for (int s = s0; s < s0 + nsweeps; ++s) {
     TRACE_FLUSH();
     TRACE(49);
@@ -1353,9 +1770,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort[s & 1] = abort;
       if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) {
-        const unsigned long long dw = gtimer() - w0;
-        atomicAdd(&c.phase_ns[PH_START], dw);
-        if (s < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + s * 8 + PH_START] += dw;
+        ph_add(c.phase_ns, s, PH_START, gtimer() - w0);
       }
     }
     TRACE(50);
@@ -1374,7 +1789,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
     // (sweep_body publishes rank_ring[k] and releases done[k] as soon as the pivot is known)
-    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, s + 1 == s0 + nsweeps, rdone, cdone,
+    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
                                    s > s0, true);
     rdone = rl;   // (= the sbstate the sweep wrote)
     cdone = rr;

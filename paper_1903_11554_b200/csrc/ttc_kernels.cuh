@@ -267,13 +267,17 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
         const double S = esum_round(s);
         const double SS = __dmul_rn(S, S);
         double v;
+        bool ok;   // (branch-free divisions; the IEEE ones only for an entry off the fast path)
         if (FAMILY == 0) {
-          v = __drcp_rn(SS);
+          v = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
+          if (!ok) v = __drcp_rn(SS);
         } else {
           double ph = p0.hi, pl = p0.lo;
           dd_mul_raw(ph, pl, B.qlh[ra][a], B.qll[ra][a]);
           dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
-          v = dde_div(DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0}, SS);
+          const DDE pe = DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0};
+          v = dde_div_fast(pe, SS, ok);
+          if (!ok) v = dde_div(pe, SS);
         }
         if (EMIT) F[a0 + a] = v;
         const double wa = B.w[a];
