@@ -857,7 +857,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     }
     // TMA ring (non-cached shape): stages of T rows x ring_tb terms in the same dynamic shared
     // memory, as many as fit (<= TMA_PMAX); TTC_NO_TMA=1 keeps the cp.async DotRing (A/B)
-    dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / (T / 32)),
+    dc.ring_tb = std::max(1, dc.ring_tb);   // (cached shapes: the ring is not used)
+    dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / std::max(1, T / 32)),
                                       c->greedy_smem / (sizeof(double) * (size_t)T * dc.ring_tb));
     dc.tma = TTC_TMA && !cached && dc.ring_p >= 2;
     dc.ext_tile = extend_tile_rows(cap);

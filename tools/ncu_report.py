@@ -3,7 +3,7 @@
 speed-of-light, scheduler and warp-state sections, launch shape, the warp-stall breakdown
 from the source page and the per-launch DRAM traffic.  Also appends the traffic to
 profiles/ncu_traffic.json under --key, which bench.py reads for its roofline "traffic".
-Usage: ncu_report.py capture.ncu-rep title [--key WORKLOAD --out profiles/NAME.txt]
+Usage: ncu_report.py capture.ncu-rep title [--key WORKLOAD --out profiles/NAME.txt] [--kernel REGEX]
 (needs only the ncu CLI; the summary goes to stdout, --out names it in ncu_traffic.json)"""
 import collections
 import csv
@@ -21,13 +21,19 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
+KFILTER = []
+
+
 def ncu_csv(rep, *args):
-    out = subprocess.run(["ncu", "-i", rep, *args, "--csv"], capture_output=True, text=True, check=True).stdout
+    out = subprocess.run(["ncu", "-i", rep, *KFILTER, *args, "--csv"], capture_output=True, text=True,
+                         check=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
 
 def main():
     rep, title = sys.argv[1], sys.argv[2]
+    if "--kernel" in sys.argv:   # (a capture of several kernels: the one whose name matches)
+        KFILTER.extend(["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]])
     key = sys.argv[sys.argv.index("--key") + 1] if "--key" in sys.argv else None
     rows = ncu_csv(rep, "--page", "details")
     h = rows[0]
