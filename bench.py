@@ -226,11 +226,16 @@ def roofline(kt, stats, family, peaks, peak_src, modes=0, workload=None, cached=
            "peak_source": FP64_PEAK_SOURCE}
     out.update({"entries_per_launch": ent, "updates_per_launch": upd})
     if name == "k_sweep" and not cached:
-        # memory side: every u_t(x) v_t(y) term streams one factor (the other is staged),
-        # every entry writes its E (and the column its raw value): 8 B/term + 16 B/entry
-        gbs = (8 * upd + 16 * ent) / avg_s / 1e9
+        # memory side: in the samples and rook steps every u_t(x) v_t(y) term
+        # streams one factor from HBM (the other is staged) and every entry writes its E and raw
+        # value (16 B); the u/v extension works on chip and writes one 8-byte u/v value per entry
+        ext_e = stats["ext_entries"] / max(1, launches)
+        ext_u = stats["ext_updates"] / max(1, launches)
+        algo = 8 * (upd - ext_u) + 16 * (ent - ext_e) + 8 * ext_e
+        gbs = algo / avg_s / 1e9
         hbm = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-               "frac": gbs / peaks["hbm_gbs"], "per_unit": "8 B/update term + 16 B/entry",
+               "frac": gbs / peaks["hbm_gbs"], "bytes_per_launch": algo,
+               "per_unit": "8 B/streamed update term + 16 B/search entry + 8 B/extension entry",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
         main, other = (hbm, alu) if hbm["frac"] >= alu["frac"] else (alu, hbm)
         out.update(main)
@@ -269,7 +274,16 @@ def _oracle_update(args):
     return k, piv, par, info["evals"]
 
 
-def oracle_sample(wl, budget_s, cores=None):
+def oracle_pool(wl, cores=None):
+    """A process pool for oracle_sample (numpy single-threaded in every process)."""
+    import multiprocessing as mp
+    cores = cores or os.cpu_count() or 1
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    return mp.get_context("fork").Pool(cores, initializer=_oracle_init, initargs=(wl.name,)), cores
+
+
+def oracle_sample(wl, budget_s, cores=None, pool=None):
     """Run the oracle (test infrastructure, as it stands) on a bounded sample of the workload
     on `cores` host processes (numpy, one thread each); returns (evals, seconds, what, cores,
     solve_s or None).
@@ -280,18 +294,18 @@ def oracle_sample(wl, budget_s, cores=None):
     cross + one Alg. 2 step, Alg. 6), stopped after the sweep in
     which the budget runs out.
     """
-    import multiprocessing as mp
     from oracle import cross as X
-    cores = cores or os.cpu_count() or 1
     _oracle_init(wl.name)
     prob = _ORACLE_PROB
     nsw = wl.alg6_sweeps
-    evals, t0 = 0, time.perf_counter()
-    env = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
-    for k in env:
-        os.environ[k] = "1"
+    own = pool is None
+    if own:
+        pool, cores = oracle_pool(wl, cores)
+    else:
+        cores = cores or os.cpu_count() or 1
+    evals = 0
     try:
-        with mp.get_context("fork").Pool(cores, initializer=_oracle_init, initargs=(wl.name,)) as pool:
+        if True:
             t0 = time.perf_counter()
             if wl.d <= 8:
                 solves = 0
@@ -318,11 +332,9 @@ def oracle_sample(wl, budget_s, cores=None):
                     f"the first {sweeps} Alg. 6 sweeps from the rank-1 start (ranks up to {max(st.ranks)}), "
                     f"superblocks spread over {cores} processes", cores, None)
     finally:
-        for k, v in env.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        if own:
+            pool.close()
+            pool.join()
 
 
 def run_reference(args):
@@ -331,13 +343,16 @@ def run_reference(args):
         return
     wl = ALL_WORKLOADS[args.workload]
     budget = max(0.5, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    pool, cores = oracle_pool(wl)   # (one pool for the run: the workers start once)
     for _ in range(args.warmup):
-        oracle_sample(wl, budget)
-    tot_e, tot_s, what, cores = 0, 0.0, "", 1
+        oracle_sample(wl, budget, cores, pool)
+    tot_e, tot_s, what = 0, 0.0, ""
     for _ in range(args.steps):
-        e, s, what, cores, _ = oracle_sample(wl, budget)
+        e, s, what, cores, _ = oracle_sample(wl, budget, cores, pool)
         tot_e += e
         tot_s += s
+    pool.close()
+    pool.join()
     v = tot_e / tot_s
     line = {
         "impl": "reference", "metric": "integrand evals/sec (fp64)", "value": v, "unit": "evals/s",

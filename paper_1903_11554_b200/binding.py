@@ -299,8 +299,9 @@ class TTCross:
         tot = dict(zip(names, out[:14].tolist()))
         if not per_sweep:
             return tot
-        log = out[14:].reshape(256, 16)[:, :14]
-        rows = [dict(zip(names[:7] + ["rounds"] + names[8:], [round(x, 2) for x in r.tolist()])) for r in log]
+        log = out[14:].reshape(256, 16)
+        rows = [dict(zip(names[:7] + ["rounds"] + names[8:] + ["ext_rows_cta", "ext_cols_cta"],
+                         [round(x, 2) for x in r.tolist()])) for r in log]
         while rows and not any(rows[-1].values()):
             rows.pop()
         return tot, rows

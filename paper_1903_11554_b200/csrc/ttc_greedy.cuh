@@ -469,10 +469,27 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
         for (int t = 0; t < r; ++t) {
           if (L > 1) __syncwarp(gmask);   // tile[t][j] final (updated at step t-1 by lane t mod L)
           double f = tile[t * TS + j];
-          if (side == 1) f = div_pre(f, pdiag[t], prcp[t]);  // v_t (= __ddiv_rn bits)
+          if (side == 1) {   // v_t (= __ddiv_rn bits)
+            bool ok;
+            const double q = div_pre_fast(f, pdiag[t], prcp[t], ok);
+            f = ok ? q : div_pre(f, pdiag[t], prcp[t]);
+          }
           const int q0 = t + 1 + ((ln - (t + 1)) & (L - 1));
-          for (int q = q0; q < r; q += L)
-            tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, coef[t * cap + q]));
+          const double* cf = coef + t * cap;
+          int q = q0;
+          // four independent read-modify-writes per iteration (distinct q: the loads of one
+          // group do not depend on its stores, so they are issued together)
+#pragma unroll 1
+          for (; q + 3 * L < r; q += 4 * L) {
+            double* p0 = tile + q * TS + j;
+            const double a0 = p0[0], a1 = p0[L * TS], a2 = p0[2 * L * TS], a3 = p0[3 * L * TS];
+            const double c0 = cf[q], c1 = cf[q + L], c2 = cf[q + 2 * L], c3 = cf[q + 3 * L];
+            p0[0] = __dsub_rn(a0, __dmul_rn(f, c0));
+            p0[L * TS] = __dsub_rn(a1, __dmul_rn(f, c1));
+            p0[2 * L * TS] = __dsub_rn(a2, __dmul_rn(f, c2));
+            p0[3 * L * TS] = __dsub_rn(a3, __dmul_rn(f, c3));
+          }
+          for (; q < r; q += L) tile[q * TS + j] = __dsub_rn(tile[q * TS + j], __dmul_rn(f, cf[q]));
         }
         if (L > 1) __syncwarp(gmask);
       }
@@ -1371,6 +1388,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   phase(PH_TABLES);
 
   // ---- phase 2: u / v of the existing pivots on the new rows and columns
+  // (per-sweep log slots 14 / 15: this phase's own time in the first row CTA / the first column
+  // CTA of the logged superblock, before the cluster barrier)
+  const bool ext_clock = c.phase_ns && job == c.phase_job && tid == 0 && (cr == 0 || cr == (G >= 2 ? G / 2 : 0));
+  const unsigned long long t_ext0 = ext_clock ? gtimer() : 0;
   {
     __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
     __shared__ double pdiag[TTC_MAX_RANK_DEV], prcp[TTC_MAX_RANK_DEV];
@@ -1422,6 +1443,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
   // (the rook steps read U / V through the TMA engine -- the async proxy: order this thread's
   // generic-proxy stores before the barrier that publishes them)
   if (c.tma) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (ext_clock && sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * TTC_LOG_W + 14 + (cr != 0)] += gtimer() - t_ext0;
   cl.sync();  // u / v of the new rows and columns visible to the whole cluster
   TRACE(5);
   phase(PH_EXTEND);

@@ -6,7 +6,7 @@ joined, by section offset, with the line table nvdisasm -g prints for the same c
 with -lineinfo).  Out-of-line subroutines live in the kernel's text section under
 `$kernel$function` labels, so their samples are attributed to their own lines / function.
 
-    python tools/ncu_lines.py <report.ncu-rep> <library.so> <kernel mangled name> [top]
+    python tools/ncu_lines.py <report.ncu-rep> <library.so> <kernel mangled name> [top] [--kernel REGEX]
 """
 import collections
 import csv
@@ -48,8 +48,9 @@ def line_table(so, kernel):
 
 def main():
     rep, so, kernel = sys.argv[1:4]
-    top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    csv_text = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
+    top = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 40
+    kf = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
+    csv_text = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source=sass"],
                               capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(csv_text)))
     hdr = rows[1]

@@ -3,7 +3,7 @@
 import json
 import sys
 
-KEYS = ["prologue", "tables", "extend", "ext_raw", "ext_rec", "samples", "rook", "col_eval", "col_argmax",
+KEYS = ["prologue", "tables", "extend", "ext_raw", "ext_rec", "ext_rows_cta", "ext_cols_cta", "samples", "rook", "col_eval", "col_argmax",
         "row_eval", "row_argmax", "final", "exit", "rounds"]
 for path in sys.argv[1:]:
     rows = [json.loads(l) for l in open(path) if l.startswith("{")]
