@@ -352,9 +352,8 @@ __device__ __forceinline__ void pivot_pos(const DevCtx& c, int k, int s, int& x,
 // ---------------------------------------------------------------------------------------
 // rows per tile: c.ext_tile (host: as many as fit in EXT_SMEM_DOUBLES next to the coefficients)
 #define EXT_SMEM_DOUBLES 8192
-#ifndef EXT_WARP
-#define EXT_WARP 0   // 1: phase 2 in registers, a warp per row group (extend_side_warp; measured
-                     // D_20 -1..+3%, C_200 +25%: off)
+#ifndef EXT_REG
+#define EXT_REG 1    // 1: phase 2 of the t-form families in registers (extend_side_reg)
 #endif
 #ifndef EXT_ILP
 #define EXT_ILP 4   // raw entries per thread per iteration of the extension
@@ -507,43 +506,122 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
   upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
 }
 
-// Phase 2, register variant (EXT_WARP), in batches of nw * EXT_RW rows:
-//   (1) the raw entries A(x, y_s) (A(x_s, y)) of the batch, spread over all threads of the CTA
-//       (EXT_ILP independent entry chains per thread) into the tile [s][TS] -- the batched
-//       fiber evaluation;
-//   (2) a warp per EXT_RW rows runs the recurrence in registers, lane l holding s = l and
-//       s = l + 32 (cap <= 64): for t = 0..r-1 the owner lane of t (t mod 32) has the final
-//       value of s = t (u_t; columns: v_t = acc_t / u_t(x_t), div_pre in every lane) -> warp
-//       shuffle -> every lane subtracts f * coef[t][s] from its s > t.  The rows are
-//       independent chains, interleaved (the division's slow-path test is warp-uniform, so the
-//       fast path is branch-free across rows).  Per s: the same subtractions in the same t
-//       order as the oracle's u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s), hence the same bits;
-//   (3) the final values (columns: acc_s / u_s(x_s)) back to the tile, then coalesced stores.
-#ifndef EXT_RW
-#define EXT_RW 4   // rows per warp per batch
-#endif
+// Phase 2, register-resident variant (t-form families, the default): the tile variant above
+// runs its recurrence through shared memory -- a load and a store per multiply-subtract, the
+// SM's shared-memory bandwidth is its roof (D_20: ~690 cycles per t step, half of a late
+// sweep's extension) -- and evaluates each raw entry from seven table loads.  Here a row x is
+// held by L adjacent lanes, lane l keeping acc[i] = the value of s = L*i + l (EXR_NS slots, so
+// L = 1, 2, 4 covers r <= 16, 32, 64), in registers from the raw entry to the final store:
+//   (1) raw entries straight into the slots.  The factors that depend only on the pivot s
+//       (rows: SB, PB * CX * QL1 and u_{k+1}[b_s] of column y_s; columns: SA, PA * CX * QR0
+//       and u_k[a_s] of row x_s) are formed once per call in shared memory (ExtFix), so an
+//       entry is P_own * F_s * Q_s[node] * rho(u_own, u_s) / (S_own + S_s)^2 -- three
+//       double-double products instead of five; the product is rounded once, so the grouping
+//       gives the same entries (R3);
+//   (2) the triangular recurrence column-oriented (t ascending): the owner lane of t (lane
+//       t mod L of the row group, slot t / L) holds the final acc_t, the group reads it with a
+//       shuffle (columns: v_t = acc_t / u_t(x_t)), every lane subtracts f * coef[t][s] from its
+//       slots s > t -- per s the same operations in the same t order as the oracle's
+//       u_s = A(x, y_s) - sum_{t<s} u_t(x) v_t(y_s), hence the same bits;
+//   (3) the final values (columns: acc_s / u_s(x_s)) straight to U / V.
+// coef[t][s] is kept as coefL[t][l][i] (s = L*i + l), so a lane's slots are contiguous.
+#define EXR_NS 16
+struct ExtFix {
+  DDE F;      // rows: PB[be_s][b_s] * CX[al][be_s] * QL1[al][b_s]; columns: PA[al_s][a_s] * CX[al_s][be] * QR0[be][a_s]
+  ESum S;     // rows: SB[be_s][b_s]; columns: SA[al_s][a_s]
+  double u;   // rows: u_{k+1}[b_s]; columns: u_k[a_s]
+  int q;      // rows: offset of QR0[be_s][.]; columns: offset of QL1[al_s][.]
+  int pad;
+};
+// coefficient row stride (doubles): the L lanes of a row group read L different rows of
+// coefL at once; 18 puts them on disjoint banks (16 = 128 bytes put all on the same ones --
+// a 4-way conflict on every read, ncu: short-scoreboard stalls on the update line) and keeps
+// the rows 16-byte aligned for paired reads
+#define EXR_CS 18
+// lanes per row: the fewest that give every pivot a slot (L * EXR_NS >= r)
+__host__ __device__ __forceinline__ int ext_reg_lanes(int r) { return r <= EXR_NS ? 1 : (r <= 2 * EXR_NS ? 2 : 4); }
 template <int FAMILY>
-__device__ __noinline__ void extend_side_warp(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
-                                              int x_hi,
-                                              const int* p_al, const int* p_a, const double* pdiag,
-                                              const double* prcp, double* coef, double* tile,
-                                              unsigned long long& ent, unsigned long long& upd) {
+__device__ __noinline__ double sb_entry_ool(const DevCtx& c, int job, int k, int al, int a, int be, int b) {
+  return sb_entry<FAMILY>(c, job, k, al, a, be, b);
+}
+
+// raw entries of slots [i0, i0 + 4) of this lane (s = L*i + l) into v; slow bit u: entry u
+// left the division's fast path
+template <int FAMILY>
+__device__ __forceinline__ void ext_raw4(double (&v)[4], int i0, int L, int l, int r, const ExtFix* fix,
+                                         const ESum& so, const DDE& po, double uo, const DDE* Qg, int z,
+                                         unsigned& slow) {
+  DDE q[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int s = min(L * (i0 + u) + l, r - 1);
+    if (FAMILY == 1) q[u] = Qg[fix[s].q + z];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int s = min(L * (i0 + u) + l, r - 1);
+    const ExtFix& f = fix[s];
+    ESum sm = so;
+    esum_add(sm, f.S);
+    const double Sd = esum_round(sm);
+    const double SS = __dmul_rn(Sd, Sd);
+    bool ok;
+    if (FAMILY == 0) {
+      v[u] = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
+    } else {
+      DDE p = po;
+      dde_mul(p, f.F);
+      dde_mul(p, q[u]);
+      bool o1, o2;
+      dde_mul_d(p, rho_fast(uo, f.u, o1));
+      v[u] = dde_div_fast(p, SS, o2);
+      ok = o1 && o2;
+    }
+    slow |= (ok ? 0u : 1u) << u;
+  }
+}
+
+template <int FAMILY>
+__device__ __noinline__ void extend_side_reg(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
+                                             int x_hi, const int* p_al, const int* p_a, const double* pdiag,
+                                             const double* prcp, double* dyn, long long smem_doubles,
+                                             unsigned long long& ent, unsigned long long& upd) {
+  static_assert(FAMILY <= 1, "t-form families only");
   const int n = c.n, cap = c.cap;
   const int sbn = (int)c.sbn;
+  const int jo = job * cap * n, jcx = job * cap * cap;
   double* U = c.U + (long long)job * cap * sbn;
   double* V = c.V + (long long)job * cap * sbn;
-  if (x_lo >= x_hi) return;
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const int t = e / r, s = e - t * r;
-    double v = 0.0;
-    if (t < s) {
-      const int q = p_al[s] * n + p_a[s];
-      v = side == 0 ? V[t * sbn + q] : U[t * sbn + q];
+  if (x_lo >= x_hi || r == 0) return;
+  const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+  const int L = ext_reg_lanes(r);
+  const int l = tid & (L - 1), P = T / L;   // slot lane, rows per pass
+  (void)smem_doubles;   // (cap * 4 * EXR_CS + 8 * cap <= extend_smem_doubles(cap) for cap <= 64)
+  double* coefL = dyn;                                                  // [cap][L][EXR_CS]
+  ExtFix* fix = reinterpret_cast<ExtFix*>(dyn + (long long)cap * L * EXR_CS);   // [cap]
+  {
+    // coefL[t][ls][i] = coef[t][L*i + ls] (i < EXR_NS; the padding is never read): eight
+    // independent loads per thread per iteration
+    const int ne = r * L * EXR_CS;
+    const double* F = side == 0 ? V : U;
+#pragma unroll 1
+    for (int e0 = tid; e0 < ne; e0 += 8 * T) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * T;
+        const int t = e / (L * EXR_CS), ls = (e / EXR_CS) % L, i = e % EXR_CS;
+        const int s = L * i + ls;
+        v[u] = 0.0;
+        if (e < ne && i < EXR_NS && t < s && s < r) v[u] = F[t * sbn + p_al[s] * n + p_a[s]];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * T < ne) coefL[e0 + u * T] = v[u];
     }
-    coef[t * cap + s] = v;
   }
   double* dst = side == 0 ? U : V;
-  const bool timer = c.phase_ns && job == c.phase_job && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0;
+  const bool timer = c.phase_ns && job == c.phase_job && tid == 0 && cg::this_cluster().block_rank() == 0;
   unsigned long long tm = timer ? gtimer() : 0;
   auto clock_to = [&](int ph) {
     if (timer) {
@@ -552,118 +630,134 @@ __device__ __noinline__ void extend_side_warp(const DevCtx& c, int sweep, int jo
       tm = t;
     }
   };
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int s0 = lane, s1 = lane + 32;
-  const bool h0 = s0 < r, h1 = s1 < r;
-  const int BR = min(nw * EXT_RW, c.ext_tile), TS = BR + 1;   // batch rows (<= the tile capacity), stride
+  // own-side tables and node values: rows SA / PA / u_k, columns SB / PB / u_{k+1}
+  const ESum* Sown = side == 0 ? c.SA + jo : c.SB + jo;
+  const DDE* Pown = side == 0 ? c.PA + jo : c.PB + jo;
+  const DDE* Qg = side == 0 ? c.QR0 : c.QL1;
+  const double* uown = c.u + (long long)(side == 0 ? k : k + 1) * n;
+  int fslot = -1;   // the slot (rows: alpha, columns: beta) the ExtFix entries were formed for
+  const int gbase = lane & ~(L - 1);
 #pragma unroll 1
-  for (int x0 = x_lo; x0 < x_hi; x0 += BR) {
-    const int nrow = min(BR, x_hi - x0);
-    // (1) raw entries of the batch, EXT_ILP per thread per iteration
+  for (int x0 = x_lo; x0 < x_hi;) {
+    const int sl0 = x0 / n;
+    const int x1 = min(min(x_hi, x0 + P), (sl0 + 1) * n);   // (a pass stays inside one slot)
+    if (sl0 != fslot) {
+      __syncthreads();   // (previous users of fix / coefL done)
+      if (tid < r) {
+        ExtFix f;
+        const int ps = p_al[tid], pn = p_a[tid];
+        if (side == 0) {   // pivot column y_s = (be, b) = (ps, pn), row slot al = sl0
+          f.S = c.SB[jo + ps * n + pn];
+          f.u = c.u[(long long)(k + 1) * n + pn];
+          f.q = jo + ps * n;
+          if (FAMILY == 1) {
+            DDE F = c.PB[jo + ps * n + pn];
+            const DDE F1 = c.CX[jcx + sl0 * cap + ps], F2 = c.QL1[jo + sl0 * n + pn];
+            dde_mul(F, F1);
+            dde_mul(F, F2);
+            f.F = F;
+          }
+        } else {           // pivot row x_s = (al, a) = (ps, pn), column slot be = sl0
+          f.S = c.SA[jo + ps * n + pn];
+          f.u = c.u[(long long)k * n + pn];
+          f.q = jo + ps * n;
+          if (FAMILY == 1) {
+            DDE F = c.PA[jo + ps * n + pn];
+            const DDE F1 = c.CX[jcx + ps * cap + sl0], F2 = c.QR0[jo + sl0 * n + pn];
+            dde_mul(F, F1);
+            dde_mul(F, F2);
+            f.F = F;
+          }
+        }
+        f.pad = 0;
+        fix[tid] = f;
+      }
+      fslot = sl0;
+      __syncthreads();
+    }
+    const int nrow = x1 - x0;
+    const int j = tid / L;
+    const bool valid = j < nrow;
+    const int x = x0 + (valid ? j : nrow - 1);   // (a lane past the pass repeats the last row)
+    const int z = x - sl0 * n;                   // node of the row within its slot
+    // (1) raw entries, four slots per iteration (their table gathers issued together: a
+    // dependent global load waits a loaded-L2 round trip), placed into the slots by selects
+    double acc[EXR_NS];
+#pragma unroll
+    for (int i = 0; i < EXR_NS; ++i) acc[i] = 0.0;
     {
-      const int ne = nrow * r, B = blockDim.x;
-      int e = threadIdx.x;
+      const ESum so = Sown[x];
+      DDE po;
+      if (FAMILY == 1) po = Pown[x];
+      else po = dde_one();
+      const double uo = uown[z];
 #pragma unroll 1
-      for (; e + (EXT_ILP - 1) * B < ne; e += EXT_ILP * B) {
-        double v[EXT_ILP];
-        int at[EXT_ILP];
-        bool ok[EXT_ILP];
-#pragma unroll
-        for (int u = 0; u < EXT_ILP; ++u) {   // (branch-free: the EXT_ILP chains interleave)
-          const int eu = e + u * B;
-          const int s = eu / nrow, j = eu - s * nrow;
-          const int x = x0 + j;
-          const int al = x / n, a = x - al * n;
-          v[u] = side == 0 ? sb_entry_fast<FAMILY>(c, job, k, al, a, p_al[s], p_a[s], ok[u])
-                           : sb_entry_fast<FAMILY>(c, job, k, p_al[s], p_a[s], al, a, ok[u]);
-          at[u] = s * TS + j;
-        }
-#pragma unroll
-        for (int u = 0; u < EXT_ILP; ++u) {
-          if (!ok[u]) {
-            const int eu = e + u * B;
-            const int s = eu / nrow, j = eu - s * nrow;
-            const int x = x0 + j;
-            const int al = x / n, a = x - al * n;
-            v[u] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
-                             : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
-          }
-          tile[at[u]] = v[u];
-        }
-      }
+      for (int g = 0; g < EXR_NS / 4 && 4 * L * g < r; ++g) {   // (warp-uniform)
+        double v[4];
+        unsigned slow = 0;
+        ext_raw4<FAMILY>(v, 4 * g, L, l, r, fix, so, po, uo, Qg, z, slow);
+        if (slow) {   // (rare: a division off its fast path -- the entry the plain way, out of line)
 #pragma unroll 1
-      for (; e < ne; e += B) {
-        const int s = e / nrow, j = e - s * nrow;
-        const int x = x0 + j;
-        const int al = x / n, a = x - al * n;
-        tile[s * TS + j] = side == 0 ? sb_entry<FAMILY>(c, job, k, al, a, p_al[s], p_a[s])
-                                     : sb_entry<FAMILY>(c, job, k, p_al[s], p_a[s], al, a);
-      }
-    }
-    __syncthreads();
-    clock_to(PH_EXT_RAW);
-    // (2) the recurrence, EXT_RW rows per warp in registers
-    const int j0 = warp * EXT_RW;
-    if (j0 < nrow) {   // (warp-uniform)
-      double v0[EXT_RW], v1[EXT_RW];
-#pragma unroll
-      for (int i = 0; i < EXT_RW; ++i) {
-        const int j = min(j0 + i, nrow - 1);   // (a ragged group repeats its last row; not written back)
-        v0[i] = h0 ? tile[s0 * TS + j] : 0.0;
-        v1[i] = h1 ? tile[s1 * TS + j] : 0.0;
-      }
-#pragma unroll 1
-      for (int t = 0; t < r; ++t) {
-        const int owner = t & 31;
-        const bool hi = t >= 32;
-        const double c0 = h0 ? coef[t * cap + s0] : 0.0;
-        const double c1 = h1 ? coef[t * cap + s1] : 0.0;
-        const bool u0 = h0 && s0 > t, u1 = h1 && s1 > t;
-        double f[EXT_RW];
-#pragma unroll
-        for (int i = 0; i < EXT_RW; ++i) f[i] = __shfl_sync(0xffffffffu, hi ? v1[i] : v0[i], owner);
-        if (side == 1) {   // v_t = acc_t / u_t(x_t): div_pre, its slow path taken warp-uniformly
-          const double dg = pdiag[t], rc = prcp[t];
-          bool ok = true;
-#pragma unroll
-          for (int i = 0; i < EXT_RW; ++i) {
-            bool o;
-            const double q = div_pre_fast(f[i], dg, rc, o);
-            ok &= o;
-            f[i] = q;
-          }
-          if (!__all_sync(0xffffffffu, ok)) {
-#pragma unroll
-            for (int i = 0; i < EXT_RW; ++i) {
-              const double a = __shfl_sync(0xffffffffu, hi ? v1[i] : v0[i], owner);
-              f[i] = div_pre(a, dg, rc);
+          for (int u = 0; u < 4; ++u)
+            if ((slow >> u) & 1u) {
+              const int s = min(L * (4 * g + u) + l, r - 1);
+              const int al = side == 0 ? sl0 : p_al[s], a = side == 0 ? z : p_a[s];
+              const int be = side == 0 ? p_al[s] : sl0, b = side == 0 ? p_a[s] : z;
+              const double w = sb_entry_ool<FAMILY>(c, job, k, al, a, be, b);
+              if (u == 0) v[0] = w;
+              else if (u == 1) v[1] = w;
+              else if (u == 2) v[2] = w;
+              else v[3] = w;
             }
-          }
         }
 #pragma unroll
-        for (int i = 0; i < EXT_RW; ++i) {
-          if (u0) v0[i] = __dsub_rn(v0[i], __dmul_rn(f[i], c0));
-          if (u1) v1[i] = __dsub_rn(v1[i], __dmul_rn(f[i], c1));
-        }
+        for (int i = 0; i < EXR_NS; ++i)
+          if ((i >> 2) == g) acc[i] = v[i & 3];
       }
-      // (3) final values back to the tile (columns: acc_s / u_s(x_s))
+    }
+    clock_to(PH_EXT_RAW);
+    // (2) the recurrence: t in four phases of 4 * L (a runtime loop each, its slot updates
+    // unrolled over the slots a phase can still reach, predicated on s > t; f = acc_t read
+    // from the phase's four candidate slots by selects): small, spill-free code
 #pragma unroll
-      for (int i = 0; i < EXT_RW; ++i) {
-        const int j = j0 + i;
-        if (j < nrow) {
-          if (h0) tile[s0 * TS + j] = side == 1 ? div_pre(v0[i], pdiag[s0], prcp[s0]) : v0[i];
-          if (h1) tile[s1 * TS + j] = side == 1 ? div_pre(v1[i], pdiag[s1], prcp[s1]) : v1[i];
+    for (int ph = 0; ph < EXR_NS / 4; ++ph) {
+      const int tb = 4 * L * ph;   // (a constant: the phase loop is unrolled)
+      if (tb >= r) break;   // (warp-uniform)
+#pragma unroll 1
+      for (int t = tb; t < tb + 4 * L; ++t) {   // (constant trip count: no bound to spill)
+        if (t >= r) continue;   // (warp-uniform)
+        const int it = t / L, lt = t - it * L;
+        double own = acc[4 * ph];
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (it == 4 * ph + u) own = acc[4 * ph + u];
+        double f = __shfl_sync(0xffffffffu, own, gbase + lt);
+        if (side == 1) {   // v_t = acc_t / u_t(x_t) (= __ddiv_rn bits)
+          bool ok;
+          const double q = div_pre_fast(f, pdiag[t], prcp[t], ok);
+          f = ok ? q : div_pre(f, pdiag[t], prcp[t]);
+        }
+        const double2* cf = reinterpret_cast<const double2*>(coefL + (t * L + l) * EXR_CS);
+#pragma unroll
+        for (int i = 4 * ph; i < EXR_NS; i += 2) {   // (paired 16-byte reads)
+          const double2 cc = cf[i >> 1];
+          if (L * i + l > t) acc[i] = __dsub_rn(acc[i], __dmul_rn(f, cc.x));
+          if (L * (i + 1) + l > t) acc[i + 1] = __dsub_rn(acc[i + 1], __dmul_rn(f, cc.y));
         }
       }
     }
-    __syncthreads();
     clock_to(PH_EXT_REC);
-    for (int e = threadIdx.x; e < r * nrow; e += blockDim.x) {
-      const int s = e / nrow, j = e - s * nrow;
-      dst[s * sbn + x0 + j] = tile[s * TS + j];
+    // (3) final values
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < EXR_NS; ++i) {
+        const int s = L * i + l;
+        if (s < r) dst[(long long)s * sbn + x] = side == 1 ? div_pre(acc[i], pdiag[s], prcp[s]) : acc[i];
+      }
     }
-    __syncthreads();
+    x0 = x1;
   }
+  __syncthreads();
   ent += (unsigned long long)(x_hi - x_lo) * r;
   upd += (unsigned long long)(x_hi - x_lo) * r * (r - 1) / 2;
 }
@@ -732,7 +826,7 @@ struct GreedySmem {
   Cand best;                         // CTA argmax / cluster winner
   int xs[TTC_MAX_RANK_DEV];          // pivot rows
   int ys[TTC_MAX_RANK_DEV];          // pivot columns
-  double vec[TTC_MAX_RANK_DEV];      // V[t][y*] (column step) or U[t][x*] (row step)
+  alignas(16) double vec[TTC_MAX_RANK_DEV];   // V[t][y*] (column step) or U[t][x*] (row step) (paired reads)
   // factors of the fixed column (row) of a step
   DDE f_slot[TTC_MAX_RANK_DEV];      // column step: CX[alpha][beta]*QL1[alpha][b]; row step: CX*QR0
   DDE f_node[STAGE_N];               // column step: QR0[beta][a]; row step: QL1[alpha][b]
@@ -883,6 +977,7 @@ struct TmaRing {
   unsigned long long* full;   // this warp's P barriers
   int lane, tb, P, nb, r, ybase, x0, T;
   int total, is;              // stages of this step, issued (lane 0)
+  int ijb, ib;                // row block and term block of the next stage to issue (no division per stage)
   RingPos pos, ipos;          // consumption / issue position
   __device__ __forceinline__ void start(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
                                         int P_, int r_, int ybase_, int xb, int xe, RingPos p) {
@@ -897,15 +992,16 @@ struct TmaRing {
     pos = p;
     ipos = p;
     is = 0;
+    ijb = 0;
+    ib = 0;
     if (lane == 0)
       for (int q = 0; q < P - 1 && is < total; ++q) issue();
   }
   __device__ __forceinline__ void issue() {   // lane 0: stage `is` into slot ipos
-    const int jb = is / nb, b = is - jb * nb;
     const unsigned fa = smem_u32(&full[ipos.slot]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fa), "r"(tb * 256) : "memory");
     const unsigned dst = smem_u32(wbuf + ipos.slot * tb * 32);
-    const int x = x0 + jb * T, y = ybase + b * tb;
+    const int x = x0 + ijb * T, y = ybase + ib * tb;
     if (EVICT_FIRST) {
       unsigned long long pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -920,6 +1016,7 @@ struct TmaRing {
           : "memory");
     }
     ++is;
+    if (++ib == nb) { ib = 0; ++ijb; }
     if (++ipos.slot == P) { ipos.slot = 0; ipos.phase ^= 1u; }
   }
   // e -= F[t][row] * vec[t], t = 0 .. r-1 in order, for this thread's row of the next row
@@ -931,7 +1028,17 @@ struct TmaRing {
       mbar_wait(&full[pos.slot], pos.phase);
       const double* src = wbuf + pos.slot * tb * 32 + lane;
       const int t0 = b * tb, tn = min(tb, r - t0);
-      for (int i = 0; i < tn; ++i) e = __dsub_rn(e, __dmul_rn(src[i * 32], vec[t0 + i]));
+      if (tn == 16) {   // (a full stage of the usual shape: unrolled, vec read in pairs)
+        const double2* v2 = reinterpret_cast<const double2*>(vec + t0);
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const double2 vv = v2[i >> 1];
+          e = __dsub_rn(e, __dmul_rn(src[i * 32], vv.x));
+          e = __dsub_rn(e, __dmul_rn(src[(i + 1) * 32], vv.y));
+        }
+      } else {
+        for (int i = 0; i < tn; ++i) e = __dsub_rn(e, __dmul_rn(src[i * 32], vec[t0 + i]));
+      }
       __syncwarp();   // (the slot is refilled two issues later, by lane 0 of this warp)
       if (++pos.slot == P) { pos.slot = 0; pos.phase ^= 1u; }
     }
@@ -1285,7 +1392,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 
 template <int FAMILY, bool CACHED>
-__device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double* dyn, int sweep, int job, int r,
+__device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, GreedySmem& S, double* dyn, int sweep, int job, int r,
                                           int rl, int rr, int* Rn, int& xstep, RingPos& rpos, bool end_sync,
                                           int rows_done, int cols_done, bool xy_known, bool release) {
   cg::cluster_group cl = cg::this_cluster();
@@ -1369,18 +1476,18 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     bool cx_pending = FAMILY == 1;
     if (do_l)
       for (int slot = rows_done; slot < rl; ++slot) {
-        sb_side_tables(c, job, 0, slot, il * T, gl * T, rl, rr, rows_done, cols_done, cx_gw, cx_pending ? cx_nwg : 0);
+        sb_side_tables(cs, job, 0, slot, il * T, gl * T, rl, rr, rows_done, cols_done, cx_gw, cx_pending ? cx_nwg : 0);
         cx_pending = false;
         __syncthreads();
       }
     if (do_r)
       for (int slot = cols_done; slot < rr; ++slot) {
-        sb_side_tables(c, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T, rl, rr, rows_done, cols_done, cx_gw,
+        sb_side_tables(cs, job, 1, slot, ir * T, (G >= 2 ? G - gl : 1) * T, rl, rr, rows_done, cols_done, cx_gw,
                        cx_pending ? cx_nwg : 0);
         cx_pending = false;
         __syncthreads();
       }
-    if (cx_pending && tid >= 32) sb_cx_share(c, job, rows_done, cols_done, rl, rr, cx_gw, cx_nwg);
+    if (cx_pending && tid >= 32) sb_cx_share(cs, job, rows_done, cols_done, rl, rr, cx_gw, cx_nwg);
   }
   TRACE(2);
   cl.sync();  // tables visible to the whole cluster
@@ -1397,6 +1504,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     __shared__ double pdiag[TTC_MAX_RANK_DEV], prcp[TTC_MAX_RANK_DEV];
     double* coef = dyn;
     double* tile = dyn + (long long)cap * cap;
+    const long long ext_dyn = extend_smem_doubles(cap);   // (dynamic shared memory is at least this)
     const int nr_new = (rl - rows_done) * n, nc_new = (rr - cols_done) * n;
     // with G >= 2 the first half of the cluster extends the rows, the second half the columns
     // (independent: the column recurrence reads u only at old pivot rows, or A(t0) at the
@@ -1405,6 +1513,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
     const bool do_rows = G == 1 || cr < gr, do_cols = G == 1 || cr >= gr;
     const int rr_i = G == 1 ? 0 : cr, cc_i = G == 1 ? 0 : cr - gr;
     const int rchunk = (nr_new + gr - 1) / gr, cchunk = (nc_new + gc - 1) / gc;
+    // the register variant when a CTA's rows fill its threads at the lanes per row the rank
+    // needs (D_20 from rank 17); else the tile variant spreads the few rows' entries over all
+    // threads (D_5: ~33 rows per CTA -- the register variant measured 0.93 vs 0.77 ms there)
+    const bool ext_reg = EXT_REG && FAMILY == 1 && min(rchunk, cchunk) * ext_reg_lanes(r) >= T;
     if (do_rows) {   // rows: fixed index = pivot columns y_s
       if (tid < r) {
         p_al[tid] = S.ys[tid] / n;
@@ -1412,13 +1524,12 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       __syncthreads();
       const int lo = rows_done * n + rr_i * rchunk;
-#if EXT_WARP
-      extend_side_warp<FAMILY>(c, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
-                               ext_ent, ext_upd);
-#else
-      extend_side<FAMILY>(c, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
-                          ext_ent, ext_upd);
-#endif
+      if (ext_reg)
+        extend_side_reg<1>(cs, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a,
+                                                  pdiag, prcp, dyn, ext_dyn, ext_ent, ext_upd);
+      else
+        extend_side<FAMILY>(cs, sweep, job, k, 0, r, lo, min(lo + rchunk, rl * n), p_al, p_a, pdiag, prcp, coef, tile,
+                            ext_ent, ext_upd);
       __syncthreads();
     }
     if (do_cols) {   // columns: fixed index = pivot rows x_s, divisors u_s(x_s) (A(t0) at first)
@@ -1430,13 +1541,12 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       }
       __syncthreads();
       const int lo = cols_done * n + cc_i * cchunk;
-#if EXT_WARP
-      extend_side_warp<FAMILY>(c, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
-                               ext_ent, ext_upd);
-#else
-      extend_side<FAMILY>(c, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
-                          ext_ent, ext_upd);
-#endif
+      if (ext_reg)
+        extend_side_reg<1>(cs, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a,
+                                                  pdiag, prcp, dyn, ext_dyn, ext_ent, ext_upd);
+      else
+        extend_side<FAMILY>(cs, sweep, job, k, 1, r, lo, min(lo + cchunk, rr * n), p_al, p_a, pdiag, prcp, coef, tile,
+                            ext_ent, ext_upd);
     }
   }
   TRACE(4);
@@ -1529,21 +1639,50 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
       TRACE(6);
       // visibility of the cache to the other threads: the __syncthreads of the first step
     }
-    // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically)
+    // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically).
+    // A warp per four samples: the lanes load the u/v factors of all four at once (t = lane,
+    // lane + 32) and form the products u_t(x) v_t(y); lanes 0-3 evaluate the raw entries;
+    // then the four E = A - sum_t u_t v_t run their t-ascending subtraction chains side by
+    // side through shuffles -- the oracle's operations in its order.  (A thread per sample
+    // waited for its 2r scattered factor loads in dependent batches: ~16 us per late D_20
+    // sweep.)
     {
       double bv = -1.0;
       long long bf = LLONG_MAX;
-      for (int q = tid; q < c.ns; q += T) {
-        const int sx = smp[2 * q], sy = smp[2 * q + 1];
-        const int al = sx / n, a = sx - al * n;
-        const int be = sy / n, b = sy - be * n;
-        double e = sb_entry<FAMILY>(c, job, k, al, a, be, b);
-        for (int t = 0; t < r; ++t) e = __dsub_rn(e, __dmul_rn(U[t * sbn + sx], V[t * sbn + sy]));
-        bool masked = false;
+      const int lane = tid & 31, nw = T >> 5;
 #pragma unroll 1
-        for (int t = 0; t < r; ++t) masked |= (S.xs[t] == sx) | (S.ys[t] == sy);
-        if (masked) e = 0.0;
-        if (cand_better(fabs(e), q, bv, bf)) { bv = fabs(e); bf = q; }
+      for (int q0 = (tid >> 5) * 4; q0 < c.ns; q0 += nw * 4) {   // (warp-uniform)
+        double pa[4], pb[4];
+        bool msk[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int q = min(q0 + m, c.ns - 1);
+          const int sx = smp[2 * q], sy = smp[2 * q + 1];
+          const int t1 = lane + 32;
+          pa[m] = lane < r ? __dmul_rn(U[lane * sbn + sx], V[lane * sbn + sy]) : 0.0;
+          pb[m] = t1 < r ? __dmul_rn(U[t1 * sbn + sx], V[t1 * sbn + sy]) : 0.0;
+          msk[m] = (lane < r && (S.xs[lane] == sx || S.ys[lane] == sy)) || (t1 < r && (S.xs[t1] == sx || S.ys[t1] == sy));
+        }
+        double raw;
+        {
+          const int q = min(q0 + (lane & 3), c.ns - 1);
+          const int sx = smp[2 * q], sy = smp[2 * q + 1];
+          const int al = sx / n, a = sx - al * n;
+          const int be = sy / n, b = sy - be * n;
+          raw = sb_entry<FAMILY>(c, job, k, al, a, be, b);
+        }
+        double e[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) e[m] = __shfl_sync(0xffffffffu, raw, m);
+#pragma unroll 4
+        for (int t = 0; t < r; ++t)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) e[m] = __dsub_rn(e[m], __shfl_sync(0xffffffffu, t < 32 ? pa[m] : pb[m], t & 31));
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          if (__any_sync(0xffffffffu, msk[m])) e[m] = 0.0;   // a pivot row or column: E is exactly 0
+          if (q0 + m < c.ns && cand_better(fabs(e[m]), q0 + m, bv, bf)) { bv = fabs(e[m]); bf = q0 + m; }
+        }
       }
       TRACE(7);
       argmax_step(&S, bv, bf, 1, 0);   // CTA-local: every CTA drew the same samples
@@ -1577,7 +1716,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
         if (jy - q * T == tid && q < 64) colmask |= 1ULL << q;
       }
     }
-    StepCtx X{&c, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
+    StepCtx X{&cs, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
               U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
               timer, dyn, c.ring_tb, c.ring_p, c.tma != 0, &rpos};
     auto column = [&](int y, bool search) -> int {
@@ -1727,8 +1866,10 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, GreedySmem& S, double
 template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int sweep) {
   __shared__ GreedySmem S;
+  __shared__ DevCtx s_ctx;   // (see k_sweeps)
   extern __shared__ __align__(1024) double dyn[];
   cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) s_ctx = c;
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   const int r = rec_rank(c.rec_cur, c.RS, k);
   const int rl = k > 0 ? rec_rank(c.rec_cur, c.RS, k - 1) : 1;
@@ -1743,7 +1884,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
   RingPos rpos{0, 0u};
-  const int rn = sweep_body<FAMILY, CACHED>(c, S, dyn, sweep, job, r, rl, rr, Rn, xstep, rpos, true,
+  const int rn = sweep_body<FAMILY, CACHED>(c, s_ctx, S, dyn, sweep, job, r, rl, rr, Rn, xstep, rpos, true,
                                             c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false, false);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
     c.rank_ring[k * 2 + (sweep & 1)] = rn;
@@ -1762,8 +1903,15 @@ template <int FAMILY, bool CACHED, int THREADS>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
   __shared__ GreedySmem S;
   __shared__ int s_abort[2];   // by sweep parity: one cluster barrier per sweep start
+  // The parameters as seen by the out-of-line helpers (tables, extension, rook-step context):
+  // a reference to the kernel parameter itself would make the compiler copy it to local
+  // memory and every helper read its fields with LDL -- L1 misses (shared memory leaves L1
+  // ~50 KB) that wait a loaded-L2 round trip while the other superblocks stream.  (Ordered
+  // before use by the first sweep's cluster barrier.)
+  __shared__ DevCtx s_ctx;
   extern __shared__ __align__(1024) double dyn[];
   cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) s_ctx = c;
   const int job = blockIdx.x / c.G, k = c.kb + job, d = c.d;
   int* Rk = c.rec_cur + (long long)k * c.RS;
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
@@ -1811,7 +1959,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
     // (sweep_body publishes rank_ring[k] and releases done[k] as soon as the pivot is known)
-    r = sweep_body<FAMILY, CACHED>(c, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
+    r = sweep_body<FAMILY, CACHED>(c, s_ctx, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
                                    s > s0, true);
     rdone = rl;   // (= the sbstate the sweep wrote)
     cdone = rr;

@@ -57,11 +57,18 @@ def main():
     ia, iall, inot = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), \
         hdr.index("Warp Stall Sampling (Not-issued Samples)")
     iex = hdr.index("Instructions Executed")
+    # per-reason stall columns, when the source page has them
+    ireason = [(i, h) for i, h in enumerate(hdr) if ("stall" in h.lower() and "Sampling" not in h)]
+    if "--headers" in sys.argv:
+        print("# columns:", hdr)
     data = rows[2:]
     base = int(data[0][ia], 16)
     table = line_table(so, kernel)
     by_line = collections.defaultdict(lambda: [0, 0, 0])
     by_func = collections.defaultdict(lambda: [0, 0, 0])
+    by_line_reason = collections.defaultdict(collections.Counter)
+    ffilter = sys.argv[sys.argv.index("--func") + 1] if "--func" in sys.argv else None
+    by_fline = collections.defaultdict(lambda: [0, 0])
     tot = 0
     for r in data:
         off = int(r[ia], 16) - base
@@ -71,16 +78,32 @@ def main():
         by_line[line][0] += s_all
         by_line[line][1] += s_not
         by_line[line][2] += ex
+        for i, h in ireason:
+            try:
+                by_line_reason[line][h] += float(r[i] or 0)
+            except ValueError:
+                pass
         by_func[func][0] += s_all
         by_func[func][1] += s_not
         by_func[func][2] += ex
+        if ffilter and re.search(ffilter, func):
+            by_fline[line][0] += s_all
+            by_fline[line][1] += ex
     print(f"# {rep}: {tot} stall samples, {len(data)} instructions")
     print("## by function (samples, share, not-issued, warp instructions executed)")
     for f, v in sorted(by_func.items(), key=lambda kv: -kv[1][0]):
         print(f"{100 * v[0] / tot:6.1f}% {v[0]:9d} {v[1]:9d} {v[2]:12d}  {f[:90]}")
+    if ffilter:
+        print(f"## lines of functions matching {ffilter} (samples, share of all, warp instructions)")
+        for ln, v in sorted(by_fline.items(), key=lambda kv: (str(kv[0][0]) if kv[0] else "", kv[0][1] if kv[0] else 0)):
+            rs = by_line_reason.get(ln)
+            top3 = ", ".join(f"{h.strip()} {int(c)}" for h, c in rs.most_common(4) if "Not Issued" not in h) if rs else ""
+            print(f"{v[0]:9d} {100 * v[0] / tot:6.2f}% {v[1]:12d}  {ln}  {top3}")
     print(f"## top {top} lines")
     for ln, v in sorted(by_line.items(), key=lambda kv: -kv[1][0])[:top]:
-        print(f"{100 * v[0] / tot:6.1f}% {v[0]:9d} {v[2]:12d}  {ln}")
+        rs = by_line_reason.get(ln)
+        top3 = ", ".join(f"{h.replace('Warp Stall Sampling','').strip()} {int(c)}" for h, c in rs.most_common(3)) if rs else ""
+        print(f"{100 * v[0] / tot:6.1f}% {v[0]:9d} {v[2]:12d}  {ln}  {top3}")
 
 
 if __name__ == "__main__":
