@@ -240,8 +240,9 @@ int tt_cross_get_wsum(ttc_ctx* ctx, int32_t mode, double* hi_out, double* lo_out
 int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64_t* launches, double* ms);
 
 /* tt_cross_get_launch_shape -- the k_sweep launch chosen at init: CTAs per superblock cluster,
- * threads per CTA, whether the rook search keeps its rows/columns in shared memory, and the
- * dynamic shared memory per CTA (bytes).  Any pointer may be NULL. */
+ * threads per CTA, flags in *cached (bit 0: the rook search keeps its rows/columns in shared
+ * memory; bit 1: tt_cross_sweep runs the persistent wavefront launch), and the dynamic shared
+ * memory per CTA (bytes).  Any pointer may be NULL. */
 int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, int32_t* cached,
                               int64_t* smem_bytes);
 

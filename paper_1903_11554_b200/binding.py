@@ -310,7 +310,8 @@ class TTCross:
         g, t, ca, sm = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
         _check(self.lib, self.lib.tt_cross_get_launch_shape(self._h, ctypes.byref(g), ctypes.byref(t), ctypes.byref(ca),
                                                             ctypes.byref(sm)), "tt_cross_get_launch_shape")
-        return {"cluster": g.value, "threads": t.value, "cached": bool(ca.value), "smem_bytes": sm.value}
+        return {"cluster": g.value, "threads": t.value, "cached": bool(ca.value & 1), "persistent": bool(ca.value & 2),
+                "smem_bytes": sm.value}
 
     def kernel_times(self):
         """{kernel name: (launches, ms)} since the last reset (ms only with timing on)."""

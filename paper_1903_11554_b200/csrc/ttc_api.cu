@@ -705,33 +705,42 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
   }
   {
     cudaError_t ce = cudaSuccess;
+    int optin = 0, dev0 = 0;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+    // smem < 0: everything the device allows a block beside the kernel's static shared memory
     auto allow = [&](const void* f, int smem) {
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (smem < 0 && ce == cudaSuccess) {
+        cudaFuncAttributes fa = {};
+        ce = cudaFuncGetAttributes(&fa, f);
+        smem = optin - (int)fa.sharedSizeBytes;
+      }
       if (ce == cudaSuccess) ce = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     };
-    allow((const void*)k_sweeps<0, false, 256>, 180 * 1024);
-    allow((const void*)k_sweeps<1, false, 256>, 180 * 1024);
-    allow((const void*)k_sweeps<0, true, 256>, 180 * 1024);
-    allow((const void*)k_sweeps<1, true, 256>, 180 * 1024);
-    allow((const void*)k_sweeps<0, false, 512>, 180 * 1024);
-    allow((const void*)k_sweeps<1, false, 512>, 180 * 1024);
-    allow((const void*)k_sweeps<0, true, 512>, 180 * 1024);
-    allow((const void*)k_sweeps<1, true, 512>, 180 * 1024);
+    allow((const void*)k_sweeps<0, false, 256>, -1);
+    allow((const void*)k_sweeps<1, false, 256>, -1);
+    allow((const void*)k_sweeps<0, true, 256>, -1);
+    allow((const void*)k_sweeps<1, true, 256>, -1);
+    allow((const void*)k_sweeps<0, false, 512>, -1);
+    allow((const void*)k_sweeps<1, false, 512>, -1);
+    allow((const void*)k_sweeps<0, true, 512>, -1);
+    allow((const void*)k_sweeps<1, true, 512>, -1);
     for (const void* f : {(const void*)k_sweep<2, false, 256>, (const void*)k_sweep<2, false, 512>,
                           (const void*)k_sweep<3, false, 256>, (const void*)k_sweep<3, false, 512>,
                           (const void*)k_sweep<4, false, 256>, (const void*)k_sweep<4, false, 512>,
                           (const void*)k_sweeps<2, false, 256>, (const void*)k_sweeps<2, false, 512>,
                           (const void*)k_sweeps<3, false, 256>, (const void*)k_sweeps<3, false, 512>,
                           (const void*)k_sweeps<4, false, 256>, (const void*)k_sweeps<4, false, 512>})
-      allow(f, 180 * 1024);
-    allow((const void*)k_sweep<0, false, 256>, 180 * 1024);
-    allow((const void*)k_sweep<1, false, 256>, 180 * 1024);
-    allow((const void*)k_sweep<0, true, 256>, 180 * 1024);
-    allow((const void*)k_sweep<1, true, 256>, 180 * 1024);
-    allow((const void*)k_sweep<0, false, 512>, 180 * 1024);
-    allow((const void*)k_sweep<1, false, 512>, 180 * 1024);
-    allow((const void*)k_sweep<0, true, 512>, 180 * 1024);
-    allow((const void*)k_sweep<1, true, 512>, 180 * 1024);
+      allow(f, -1);
+    allow((const void*)k_sweep<0, false, 256>, -1);
+    allow((const void*)k_sweep<1, false, 256>, -1);
+    allow((const void*)k_sweep<0, true, 256>, -1);
+    allow((const void*)k_sweep<1, true, 256>, -1);
+    allow((const void*)k_sweep<0, false, 512>, -1);
+    allow((const void*)k_sweep<1, false, 512>, -1);
+    allow((const void*)k_sweep<0, true, 512>, -1);
+    allow((const void*)k_sweep<1, true, 512>, -1);
     allow((const void*)k_fiber_wsum<0, false>, fw_smem_bytes());
     allow((const void*)k_fiber_wsum<1, false>, fw_smem_bytes());
     allow((const void*)k_fiber_wsum<0, true>, fw_smem_bytes());
@@ -782,12 +791,16 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     };
     const size_t ext_bytes = (size_t)extend_smem_doubles(cap) * sizeof(double);
     const size_t smem_lim = 180 * 1024;
-    // the non-cached variant also holds the rook steps' DotRing (at least 4 terms per stage)
-    // (TTC_RING_KB: experiments with a larger ring in the non-cached shape)
-    const size_t ring_min = std::getenv("TTC_RING_KB") ? (size_t)std::atoi(std::getenv("TTC_RING_KB")) * 1024 : 0;
-    auto smem_for = [&](int g, bool cached) -> size_t {
-      return std::max(ext_bytes, cached ? cache_for(g) : std::max(ring_min, (size_t)RING_P * 4 * T * sizeof(double)));
-    };
+    // after the ring / cache / extension part: the staged node factors f_node (family D, n <=
+    // STAGE_N) or the Alg. 2 sample positions, whichever is larger
+    const size_t fnode_bytes =
+        ((std::max<size_t>(k.family == TTC_FAMILY_D && n <= STAGE_N ? (size_t)n * sizeof(DDE) : 0,
+                           (size_t)2 * dc.ns * sizeof(int)) + 15) / 16) * 16;
+    // (TTC_RING_KB: experiments, the ring part of a non-cached shape in KB)
+    const size_t ring_env = std::getenv("TTC_RING_KB") ? (size_t)std::atoi(std::getenv("TTC_RING_KB")) * 1024 : 0;
+    size_t ring = ring_env ? ring_env : (size_t)RING_P * 4 * T * sizeof(double);
+    auto base_for = [&](int g, bool cached) -> size_t { return std::max(ext_bytes, cached ? cache_for(g) : ring); };
+    auto smem_for = [&](int g, bool cached) -> size_t { return base_for(g, cached) + fnode_bytes; };
     // T = threads per CTA; kernels are compiled for 256 (two CTAs per SM) and 512 (one)
     auto fn_for = [&](bool cached) -> const void* {
       const bool big = T > 256;
@@ -801,6 +814,20 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
         case TTC_FAMILY_CX: return big ? (const void*)k_sweep<2, false, 512> : (const void*)k_sweep<2, false, 256>;
         case TTC_FAMILY_DX: return big ? (const void*)k_sweep<3, false, 512> : (const void*)k_sweep<3, false, 256>;
         default: return big ? (const void*)k_sweep<4, false, 512> : (const void*)k_sweep<4, false, 256>;
+      }
+    };
+    auto sweeps_for = [&](bool cached) -> const void* {
+      const bool big = T > 256;
+      switch (k.family) {
+        case TTC_FAMILY_C:
+          return big ? (cached ? (const void*)k_sweeps<0, true, 512> : (const void*)k_sweeps<0, false, 512>)
+                     : (cached ? (const void*)k_sweeps<0, true, 256> : (const void*)k_sweeps<0, false, 256>);
+        case TTC_FAMILY_D:
+          return big ? (cached ? (const void*)k_sweeps<1, true, 512> : (const void*)k_sweeps<1, false, 512>)
+                     : (cached ? (const void*)k_sweeps<1, true, 256> : (const void*)k_sweeps<1, false, 256>);
+        case TTC_FAMILY_CX: return big ? (const void*)k_sweeps<2, false, 512> : (const void*)k_sweeps<2, false, 256>;
+        case TTC_FAMILY_DX: return big ? (const void*)k_sweeps<3, false, 512> : (const void*)k_sweeps<3, false, 256>;
+        default: return big ? (const void*)k_sweeps<4, false, 512> : (const void*)k_sweeps<4, false, 256>;
       }
     };
     // resident clusters for (G, cached)
@@ -844,40 +871,73 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
         if (resident(G, cached) < nj) T = Tsave;
       }
     }
+    // Streaming shapes (the rook steps read U / V from HBM through the TMA ring): a step of a
+    // CTA is bound by the bytes its ring keeps in flight (~ the ring: 64 KB at ~1.8 us per
+    // round trip = 36 GB/s per CTA, D_20), so the shape maximises the ring capacity of all
+    // resident CTAs -- (threads, CTAs per SM, cluster size) with every cluster resident and
+    // each CTA's ring as large as the SM's shared memory allows (whole 16-term stages per
+    // warp).  D_20: 19 clusters of 6 x 512 threads (one CTA per SM, 192 KB rings) instead of
+    // 8 x 256 (two per SM, 64 KB): 18.5 -> ~15 ms (profiles/r02c_*).
+    const bool shape_env = std::getenv("TTC_GREEDY_T") || std::getenv("TTC_GREEDY_G");
+    if (!cached && TTC_TMA && !shape_env) {
+      int smem_sm = 0, optin = 0;
+      const long long ring_sm = std::getenv("TTC_RING_SM_KB") ? std::atoll(std::getenv("TTC_RING_SM_KB")) * 1024 : 128 * 1024;
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      double best = -1.0;
+      int bT = T, bG = G;
+      const size_t ring0 = ring;
+      size_t bring = ring;
+      const int Tsave = T;
+      for (int t : {512, 256})
+        for (int cps : {1, 2}) {
+          if (t * cps > 512) continue;
+          T = t;
+          cudaFuncAttributes fa = {};
+          if (cudaFuncGetAttributes(&fa, sweeps_for(false)) != cudaSuccess) { cudaGetLastError(); continue; }
+          const long long avail = std::min<long long>(smem_sm / cps - 1024, optin) - (long long)fa.sharedSizeBytes -
+                                  (long long)fnode_bytes;
+          const long long unit = (long long)t * 16 * (long long)sizeof(double);   // a 16-term stage per warp
+          // (at most ring_sm per SM: the rest of the 256 KB L1 / shared memory stays L1 for the
+          // tables and factor rows the steps read through it -- 192 KB rings measured slower)
+          const long long cap_b = std::min<long long>(avail, ring_sm / cps);
+          const size_t rg = ring_env ? ring_env : (size_t)std::max(0LL, cap_b / unit * unit);
+          if (rg < (size_t)2 * unit || rg < ext_bytes || (long long)rg > avail) continue;
+          ring = rg;
+          for (int g = std::min<long long>(16, by_rows); g >= 1; --g) {
+            if (resident(g, false) < nj || resident_of(sweeps_for(false), g, false) < nj) continue;
+            const double score = (double)nj * g * rg + 1e-3 * (double)nj * g * t;   // ring, then threads
+            if (score > best) { best = score; bT = t; bG = g; bring = rg; }
+            break;   // (the largest resident g for this (t, cps))
+          }
+        }
+      T = Tsave;
+      ring = ring0;
+      if (best > 0) { T = bT; G = bG; ring = bring; dc.G = G; }
+    }
     c->greedy_threads = T;
     c->greedy_cached = cached;
     c->greedy_smem = smem_for(G, cached);
-    dc.ring_tb = (int)std::min<size_t>(8, c->greedy_smem / (sizeof(double) * RING_P * T));
+    dc.fnode_off = (int)(base_for(G, cached) / sizeof(double));
+    const size_t ring_part = base_for(G, cached);
+    dc.ring_tb = (int)std::min<size_t>(8, ring_part / (sizeof(double) * RING_P * T));
     // TMA ring: 16 terms per stage when two stages per warp fit (D_20: 20.8 ms vs 24.0 with 8
     // terms x 4 stages, C_200 5.39 vs 6.01; profiles/r02_ring_shape.log)
-    if (TTC_TMA && !cached && c->greedy_smem >= 2 * 16 * (size_t)T * sizeof(double)) dc.ring_tb = 16;
+    if (TTC_TMA && !cached && ring_part >= 2 * 16 * (size_t)T * sizeof(double)) dc.ring_tb = 16;
     if (const char* e = std::getenv("TTC_RING_TB")) {   // (experiments: terms per ring stage)
       const int v = std::atoi(e);
-      if (v >= 1 && v <= 64 && (size_t)v * 2 * T * sizeof(double) <= c->greedy_smem) dc.ring_tb = v;
+      if (v >= 1 && v <= 64 && (size_t)v * 2 * T * sizeof(double) <= ring_part) dc.ring_tb = v;
     }
-    // TMA ring (non-cached shape): stages of T rows x ring_tb terms in the same dynamic shared
-    // memory, as many as fit (<= TMA_PMAX); TTC_NO_TMA=1 keeps the cp.async DotRing (A/B)
+    // TMA ring (non-cached shape): stages of T rows x ring_tb terms in the ring part of the
+    // dynamic shared memory, as many as fit (<= TMA_PMAX)
     dc.ring_tb = std::max(1, dc.ring_tb);   // (cached shapes: the ring is not used)
     dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / std::max(1, T / 32)),
-                                      c->greedy_smem / (sizeof(double) * (size_t)T * dc.ring_tb));
+                                      ring_part / (sizeof(double) * (size_t)T * dc.ring_tb));
     dc.tma = TTC_TMA && !cached && dc.ring_p >= 2;
     dc.ext_tile = extend_tile_rows(cap);
     c->greedy_fn = fn_for(c->greedy_cached);
     {
-      const bool big = T > 256;
-      switch (k.family) {
-        case TTC_FAMILY_C:
-          c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<0, true, 512> : (const void*)k_sweeps<0, false, 512>)
-                             : (cached ? (const void*)k_sweeps<0, true, 256> : (const void*)k_sweeps<0, false, 256>);
-          break;
-        case TTC_FAMILY_D:
-          c->sweeps_fn = big ? (cached ? (const void*)k_sweeps<1, true, 512> : (const void*)k_sweeps<1, false, 512>)
-                             : (cached ? (const void*)k_sweeps<1, true, 256> : (const void*)k_sweeps<1, false, 256>);
-          break;
-        case TTC_FAMILY_CX: c->sweeps_fn = big ? (const void*)k_sweeps<2, false, 512> : (const void*)k_sweeps<2, false, 256>; break;
-        case TTC_FAMILY_DX: c->sweeps_fn = big ? (const void*)k_sweeps<3, false, 512> : (const void*)k_sweeps<3, false, 256>; break;
-        default: c->sweeps_fn = big ? (const void*)k_sweeps<4, false, 512> : (const void*)k_sweeps<4, false, 256>; break;
-      }
+      c->sweeps_fn = sweeps_for(cached);
       // the wavefront needs every cluster resident at once
       // (queried for the persistent kernel itself: its register / shared-memory footprint
       // differs from the single-sweep kernel's)
@@ -1172,7 +1232,7 @@ int tt_cross_get_launch_shape(ttc_ctx* c, int32_t* cluster, int32_t* threads, in
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (cluster) *cluster = c->dc.G;
   if (threads) *threads = c->greedy_threads;
-  if (cached) *cached = c->greedy_cached ? 1 : 0;
+  if (cached) *cached = (c->greedy_cached ? 1 : 0) | (c->persistent ? 2 : 0);
   if (smem_bytes) *smem_bytes = (int64_t)c->greedy_smem;
   return TTC_OK;
 }

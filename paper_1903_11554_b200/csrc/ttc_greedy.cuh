@@ -829,7 +829,9 @@ struct GreedySmem {
   alignas(16) double vec[TTC_MAX_RANK_DEV];   // V[t][y*] (column step) or U[t][x*] (row step) (paired reads)
   // factors of the fixed column (row) of a step
   DDE f_slot[TTC_MAX_RANK_DEV];      // column step: CX[alpha][beta]*QL1[alpha][b]; row step: CX*QR0
-  DDE f_node[STAGE_N];               // column step: QR0[beta][a]; row step: QL1[alpha][b]
+  // (f_node -- column step: QR0[beta][a]; row step: QL1[alpha][b] -- lives in the dynamic
+  // shared memory at c.fnode_off, sized for n: the static footprint stays small, so the
+  // rook-step ring can take the rest of the SM's shared memory)
   ESum fs;                           // SB[beta][b] (column step) or SA[alpha][a] (row step)
   DDE fp;                            // PB[beta][b] or PA[alpha][a]
   double pv;                         // E(x*, y*) of the final pivot (owner CTA of column y*)
@@ -1074,6 +1076,7 @@ struct StepCtx {
   int ring_p;                           // TMA ring stages
   bool tma;                             // stream through the TMA ring (else the cp.async DotRing)
   RingPos* rpos;                        // TMA ring position (persists across steps and sweeps)
+  DDE* f_node;                          // staged node factors (dynamic shared memory, stage_n)
 };
 
 // column step E(:, y) on this CTA's rows -> U[r][:] (or the row cache), raw values; returns
@@ -1100,7 +1103,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       S.f_slot[al] = f;
     }
     if (X.stage_n)
-      for (int a = tid; a < n; a += T) S.f_node[a] = c.QR0[jo + be * n + a];
+      for (int a = tid; a < n; a += T) X.f_node[a] = c.QR0[jo + be * n + a];
   }
   const double ub = X.uk1[b];
   __syncthreads();
@@ -1155,7 +1158,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
       DDE p = CACHED ? X.PAc[x - xb] : c.PA[jo + x];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[al]);
-      dde_mul(p, X.stage_n ? S.f_node[a] : c.QR0[jo + be * n + a]);
+      dde_mul(p, X.stage_n ? X.f_node[a] : c.QR0[jo + be * n + a]);
       bool o1, o2;
       DDE pr = p;
       dde_mul_d(pr, rho_fast(ua, ub, o1));
@@ -1216,7 +1219,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       S.f_slot[be] = f;
     }
     if (X.stage_n)
-      for (int b = tid; b < n; b += T) S.f_node[b] = c.QL1[jo + al * n + b];
+      for (int b = tid; b < n; b += T) X.f_node[b] = c.QL1[jo + al * n + b];
   }
   const double ua = X.uk[a];
   __syncthreads();
@@ -1269,7 +1272,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
       DDE p = CACHED ? X.PBc[y - yb] : c.PB[jo + y];
       dde_mul(p, S.fp);
       dde_mul(p, S.f_slot[be]);
-      dde_mul(p, X.stage_n ? S.f_node[b] : c.QL1[jo + al * n + b]);
+      dde_mul(p, X.stage_n ? X.f_node[b] : c.QL1[jo + al * n + b]);
       bool o1, o2;
       DDE pr = p;
       dde_mul_d(pr, rho_fast(ua, ub, o1));
@@ -1447,8 +1450,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
   }
   // Alg. 2 line 1 sample positions of this sweep, drawn now (they depend only on the sweep,
   // k and the superblock shape) by the warps after warp 0, which starts the tables; kept in
-  // S.f_node until the samples phase (the rook steps restage it afterwards)
-  int* smp = reinterpret_cast<int*>(S.f_node);
+  // the f_node region until the samples phase (the rook steps restage it afterwards)
+  DDE* f_node = reinterpret_cast<DDE*>(dyn + c.fnode_off);
+  int* smp = reinterpret_cast<int*>(f_node);
   {
     const uint64_t tag = 1ULL + (uint64_t)sweep;
     for (int q = tid >= 32 ? tid - 32 : tid + T - 32; q < c.ns; q += T) {
@@ -1689,7 +1693,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       const int q = (int)S.best.idx;
       xst = smp[2 * q];
       yst = smp[2 * q + 1];
-      // smp aliases S.f_node, which the first column step (family D, staged) overwrites
+      // smp aliases f_node, which the first column step (family D, staged) overwrites
       // before its own barrier: every thread must have read the winner first
       if (FAMILY == 1 && stage_n) __syncthreads();
       if (cr == 0 && tid == 0) {
@@ -1718,7 +1722,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
     }
     StepCtx X{&cs, &S, job, k, n, cap, r, rl, rr, tid, T, xb, xe, yb, ye, sbn, rpcap, jo, jcx,
               U, V, Araw, Uc, Ecol, Acol, Vc, Erow, SAc, PAc, SBc, PBc, uk, uk1, stage_n, rowmask, colmask,
-              timer, dyn, c.ring_tb, c.ring_p, c.tma != 0, &rpos};
+              timer, dyn, c.ring_tb, c.ring_p, c.tma != 0, &rpos, f_node};
     auto column = [&](int y, bool search) -> int {
       double bv;
       long long bf;
