@@ -934,6 +934,13 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / std::max(1, T / 32)),
                                       ring_part / (sizeof(double) * (size_t)T * dc.ring_tb));
     dc.tma = TTC_TMA && !cached && dc.ring_p >= 2;
+    // rows per thread from which a step streams through the ring (the DotRing needs a few rows
+    // per thread to fill its stages; the TMA ring streams any row count)
+    dc.ring_min = dc.tma ? 1 : RING_MIN_ROWS;
+    if (const char* e = std::getenv("TTC_RING_MIN")) {   // (experiments)
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= 64) dc.ring_min = v;
+    }
     dc.ext_tile = extend_tile_rows(cap);
     c->greedy_fn = fn_for(c->greedy_cached);
     {

@@ -779,6 +779,11 @@ __host__ __device__ __forceinline__ long long extend_smem_doubles(int cap) {
 #define TMA_NBAR 128  // TMA ring barriers: warps x stages
 #define STAGE_N 1024  // n up to which the n-indexed factor of a step is staged in shared memory
 
+#ifndef TTC_PREFETCH
+#define TTC_PREFETCH 0   // rook steps: prefetch the next row block's tables into L1 (A/B)
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 struct Cand {
   double val;
   long long idx;
@@ -1038,8 +1043,10 @@ struct TmaRing {
           e = __dsub_rn(e, __dmul_rn(src[i * 32], vv.x));
           e = __dsub_rn(e, __dmul_rn(src[(i + 1) * 32], vv.y));
         }
-      } else {
-        for (int i = 0; i < tn; ++i) e = __dsub_rn(e, __dmul_rn(src[i * 32], vec[t0 + i]));
+      } else {   // (the last stage of a rank that is not a multiple of 16: unrolled, guarded)
+#pragma unroll
+        for (int i = 0; i < 15; ++i)
+          if (i < tn) e = __dsub_rn(e, __dmul_rn(src[i * 32], vec[t0 + i]));
       }
       __syncwarp();   // (the slot is refilled two issues later, by lane 0 of this warp)
       if (++pos.slot == P) { pos.slot = 0; pos.phase ^= 1u; }
@@ -1110,7 +1117,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   TRACE(11);
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  const bool stream = !CACHED && xe - xb >= RING_MIN_ROWS * T;
+  const bool stream = !CACHED && xe - xb >= c.ring_min * T;
 #if TTC_TMA
   // (one ring kind per build: both live at once cost ~1 KB of spills per thread)
   constexpr bool use_ring = false;
@@ -1137,6 +1144,10 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   for (int x = xb + tid; x < xe; x += T, ++jrow) {
     constexpr bool valid = true;
 #endif
+    if (TTC_PREFETCH && !CACHED && FAMILY < 2 && valid && x + T < xe) {   // the next row block's tables
+      prefetch_l1(&c.SA[jo + x + T]);
+      if (FAMILY == 1) prefetch_l1(&c.PA[jo + x + T]);
+    }
     const int al = x / n, a = x - al * n;
     const double ua = X.uk[a];
     double raw;
@@ -1226,7 +1237,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   TRACE(21);
   double bv = -1.0;
   long long bf = LLONG_MAX;
-  const bool stream = !CACHED && ye - yb >= RING_MIN_ROWS * T;
+  const bool stream = !CACHED && ye - yb >= c.ring_min * T;
 #if TTC_TMA
   // (one ring kind per build: both live at once cost ~1 KB of spills per thread)
   constexpr bool use_ring = false;
@@ -1251,6 +1262,10 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   for (int y = yb + tid; y < ye; y += T, ++jcol) {
     constexpr bool valid = true;
 #endif
+    if (TTC_PREFETCH && !CACHED && FAMILY < 2 && valid && y + T < ye) {   // the next column block's tables
+      prefetch_l1(&c.SB[jo + y + T]);
+      if (FAMILY == 1) prefetch_l1(&c.PB[jo + y + T]);
+    }
     const int be = y / n, b = y - be * n;
     const double ub = X.uk1[b];
     double e;
@@ -1732,7 +1747,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       if (tid == 0) {
         evals += (unsigned long long)max(0, xe - xb);
         upd += (unsigned long long)max(0, xe - xb) * r;
-        ring_steps += !CACHED && xe - xb >= RING_MIN_ROWS * T;   // (column_eval's use_ring)
+        ring_steps += !CACHED && xe - xb >= c.ring_min * T;   // (column_eval's stream)
       }
       if (!search) {
         __syncthreads();
@@ -1755,7 +1770,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       if (tid == 0) {
         evals += (unsigned long long)max(0, ye - yb);
         upd += (unsigned long long)max(0, ye - yb) * r;
-        ring_steps += !CACHED && ye - yb >= RING_MIN_ROWS * T;   // (row_eval's use_ring)
+        ring_steps += !CACHED && ye - yb >= c.ring_min * T;   // (row_eval's stream)
       }
       if (!search) {
         __syncthreads();
