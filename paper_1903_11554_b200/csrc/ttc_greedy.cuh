@@ -581,6 +581,56 @@ __device__ __forceinline__ void ext_raw4(double (&v)[4], int i0, int L, int l, i
   }
 }
 
+// phase-2 recurrence of one row group (see extend_side_reg): lane l of the L lanes holds
+// acc[i] = slot s = L*i + l; for t = 0..r-1 the owner lane's acc_t (columns: / u_t(x_t)) is
+// broadcast and every slot s > t subtracts f * coef[t][s] -- per s the oracle's operations in
+// its t order.
+template <int L>
+__device__ __forceinline__ void ext_rec(double (&acc)[EXR_NS], int r, int l, int gbase, int side, const double* pdiag,
+                                        const double* prcp, const double* coefL) {
+  constexpr int LG = L == 1 ? 0 : (L == 2 ? 1 : 2);
+#pragma unroll
+  for (int ph = 0; ph < EXR_NS / 4; ++ph) {
+    const int tb = 4 * L * ph;   // (a constant: the phase loop is unrolled)
+    if (tb >= r) break;          // (warp-uniform)
+#pragma unroll 1
+    for (int t = tb; t < tb + 4 * L; ++t) {   // (constant trip count: no bound to spill)
+      if (t >= r) continue;                    // (warp-uniform)
+      const int it = t >> LG, lt = t & (L - 1);
+      double own = acc[4 * ph];
+#pragma unroll
+      for (int u = 1; u < 4; ++u)
+        if (it == 4 * ph + u) own = acc[4 * ph + u];
+      const double2* cf = reinterpret_cast<const double2*>(coefL + (t * L + l) * EXR_CS);
+      // the phase's own four coefficients, loaded before the broadcast / division
+      const double2 c0 = cf[2 * ph], c1 = cf[2 * ph + 1];
+      double f = __shfl_sync(0xffffffffu, own, gbase + lt);
+      if (side == 1) {   // v_t = acc_t / u_t(x_t) (= __ddiv_rn bits)
+        bool ok;
+        const double q = div_pre_fast(f, pdiag[t], prcp[t], ok);
+        f = ok ? q : div_pre(f, pdiag[t], prcp[t]);
+      }
+      const int thr = (t - l) >> LG;   // slots i <= thr hold s <= t (arithmetic shift: -1 for t < l)
+      // the phase's own four slots: s > t depends on the lane
+      if (4 * ph > thr) acc[4 * ph] = __dsub_rn(acc[4 * ph], __dmul_rn(f, c0.x));
+      if (4 * ph + 1 > thr) acc[4 * ph + 1] = __dsub_rn(acc[4 * ph + 1], __dmul_rn(f, c0.y));
+      if (4 * ph + 2 > thr) acc[4 * ph + 2] = __dsub_rn(acc[4 * ph + 2], __dmul_rn(f, c1.x));
+      if (4 * ph + 3 > thr) acc[4 * ph + 3] = __dsub_rn(acc[4 * ph + 3], __dmul_rn(f, c1.y));
+      // later slots: s >= L*(4*ph + 4) > t on every lane (no predicate), in groups of four
+      // whose coefficient loads the compiler is free to hoist (no stores in between)
+#pragma unroll
+      for (int i = 4 * ph + 4; i < EXR_NS; i += 4) {
+        if (L * i >= r) break;   // (warp-uniform: no lane has a slot s < r from here on)
+        const double2 a0 = cf[i >> 1], a1 = cf[(i >> 1) + 1];
+        acc[i] = __dsub_rn(acc[i], __dmul_rn(f, a0.x));
+        acc[i + 1] = __dsub_rn(acc[i + 1], __dmul_rn(f, a0.y));
+        acc[i + 2] = __dsub_rn(acc[i + 2], __dmul_rn(f, a1.x));
+        acc[i + 3] = __dsub_rn(acc[i + 3], __dmul_rn(f, a1.y));
+      }
+    }
+  }
+}
+
 template <int FAMILY>
 __device__ __noinline__ void extend_side_reg(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
                                              int x_hi, const int* p_al, const int* p_a, const double* pdiag,
@@ -718,34 +768,14 @@ __device__ __noinline__ void extend_side_reg(const DevCtx& c, int sweep, int job
     clock_to(PH_EXT_RAW);
     // (2) the recurrence: t in four phases of 4 * L (a runtime loop each, its slot updates
     // unrolled over the slots a phase can still reach, predicated on s > t; f = acc_t read
-    // from the phase's four candidate slots by selects): small, spill-free code
-#pragma unroll
-    for (int ph = 0; ph < EXR_NS / 4; ++ph) {
-      const int tb = 4 * L * ph;   // (a constant: the phase loop is unrolled)
-      if (tb >= r) break;   // (warp-uniform)
-#pragma unroll 1
-      for (int t = tb; t < tb + 4 * L; ++t) {   // (constant trip count: no bound to spill)
-        if (t >= r) continue;   // (warp-uniform)
-        const int it = t / L, lt = t - it * L;
-        double own = acc[4 * ph];
-#pragma unroll
-        for (int u = 1; u < 4; ++u)
-          if (it == 4 * ph + u) own = acc[4 * ph + u];
-        double f = __shfl_sync(0xffffffffu, own, gbase + lt);
-        if (side == 1) {   // v_t = acc_t / u_t(x_t) (= __ddiv_rn bits)
-          bool ok;
-          const double q = div_pre_fast(f, pdiag[t], prcp[t], ok);
-          f = ok ? q : div_pre(f, pdiag[t], prcp[t]);
-        }
-        const double2* cf = reinterpret_cast<const double2*>(coefL + (t * L + l) * EXR_CS);
-#pragma unroll
-        for (int i = 4 * ph; i < EXR_NS; i += 2) {   // (paired 16-byte reads)
-          const double2 cc = cf[i >> 1];
-          if (L * i + l > t) acc[i] = __dsub_rn(acc[i], __dmul_rn(f, cc.x));
-          if (L * (i + 1) + l > t) acc[i + 1] = __dsub_rn(acc[i + 1], __dmul_rn(f, cc.y));
-        }
-      }
-    }
+    // from the phase's four candidate slots by selects): small, spill-free code.  L is a
+    // template constant here (ext_rec<L>): the slot predicate is one compare with an
+    // immediate, and a phase's coefficient pairs are all read before the first update (the
+    // runtime-L form re-used one register quad per pair: eight dependent shared-memory round
+    // trips per t, ~800 cycles per t on D_20)
+    if (L == 1) ext_rec<1>(acc, r, l, gbase, side, pdiag, prcp, coefL);
+    else if (L == 2) ext_rec<2>(acc, r, l, gbase, side, pdiag, prcp, coefL);
+    else ext_rec<4>(acc, r, l, gbase, side, pdiag, prcp, coefL);
     clock_to(PH_EXT_REC);
     // (3) final values
     if (valid) {
