@@ -937,6 +937,11 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     // rows per thread from which a step streams through the ring (the DotRing needs a few rows
     // per thread to fill its stages; the TMA ring streams any row count)
     dc.ring_min = dc.tma ? 1 : RING_MIN_ROWS;
+    dc.l2_keep = 0.f;
+    if (const char* e = std::getenv("TTC_L2_KEEP")) {   // (experiments)
+      const float v = (float)std::atof(e);
+      if (v >= 0.f && v <= 1.f) dc.l2_keep = v;
+    }
     if (const char* e = std::getenv("TTC_RING_MIN")) {   // (experiments)
       const int v = std::atoi(e);
       if (v >= 1 && v <= 64) dc.ring_min = v;

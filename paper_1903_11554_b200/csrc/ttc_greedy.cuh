@@ -728,6 +728,10 @@ __device__ __noinline__ void extend_side_reg(const DevCtx& c, int sweep, int job
     const int nrow = x1 - x0;
     const int j = tid / L;
     const bool valid = j < nrow;
+    if ((tid & ~31) / L >= nrow) {   // a warp with no row in this pass (the last, partial one) idles
+      x0 = x1;
+      continue;
+    }
     const int x = x0 + (valid ? j : nrow - 1);   // (a lane past the pass repeats the last row)
     const int z = x - sl0 * n;                   // node of the row within its slot
     // (1) raw entries, four slots per iteration (their table gathers issued together: a
@@ -1014,11 +1018,13 @@ struct TmaRing {
   unsigned long long* full;   // this warp's P barriers
   int lane, tb, P, nb, r, ybase, x0, T;
   int total, is;              // stages of this step, issued (lane 0)
+  float keep;                 // L2 evict_last fraction of the stream (c.l2_keep)
   int ijb, ib;                // row block and term block of the next stage to issue (no division per stage)
   RingPos pos, ipos;          // consumption / issue position
   __device__ __forceinline__ void start(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
-                                        int P_, int r_, int ybase_, int xb, int xe, RingPos p) {
+                                        int P_, int r_, int ybase_, int xb, int xe, RingPos p, float keep_) {
     const int warp = tid >> 5;
+    keep = keep_;
     lane = tid & 31;
     tmap = tmap_; T = T_; tb = tb_; P = P_; r = r_; ybase = ybase_;
     wbuf = buf + (long long)warp * P * tb * 32;
@@ -1041,7 +1047,10 @@ struct TmaRing {
     const int x = x0 + ijb * T, y = ybase + ib * tb;
     if (EVICT_FIRST) {
       unsigned long long pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      if (keep > 0.f)   // a fraction of the lines evict_last: they survive until the next step
+        asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(keep));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
           " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst), "l"(tmap), "r"(x), "r"(y), "r"(fa), "l"(pol)
@@ -1153,7 +1162,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
   constexpr bool use_ring = false;
   const bool use_tma = stream && X.tma;   // (else plain loads)
   TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> ring;
-  if (use_tma) ring.start(X.ring, c.tmapU, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, xb, xe, *X.rpos);
+  if (use_tma) ring.start(X.ring, c.tmapU, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, xb, xe, *X.rpos, c.l2_keep);
 #else
   constexpr bool use_tma = false;
   const bool use_ring = stream;
@@ -1273,7 +1282,7 @@ __device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out
   constexpr bool use_ring = false;
   const bool use_tma = stream && X.tma;   // (else plain loads)
   TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> ring;
-  if (use_tma) ring.start(X.ring, c.tmapV, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, yb, ye, *X.rpos);
+  if (use_tma) ring.start(X.ring, c.tmapV, &S, T, tid, X.ring_tb, X.ring_p, r, X.job * cap, yb, ye, *X.rpos, c.l2_keep);
 #else
   constexpr bool use_tma = false;
   const bool use_ring = stream;
