@@ -145,22 +145,16 @@ __device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, doub
 // evaluated on the fly, nothing written per entry.
 // A CTA owns a tile of FW_TA x FW_TB fibers (thread = fiber) and one of NS node ranges; the
 // NS CTAs of a tile form a cluster (1, NS, 1) and combine their partial sums through
-// distributed shared memory in node-range order.  The node range is walked in chunks of
-// FW_CH nodes, double-buffered in shared memory with cp.async: the chunk's Q_L rows of the
-// tile's alphas, Q_R rows of its betas (hi / lo / e planes, row stride FW_CH + 1 so the 16
-// rows a warp reads at one node fall in distinct banks) and c_m, w_m of its nodes -- every
-// factor is fetched once per tile instead of once per entry.  The fiber's frozen factors
-// (S_L + S_R, Pf) stay in registers.
-// P = Pf * Q_L * Q_R is formed without intermediate renormalisation: every stored factor has
-// hi in [2^-250, 1] (or 0), so the partial products and their error terms stay normal and
-// the result is the renormalised chain's up to an exact power of two; dde_div applies it --
-// the same bits as dde_mul + dde_round + division (R3).  Every
-// term w_a * A >= 0 (positive weights, positive entries), so the double-double accumulation
-// is the same-sign sum: two_sum of the high parts, low parts added, one renormalisation
-// (relative error ~2^-104 per term, no cancellation).
+// distributed shared memory in node-range order.  The CTA stages its node range (<= FW_CH
+// nodes: every configuration's range fits in one chunk, so one barrier pair per CTA instead of
+// one per 33-node chunk) in shared memory with cp.async: the Q_L rows of the tile's alphas, Q_R
+// rows of its betas (hi / lo / e planes, odd row stride FW_CH + 1 so the 16 rows a warp reads
+// at one node fall in distinct banks) and c_m, w_m of its nodes -- every factor is fetched once
+// per tile instead of once per entry.  The fiber's frozen factors (S_L + S_R, Pf) stay in
+// registers.
 #define FW_TA 16
 #define FW_TB 16
-#define FW_CH 36   // max nodes per chunk (row stride 37 doubles: 16 rows in distinct banks)
+#define FW_CH 72   // max nodes per chunk (row stride 73 doubles: 16 rows in distinct banks)
 #define FW_RS (FW_CH + 1)
 struct FwBuf {
   double qlh[FW_TA][FW_RS], qll[FW_TA][FW_RS];
@@ -169,7 +163,7 @@ struct FwBuf {
   long long chi[FW_CH], clo[FW_CH];
   double w[FW_CH];
 };
-__host__ __device__ constexpr int fw_smem_bytes() { return 2 * (int)sizeof(FwBuf); }
+__host__ __device__ constexpr int fw_smem_bytes() { return (int)sizeof(FwBuf); }
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -245,20 +239,16 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
   }
   double hi = 0.0, lo = 0.0;
   double* F = EMIT ? c.fib + (long long)j * c.fib_stride + ((long long)al * jb.ry + be) * n : nullptr;
-  // balanced chunks of <= FW_CH nodes (65 nodes: 33 + 32, not 36 + 29 or 32 + 32 + 1)
+  // balanced chunks of <= FW_CH nodes (one for every configuration's node range)
   const int nchunk = (a_hi - a_lo + FW_CH - 1) / FW_CH;
   const int csz = nchunk > 0 ? (a_hi - a_lo + nchunk - 1) / nchunk : 0;
-  if (nchunk > 0) stage(0, a_lo, min(csz, a_hi - a_lo));
   for (int ci = 0; ci < nchunk; ++ci) {
     const int a0 = a_lo + ci * csz, cn = min(csz, a_hi - a0);
-    if (ci + 1 < nchunk) {
-      stage((ci + 1) & 1, a0 + csz, min(csz, a_hi - a0 - csz));
-      cp_async_wait_group<1>();
-    } else {
-      cp_async_wait_group<0>();
-    }
+    if (ci > 0) __syncthreads();   // (the previous chunk is read by every thread before restaging)
+    stage(0, a0, cn);
+    cp_async_wait_group<0>();
     __syncthreads();
-    const FwBuf& B = buf[ci & 1];
+    const FwBuf& B = buf[0];
     if (live) {
 #pragma unroll 2
       for (int a = 0; a < cn; ++a) {
@@ -291,7 +281,6 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
         lo = __dsub_rn(l1, __dsub_rn(hi, s1));
       }
     }
-    __syncthreads();   // buffer ci & 1 is restaged at iteration ci + 1
   }
   part[tid] = DD{hi, lo};
   if (NS == 1) {
