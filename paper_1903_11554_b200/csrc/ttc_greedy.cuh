@@ -526,6 +526,9 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
 //   (3) the final values (columns: acc_s / u_s(x_s)) straight to U / V.
 // coef[t][s] is kept as coefL[t][l][i] (s = L*i + l), so a lane's slots are contiguous.
 #define EXR_NS 16
+#ifndef TTC_EXT_INLINE
+#define TTC_EXT_INLINE __noinline__   // (A/B: __forceinline__ puts phase 2 in the kernel's register allocation)
+#endif
 struct ExtFix {
   DDE F;      // rows: PB[be_s][b_s] * CX[al][be_s] * QL1[al][b_s]; columns: PA[al_s][a_s] * CX[al_s][be] * QR0[be][a_s]
   ESum S;     // rows: SB[be_s][b_s]; columns: SA[al_s][a_s]
@@ -581,6 +584,11 @@ __device__ __forceinline__ void ext_raw4(double (&v)[4], int i0, int L, int l, i
   }
 }
 
+// the column recurrence's divisors u_t(x_t) and their refined reciprocals: file-scope shared
+// arrays (constant addresses: ext_rec reads them without a pointer that the register
+// allocator of the sweep kernel would spill to local memory)
+__shared__ double s_pdiag[TTC_MAX_RANK_DEV], s_prcp[TTC_MAX_RANK_DEV];
+
 // phase-2 recurrence of one row group (see extend_side_reg): lane l of the L lanes holds
 // acc[i] = slot s = L*i + l; for t = 0..r-1 the owner lane's acc_t (columns: / u_t(x_t)) is
 // broadcast and every slot s > t subtracts f * coef[t][s] -- per s the oracle's operations in
@@ -602,13 +610,14 @@ __device__ __forceinline__ void ext_rec(double (&acc)[EXR_NS], int r, int l, int
       for (int u = 1; u < 4; ++u)
         if (it == 4 * ph + u) own = acc[4 * ph + u];
       const double2* cf = reinterpret_cast<const double2*>(coefL + (t * L + l) * EXR_CS);
-      // the phase's own four coefficients, loaded before the broadcast / division
+      // the phase's own four coefficients and the divisor, loaded before the broadcast
       const double2 c0 = cf[2 * ph], c1 = cf[2 * ph + 1];
+      const double pd = s_pdiag[t], pr = s_prcp[t];
       double f = __shfl_sync(0xffffffffu, own, gbase + lt);
       if (side == 1) {   // v_t = acc_t / u_t(x_t) (= __ddiv_rn bits)
         bool ok;
-        const double q = div_pre_fast(f, pdiag[t], prcp[t], ok);
-        f = ok ? q : div_pre(f, pdiag[t], prcp[t]);
+        const double q = div_pre_fast(f, pd, pr, ok);
+        f = ok ? q : div_pre(f, pd, pr);
       }
       const int thr = (t - l) >> LG;   // slots i <= thr hold s <= t (arithmetic shift: -1 for t < l)
       // the phase's own four slots: s > t depends on the lane
@@ -632,7 +641,7 @@ __device__ __forceinline__ void ext_rec(double (&acc)[EXR_NS], int r, int l, int
 }
 
 template <int FAMILY>
-__device__ __noinline__ void extend_side_reg(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
+__device__ TTC_EXT_INLINE void extend_side_reg(const DevCtx& c, int sweep, int job, int k, int side, int r, int x_lo,
                                              int x_hi, const int* p_al, const int* p_a, const double* pdiag,
                                              const double* prcp, double* dyn, long long smem_doubles,
                                              unsigned long long& ent, unsigned long long& upd) {
@@ -1559,7 +1568,8 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
   const unsigned long long t_ext0 = ext_clock ? gtimer() : 0;
   {
     __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
-    __shared__ double pdiag[TTC_MAX_RANK_DEV], prcp[TTC_MAX_RANK_DEV];
+    double* pdiag = s_pdiag;
+    double* prcp = s_prcp;
     double* coef = dyn;
     double* tile = dyn + (long long)cap * cap;
     const long long ext_dyn = extend_smem_doubles(cap);   // (dynamic shared memory is at least this)

@@ -14,7 +14,8 @@ using namespace ttc;
 template <int L>
 __global__ void __launch_bounds__(512, 1) k_rec(int r, int side, int reps, double* sink, unsigned long long* out) {
   extern __shared__ double coefL[];
-  __shared__ double pdiag[64], prcp[64];
+  double* pdiag = s_pdiag;
+  double* prcp = s_prcp;
   const int cap = 64;
   for (int e = threadIdx.x; e < cap * L * EXR_CS; e += blockDim.x) coefL[e] = 1e-3 * ((e * 7) % 13) - 0.006;
   if (threadIdx.x < 64) {
