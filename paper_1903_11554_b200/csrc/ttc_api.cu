@@ -82,7 +82,7 @@ struct ttc_ctx {
   bool greedy_cached = false;  // k_sweep keeps its rows' u / columns' v in shared memory
   size_t greedy_smem = 0;      // dynamic shared memory of k_sweep
   int greedy_threads = 256;    // CTA size of k_sweep (256: two CTAs per SM, 512: one)
-  int fw_ns = 0;               // k_fiber_wsum cluster size override (TTC_FW_NS; 0 = host rule)
+  int fw_ns = 0;               // k_fiber_wsum node ranges per tile override (TTC_FW_NS; 0 = host rule)
   const void* greedy_fn = nullptr;   // k_sweep variant (one sweep)
   const void* sweeps_fn = nullptr;   // k_sweeps variant (persistent, world == 1)
   bool persistent = false;           // k_sweeps usable (all clusters resident)
@@ -220,7 +220,7 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool emit = false,
   {
     Timed t(c, K_FIBER);
     // tiles of FW_TA x FW_TB fibers (the grid covers rank = cap; tiles beyond the actual
-    // ranks exit at once) x NS node ranges, NS (the cluster size) doubled up to 8 while
+    // ranks exit at once) x NS node ranges, NS doubled up to 8 while
     // the grid has fewer than 4 waves of 4 CTAs per SM and the ranges keep >= 32 nodes
     const int ta = (tup + FW_TA - 1) / FW_TA, tb = (tup + FW_TB - 1) / FW_TB;
     const long long tiles = (long long)ta * tb * njobs;
@@ -232,13 +232,7 @@ int launch_fibers(ttc_ctx* c, int kind, int jbase, int njobs, bool emit = false,
     lc.blockDim = dim3(FW_TA * FW_TB);
     lc.dynamicSmemBytes = fw_smem_bytes();
     lc.stream = c->ls;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = ns;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = 0;   // (the NS CTAs of a tile are independent: last-arrival reduction)
     cudaError_t e;
     if (dc.family == TTC_FAMILY_C)
       e = emit ? cudaLaunchKernelEx(&lc, k_fiber_wsum<0, true>, dc, kind, jbase, tb)
@@ -686,6 +680,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &dc.pll, (size_t)c->slots * cap)) || (e = dalloc(c, &dc.prr, (size_t)c->slots * cap)) ||
       (e = dalloc(c, &dc.pf, (size_t)c->slots * cap * cap)) ||
       (e = dalloc(c, &dc.W, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.M, (size_t)d * cap * cap)) ||
+      (e = dalloc(c, &dc.wpart, (size_t)d * cap * cap * FW_NSMAX)) ||
+      (e = dalloc(c, &dc.wcnt, (size_t)d * ((cap + FW_TA - 1) / FW_TA) * ((cap + FW_TB - 1) / FW_TB))) ||
       (e = dalloc(c, &dc.H, (size_t)d * cap * cap)) || (e = dalloc(c, &dc.flags, 4)) ||
       (e = dalloc(c, &dc.rank_ring, (size_t)2 * d)) || (e = dalloc(c, &dc.done, (size_t)d)) ||
       (e = dalloc(c, &dc.counters, TTC_NCOUNTERS)) || (e = dalloc(c, &c->phase_buf, TTC_PHASE_WORDS)) ||
@@ -693,6 +689,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &c->chainA, (size_t)(nj + 1) * cap * cap)) || (e = dalloc(c, &c->chainB, (size_t)(nj + 1) * cap * cap)) ||
       (e = dalloc(c, &c->chainAd, (size_t)(nj + 1) * 3)) || (e = dalloc(c, &c->chainBd, (size_t)(nj + 1) * 3)))
     return bail(e);
+  if (cudaMemset(dc.wcnt, 0, sizeof(int) * d * ((cap + FW_TA - 1) / FW_TA) * ((cap + FW_TB - 1) / FW_TB)) != cudaSuccess)
+    return bail(fail(TTC_ERR_CUDA, "cudaMemset(wcnt) failed"));
   if (k.family == TTC_FAMILY_D) {
     if ((e = dalloc(c, &dc.ql, (size_t)c->slots * cap * n)) || (e = dalloc(c, &dc.qr, (size_t)c->slots * cap * n)) ||
         (e = dalloc(c, &dc.PA, tab)) || (e = dalloc(c, &dc.PB, tab)) || (e = dalloc(c, &dc.QL1, tab)) ||

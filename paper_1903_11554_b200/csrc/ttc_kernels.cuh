@@ -144,8 +144,8 @@ __device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, doub
 // tt_integrate: W_m[alpha][beta] = sum_a w_{m,a} A(X_alpha, a, Y_beta) with the entries
 // evaluated on the fly, nothing written per entry.
 // A CTA owns a tile of FW_TA x FW_TB fibers (thread = fiber) and one of NS node ranges; the
-// NS CTAs of a tile form a cluster (1, NS, 1) and combine their partial sums through
-// distributed shared memory in node-range order.  The CTA stages its node range (<= FW_CH
+// NS CTAs of a tile write their partial sums to global memory and the last one to arrive
+// combines them in node-range order.  The CTA stages its node range (<= FW_CH
 // nodes: every configuration's range fits in one chunk, so one barrier pair per CTA instead of
 // one per 33-node chunk) in shared memory with cp.async: the Q_L rows of the tile's alphas, Q_R
 // rows of its betas (hi / lo / e planes, odd row stride FW_CH + 1 so the 16 rows a warp reads
@@ -156,6 +156,11 @@ __device__ __forceinline__ void dd_mul_raw(double& h, double& l, double yh, doub
 #define FW_TB 16
 #define FW_CH 72   // max nodes per chunk (row stride 73 doubles: 16 rows in distinct banks)
 #define FW_RS (FW_CH + 1)
+#define FW_NSMAX 8   // node ranges per tile (at most)
+#ifndef FW_MINB
+#define FW_MINB 4    // resident CTAs per SM the register budget is sized for
+#endif
+
 struct FwBuf {
   double qlh[FW_TA][FW_RS], qll[FW_TA][FW_RS];
   double qrh[FW_TB][FW_RS], qrl[FW_TB][FW_RS];
@@ -178,15 +183,13 @@ __device__ __forceinline__ void cp_async8g(void* smem, const void* gmem) {
 // F[alpha][beta][a] -> c.fib, so the fiber entries checked against the oracle are the product
 // path's own (the stores are uncoalesced; diagnostics only).
 template <int FAMILY, bool EMIT>
-__global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int kind, int jbase, int tiles_b) {
+__global__ void __launch_bounds__(FW_TA * FW_TB, FW_MINB) k_fiber_wsum(DevCtx c, int kind, int jbase, int tiles_b) {
   extern __shared__ __align__(16) unsigned char fw_dyn[];
   FwBuf* buf = reinterpret_cast<FwBuf*>(fw_dyn);
-  __shared__ DD part[FW_TA * FW_TB];
-  cg::cluster_group cl = cg::this_cluster();
   const int j = jbase + blockIdx.z;
   Job jb = make_job(c, kind, j);   // (entries counted by k_frozen_sides)
   const int A0 = (blockIdx.x / tiles_b) * FW_TA, B0 = (blockIdx.x % tiles_b) * FW_TB;
-  if (A0 >= jb.rx || B0 >= jb.ry) return;   // (uniform over the cluster: same tile)
+  if (A0 >= jb.rx || B0 >= jb.ry) return;   // (uniform over the tile's NS CTAs)
   const int tid = threadIdx.x;
   const int ra = tid / FW_TB, rb = tid % FW_TB;
   const int al = A0 + ra, be = B0 + rb;
@@ -250,50 +253,104 @@ __global__ void __launch_bounds__(FW_TA * FW_TB, 4) k_fiber_wsum(DevCtx c, int k
     __syncthreads();
     const FwBuf& B = buf[0];
     if (live) {
-#pragma unroll 2
-      for (int a = 0; a < cn; ++a) {
-        ESum s = s0;
-        esum_add(s, B.chi[a], B.clo[a]);
-        const double S = esum_round(s);
-        const double SS = __dmul_rn(S, S);
-        double v;
-        bool ok;   // (branch-free divisions; the IEEE ones only for an entry off the fast path)
-        if (FAMILY == 0) {
-          v = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
-          if (!ok) v = __drcp_rn(SS);
-        } else {
-          double ph = p0.hi, pl = p0.lo;
-          dd_mul_raw(ph, pl, B.qlh[ra][a], B.qll[ra][a]);
-          dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
-          const DDE pe = DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0};
-          v = dde_div_fast(pe, SS, ok);
-          if (!ok) v = dde_div(pe, SS);
+      // groups of FW_ILP nodes: the entries of a group on their branch-free fast paths side by
+      // side (their dependent chains interleave), an entry off the fast path redone the plain
+      // way after the group, then the weighted terms accumulated in node order
+      // (family C: 4 -- 74 vs 84 us on C_200; family D: 2 -- its longer entry fills the issue
+      // slots already, 4 measured 3% slower on D_20)
+      constexpr int FW_ILP = FAMILY == 0 ? 4 : 2;
+#pragma unroll 1
+      for (int g0 = 0; g0 < cn; g0 += FW_ILP) {
+        double v[FW_ILP];
+        unsigned slow = 0;
+#pragma unroll
+        for (int u = 0; u < FW_ILP; ++u) {
+          const int a = min(g0 + u, cn - 1);
+          ESum s = s0;
+          esum_add(s, B.chi[a], B.clo[a]);
+          const double S = esum_round(s);
+          const double SS = __dmul_rn(S, S);
+          bool ok;
+          if (FAMILY == 0) {
+            v[u] = div_pre_fast(1.0, SS, rcp_refined(SS), ok);
+          } else {
+            double ph = p0.hi, pl = p0.lo;
+            dd_mul_raw(ph, pl, B.qlh[ra][a], B.qll[ra][a]);
+            dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
+            v[u] = dde_div_fast(DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0}, SS, ok);
+          }
+          slow |= (ok ? 0u : 1u) << u;
         }
-        if (EMIT) F[a0 + a] = v;
-        const double wa = B.w[a];
-        const double pr = __dmul_rn(wa, v);
-        const double pe = fma(wa, v, -pr);
-        const double s1 = __dadd_rn(hi, pr);
-        const double bb = __dsub_rn(s1, hi);
-        const double er = __dadd_rn(__dsub_rn(hi, __dsub_rn(s1, bb)), __dsub_rn(pr, bb));
-        const double l1 = __dadd_rn(lo, __dadd_rn(er, pe));
-        hi = __dadd_rn(s1, l1);
-        lo = __dsub_rn(l1, __dsub_rn(hi, s1));
+        if (slow) {   // (rare: the IEEE division, out of the group's chains)
+#pragma unroll 1
+          for (int u = 0; u < FW_ILP; ++u) {
+            if (!((slow >> u) & 1u)) continue;
+            const int a = min(g0 + u, cn - 1);
+            ESum s = s0;
+            esum_add(s, B.chi[a], B.clo[a]);
+            const double S = esum_round(s);
+            const double SS = __dmul_rn(S, S);
+            double w;
+            if (FAMILY == 0) {
+              w = __drcp_rn(SS);
+            } else {
+              double ph = p0.hi, pl = p0.lo;
+              dd_mul_raw(ph, pl, B.qlh[ra][a], B.qll[ra][a]);
+              dd_mul_raw(ph, pl, B.qrh[rb][a], B.qrl[rb][a]);
+              w = dde_div(DDE{ph, pl, p0.e + B.qle[ra][a] + B.qre[rb][a], 0}, SS);
+            }
+#pragma unroll
+            for (int q = 0; q < FW_ILP; ++q)
+              if (q == u) v[q] = w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < FW_ILP; ++u) {
+          if (g0 + u >= cn) break;
+          const int a = g0 + u;
+          if (EMIT) F[a0 + a] = v[u];
+          const double wa = B.w[a];
+          const double pr = __dmul_rn(wa, v[u]);
+          const double pe = fma(wa, v[u], -pr);
+          const double s1 = __dadd_rn(hi, pr);
+          const double bb = __dsub_rn(s1, hi);
+          const double er = __dadd_rn(__dsub_rn(hi, __dsub_rn(s1, bb)), __dsub_rn(pr, bb));
+          const double l1 = __dadd_rn(lo, __dadd_rn(er, pe));
+          hi = __dadd_rn(s1, l1);
+          lo = __dsub_rn(l1, __dsub_rn(hi, s1));
+        }
       }
     }
   }
-  part[tid] = DD{hi, lo};
+  const long long wi = ((long long)j * c.cap + al) * c.cap + be;
   if (NS == 1) {
-    if (live) c.W[((long long)j * c.cap + al) * c.cap + be] = part[tid];
+    if (live) c.W[wi] = DD{hi, lo};
     return;
   }
-  cl.sync();
-  if (ns == 0 && live) {
-    DD acc = part[tid];
-    for (int r = 1; r < NS; ++r) acc = dd_add(acc, cl.map_shared_rank(part, r)[tid]);
-    c.W[((long long)j * c.cap + al) * c.cap + be] = acc;
+  // the NS node-range partials go to global memory; the last CTA of the tile to arrive (a
+  // counter per tile) sums them in node-range order -- no CTA waits for the others (a cluster
+  // reduction kept every CTA of the tile resident until the slowest one finished)
+  if (live) c.wpart[wi * FW_NSMAX + ns] = DD{hi, lo};
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  if (tid == 0) {
+    int* cnt = &c.wcnt[(long long)j * gridDim.x + blockIdx.x];
+    const int old = atomicAdd(cnt, 1);
+    s_last = old == NS - 1;
+    if (s_last) *cnt = 0;   // (every CTA of the tile has arrived: ready for the next launch)
   }
-  cl.sync();   // the partials stay readable until rank 0 has summed them
+  __syncthreads();
+  if (s_last && live) {
+    __threadfence();
+    const double2 v0 = __ldcg(reinterpret_cast<const double2*>(&c.wpart[wi * FW_NSMAX]));   // (L2: written by other SMs)
+    DD acc = DD{v0.x, v0.y};
+    for (int q = 1; q < NS; ++q) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(&c.wpart[wi * FW_NSMAX + q]));
+      acc = dd_add(acc, DD{v.x, v.y});
+    }
+    c.W[wi] = acc;
+  }
 }
 
 // quadrature fibers of the x-form families: direct evaluation of every entry (the x-form
