@@ -994,9 +994,16 @@ struct DotRing {
 // rfull and reads back its own row's terms.  Warps never wait for each other (the cp.async
 // DotRing's property, without its 8-byte copy per thread and term).  The ring position
 // (slot, phase) is the same in every thread and persists across steps and sweeps (RingPos).
+#ifndef TTC_RING_PREFETCH
+#define TTC_RING_PREFETCH 0   // bit 0: the first column step's first stage during the samples; bit 1: a row step's after its column step (both measured slower: C_200 5.09 -> 5.39 ms, profiles/r02k_prefetch.log)
+#endif
+#ifndef TTC_FENCE_ALL
+#define TTC_FENCE_ALL 1       // the post-extension proxy fence covers shared memory too
+#endif
 struct RingPos {
   int slot;
   unsigned phase;
+  int pre;   // 1: the next step's first stage is already in flight (TmaRing::prefetch)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -1030,8 +1037,8 @@ struct TmaRing {
   float keep;                 // L2 evict_last fraction of the stream (c.l2_keep)
   int ijb, ib;                // row block and term block of the next stage to issue (no division per stage)
   RingPos pos, ipos;          // consumption / issue position
-  __device__ __forceinline__ void start(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
-                                        int P_, int r_, int ybase_, int xb, int xe, RingPos p, float keep_) {
+  __device__ __forceinline__ void setup(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_, int P_,
+                                        int r_, int ybase_, int xb, int xe, RingPos p, float keep_) {
     const int warp = tid >> 5;
     keep = keep_;
     lane = tid & 31;
@@ -1042,12 +1049,33 @@ struct TmaRing {
     nb = (r + tb - 1) / tb;
     total = xe > xb ? ((xe - xb + T - 1) / T) * nb : 0;
     pos = p;
-    ipos = p;
+    pos.pre = 0;
+    ipos = pos;
     is = 0;
     ijb = 0;
     ib = 0;
+  }
+  __device__ __forceinline__ void start(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
+                                        int P_, int r_, int ybase_, int xb, int xe, RingPos p, float keep_) {
+    setup(buf, tmap_, S, T_, tid, tb_, P_, r_, ybase_, xb, xe, p, keep_);
+    if (p.pre && total > 0) {   // stage 0 was issued by prefetch() into slot p.slot
+      is = 1;
+      if (++ib == nb) { ib = 0; ++ijb; }
+      if (++ipos.slot == P) { ipos.slot = 0; ipos.phase ^= 1u; }
+    }
     if (lane == 0)
-      for (int q = 0; q < P - 1 && is < total; ++q) issue();
+      for (int q = is; q < P - 1 && is < total; ++q) issue();
+  }
+  // the first stage of a step that is certain to follow (the ring is empty: every stage of the
+  // previous step consumed), issued while the current step's argmax -- or the samples phase --
+  // still runs: the data of a column step (U of the CTA's rows) does not depend on the column y,
+  // nor a row step's (V of its columns) on the row x.  Every thread marks p.pre.
+  __device__ __forceinline__ void prefetch(double* buf, const void* tmap_, GreedySmem* S, int T_, int tid, int tb_,
+                                           int P_, int r_, int ybase_, int xb, int xe, RingPos& p, float keep_) {
+    setup(buf, tmap_, S, T_, tid, tb_, P_, r_, ybase_, xb, xe, p, keep_);
+    if (total <= 0) return;
+    if (lane == 0) issue();
+    p.pre = 1;
   }
   __device__ __forceinline__ void issue() {   // lane 0: stage `is` into slot ipos
     const unsigned fa = smem_u32(&full[ipos.slot]);
@@ -1620,7 +1648,11 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
   TRACE(4);
   // (the rook steps read U / V through the TMA engine -- the async proxy: order this thread's
   // generic-proxy stores before the barrier that publishes them)
-  if (c.tma) asm volatile("fence.proxy.async.global;" ::: "memory");
+  // (and the extension's shared-memory scratch, which the TMA ring overwrites next)
+  if (c.tma) {
+    if (TTC_FENCE_ALL) asm volatile("fence.proxy.async;" ::: "memory");
+    else asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
   if (ext_clock && sweep < TTC_LOG_SWEEPS) c.phase_ns[TTC_NPHASES + sweep * TTC_LOG_W + 14 + (cr != 0)] += gtimer() - t_ext0;
   cl.sync();  // u / v of the new rows and columns visible to the whole cluster
   TRACE(5);
@@ -1706,6 +1738,12 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       cp_async_wait_all();
       TRACE(6);
       // visibility of the cache to the other threads: the __syncthreads of the first step
+    }
+    // the first column step's first ring stage, in flight during the samples phase (U of this
+    // CTA's rows: independent of the sampled column)
+    if ((TTC_RING_PREFETCH & 1) && !CACHED && c.tma && xe - xb >= c.ring_min * T) {
+      TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> pf;
+      pf.prefetch(dyn, c.tmapU, &S, T, tid, c.ring_tb, c.ring_p, r, job * cap, xb, xe, rpos, c.l2_keep);
     }
     // ---- Alg. 2 line 1: n_samples random entries, largest |E| (every CTA, identically).
     // A warp per four samples: the lanes load the u/v factors of all four at once (t = lane,
@@ -1801,6 +1839,12 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       if (!search) {
         __syncthreads();
         return -1;
+      }
+      // a search column step is always followed by a row step: its first ring stage (V of this
+      // CTA's columns) goes out before the argmax
+      if ((TTC_RING_PREFETCH & 2) && !CACHED && c.tma && ye - yb >= c.ring_min * T) {
+        TmaRing<TTC_EVICT_FIRST && FAMILY <= 1> pf;
+        pf.prefetch(dyn, c.tmapV, &S, T, tid, c.ring_tb, c.ring_p, r, job * cap, yb, ye, rpos, c.l2_keep);
       }
       argmax_step(&S, bv, bf, G, xstep);
       if (timer) {
@@ -1951,7 +1995,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
     for (int t = threadIdx.x; t < c.RS; t += blockDim.x) Rn[t] = Rc[t];
   cl.sync();  // record copy and exchange barriers ready
   int xstep = 0;
-  RingPos rpos{0, 0u};
+  RingPos rpos{0, 0u, 0};
   const int rn = sweep_body<FAMILY, CACHED>(c, s_ctx, S, dyn, sweep, job, r, rl, rr, Rn, xstep, rpos, true,
                                             c.sbstate[job * 4 + 0], c.sbstate[job * 4 + 1], false, false);
   if (cl.block_rank() == 0 && threadIdx.x == 0) {
@@ -1985,7 +2029,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
   int r = c.rank_ring[k * 2 + ((s0 - 1) & 1)];
   int rdone = c.sbstate[job * 4 + 0], cdone = c.sbstate[job * 4 + 1];
   int xstep = 0;
-  RingPos rpos{0, 0u};
+  RingPos rpos{0, 0u, 0};
   TRACE_INIT();
   xbar_init(&S);  // ordered before remote use by the cluster barriers of the first sweep
   tma_ring_init(&S);
