@@ -139,7 +139,11 @@ __device__ void sb_cx_table_warp(const DevCtx& c, int job, int al, int be) {
     act = min(32, np);
     for (int q = lane; q < np; q += 32) {
       const int i = q / nj, j = k + 2 + (q - i * nj);
-      dde_mul_d(p, rho_ool(c.u[i * n + TX[i]], c.u[j * n + TY[j]]));
+      const double xi = c.u[i * n + TX[i]], yj = c.u[j * n + TY[j]];
+      bool ok;
+      double rr = rho_fast(xi, yj, ok);   // (the IEEE division's bits; its slow path out of line)
+      if (!ok) rr = rho_ool(xi, yj);
+      dde_mul_d(p, rr);
     }
   }
 #pragma unroll
@@ -215,7 +219,13 @@ __device__ __noinline__ void sb_side_tables(const DevCtx& c, int job, int side, 
     if (c.family == 1)
       for (int a = lo + lane; a < hi; a += 32) {
         const double ua = c.u[a * n + T[a]];
-        for (int b = a + 1; b < hi; ++b) dde_mul_d(p, rho_ool(ua, c.u[b * n + T[b]]));
+        for (int b = a + 1; b < hi; ++b) {
+          const double ub = c.u[b * n + T[b]];
+          bool ok;
+          double rr = rho_fast(ua, ub, ok);
+          if (!ok) rr = rho_ool(ua, ub);
+          dde_mul_d(p, rr);
+        }
       }
     // butterfly levels with offset >= the lanes holding data only combine identities (exact
     // no-ops: +0, *1): skipped
