@@ -931,7 +931,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     dc.ring_tb = std::max(1, dc.ring_tb);   // (cached shapes: the ring is not used)
     dc.ring_p = (int)std::min<size_t>(std::min(TMA_PMAX, TMA_NBAR / std::max(1, T / 32)),
                                       ring_part / (sizeof(double) * (size_t)T * dc.ring_tb));
-    dc.tma = TTC_TMA && !cached && dc.ring_p >= 2;
+    dc.tma = TTC_TMA && !cached && dc.ring_p >= 2 && dc.ring_tb == 16;
+    if (dc.tma) dc.ring_p = 2;   // (TmaRing: two 16-term stages per warp, compile-time)
     // rows per thread from which a step streams through the ring (the DotRing needs a few rows
     // per thread to fill its stages; the TMA ring streams any row count)
     dc.ring_min = dc.tma ? 1 : RING_MIN_ROWS;

@@ -1042,7 +1042,10 @@ struct TmaRing {
   double* wbuf;               // this warp's P stages of [tb][32]
   const void* tmap;
   unsigned long long* full;   // this warp's P barriers
-  int lane, tb, P, nb, r, ybase, x0, T;
+  // (two stages of 16 terms per warp: compile-time constants -- the best measured shape, and
+  // fewer live registers in the consumer loop; the host sets ring_tb = 16, ring_p = 2)
+  static constexpr int tb = 16, P = 2;
+  int lane, nb, r, ybase, x0, T;
   int total, is;              // stages of this step, issued (lane 0)
   float keep;                 // L2 evict_last fraction of the stream (c.l2_keep)
   int ijb, ib;                // row block and term block of the next stage to issue (no division per stage)
@@ -1052,7 +1055,9 @@ struct TmaRing {
     const int warp = tid >> 5;
     keep = keep_;
     lane = tid & 31;
-    tmap = tmap_; T = T_; tb = tb_; P = P_; r = r_; ybase = ybase_;
+    tmap = tmap_; T = T_; r = r_; ybase = ybase_;
+    (void)tb_;
+    (void)P_;
     wbuf = buf + (long long)warp * P * tb * 32;
     full = &S->rfull[warp * P];
     x0 = xb + warp * 32;
@@ -1149,6 +1154,9 @@ __host__ __device__ __forceinline__ long long greedy_cache_doubles(long long rpc
   return rpcap * ((cap - 1) + 1 + 1 + 2 + 3 + (cap - 1) + 1 + 2 + 3);
 }
 
+#ifndef TTC_STEP_INLINE
+#define TTC_STEP_INLINE __forceinline__   // (__noinline__: StepCtx goes to local memory, D_20 14.7 -> 17.1 ms)
+#endif
 // everything a rook step needs (one per CTA, built once per launch)
 struct StepCtx {
   const DevCtx* c;
@@ -1177,7 +1185,7 @@ struct StepCtx {
 // once per step: S.fs = SB[beta][b], S.fp = PB[beta][b], f_slot[alpha] = CX[alpha][beta] *
 // QL1[alpha][b], f_node[a] = QR0[beta][a].
 template <int FAMILY, bool CACHED>
-__device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_out, long long& bf_out) {
+__device__ TTC_STEP_INLINE void column_eval(const StepCtx& X, int y, double& bv_out, long long& bf_out) {
   const DevCtx& c = *X.c;
   GreedySmem& S = *X.S;
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
@@ -1297,7 +1305,7 @@ __device__ __forceinline__ void column_eval(const StepCtx& X, int y, double& bv_
 // S.fs = SA[alpha][a], S.fp = PA[alpha][a], f_slot[beta] = CX[alpha][beta] * QR0[beta][a],
 // f_node[b] = QL1[alpha][b]
 template <int FAMILY, bool CACHED>
-__device__ __forceinline__ void row_eval(const StepCtx& X, int x, double& bv_out, long long& bf_out) {
+__device__ TTC_STEP_INLINE void row_eval(const StepCtx& X, int x, double& bv_out, long long& bf_out) {
   const DevCtx& c = *X.c;
   GreedySmem& S = *X.S;
   const int n = X.n, cap = X.cap, r = X.r, tid = X.tid, T = X.T;
