@@ -229,13 +229,18 @@ def roofline(kt, stats, family, peaks, peak_src, modes=0, workload=None, cached=
         # memory side: in the samples and rook steps every u_t(x) v_t(y) term
         # streams one factor from HBM (the other is staged) and every entry writes its E and raw
         # value (16 B); the u/v extension works on chip and writes one 8-byte u/v value per entry
+        # value (16 B) and reads its row's (column's) own-side factor tables: SA (16 B) for the
+        # C family, SA + PA (16 + 24 B) for D -- per row and step, too many to stay on chip in
+        # the streaming shapes
         ext_e = stats["ext_entries"] / max(1, launches)
         ext_u = stats["ext_updates"] / max(1, launches)
-        algo = 8 * (upd - ext_u) + 16 * (ent - ext_e) + 8 * ext_e
+        tab = 40 if family == 1 else (16 if family == 0 else 0)
+        algo = 8 * (upd - ext_u) + (16 + tab) * (ent - ext_e) + 8 * ext_e
         gbs = algo / avg_s / 1e9
         hbm = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                "frac": gbs / peaks["hbm_gbs"], "bytes_per_launch": algo,
-               "per_unit": "8 B/streamed update term + 16 B/search entry + 8 B/extension entry",
+               "per_unit": f"8 B/streamed update term + {16 + tab} B/search entry (E and raw written, "
+                           f"{tab} B of own-side tables read) + 8 B/extension entry",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
         main, other = (hbm, alu) if hbm["frac"] >= alu["frac"] else (alu, hbm)
         out.update(main)
