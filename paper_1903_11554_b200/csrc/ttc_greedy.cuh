@@ -536,6 +536,9 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
 //   (3) the final values (columns: acc_s / u_s(x_s)) straight to U / V.
 // coef[t][s] is kept as coefL[t][l][i] (s = L*i + l), so a lane's slots are contiguous.
 #define EXR_NS 16
+#ifndef TTC_EXT_ALL
+#define TTC_EXT_ALL 1   // phase 2, streaming shapes: every CTA extends a share of the rows, then of the columns
+#endif
 #ifndef TTC_EXT_INLINE
 #define TTC_EXT_INLINE __noinline__   // (A/B: __forceinline__ puts phase 2 in the kernel's register allocation)
 #endif
@@ -1623,14 +1626,18 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
     // with G >= 2 the first half of the cluster extends the rows, the second half the columns
     // (independent: the column recurrence reads u only at old pivot rows, or A(t0) at the
     // first sweep), so the two latency chains overlap
-    const int gr = G >= 2 ? G / 2 : 1, gc = G >= 2 ? G - gr : 1;
-    const bool do_rows = G == 1 || cr < gr, do_cols = G == 1 || cr >= gr;
-    const int rr_i = G == 1 ? 0 : cr, cc_i = G == 1 ? 0 : cr - gr;
+    // streaming shapes: every CTA extends a share of the rows, then of the columns (D_20:
+    // 14.80 -> 14.65 ms -- the slower column half no longer sets the pace alone); the cached
+    // shapes of the small problems keep the halves (D_5: 0.76 vs 0.82 ms)
+    constexpr bool ext_all = TTC_EXT_ALL && !CACHED && FAMILY == 1;   // (family C: its tile variant on few rows per CTA -- C_10 1.63 -> 1.73 ms -- keeps the halves)
+    const int gr = ext_all ? G : (G >= 2 ? G / 2 : 1), gc = ext_all ? G : (G >= 2 ? G - gr : 1);
+    const bool do_rows = ext_all || G == 1 || cr < gr, do_cols = ext_all || G == 1 || cr >= gr;
+    const int rr_i = ext_all ? cr : (G == 1 ? 0 : cr), cc_i = ext_all ? cr : (G == 1 ? 0 : cr - gr);
     const int rchunk = (nr_new + gr - 1) / gr, cchunk = (nc_new + gc - 1) / gc;
     // the register variant when a CTA's rows fill its threads at the lanes per row the rank
     // needs (D_20 from rank 17); else the tile variant spreads the few rows' entries over all
     // threads (D_5: ~33 rows per CTA -- the register variant measured 0.93 vs 0.77 ms there)
-    const bool ext_reg = EXT_REG && FAMILY == 1 && min(rchunk, cchunk) * ext_reg_lanes(r) >= T;
+    const bool ext_reg = EXT_REG && FAMILY == 1 && min(rchunk, cchunk) * ext_reg_lanes(r) >= (ext_all ? T / 2 : T);
     if (do_rows) {   // rows: fixed index = pivot columns y_s
       if (tid < r) {
         p_al[tid] = S.ys[tid] / n;
