@@ -476,7 +476,7 @@ int reset_device(ttc_ctx* c) {
   CK(cudaMemsetAsync(c->dc.counters, 0, TTC_NCOUNTERS * sizeof(unsigned long long), c->ls));
   {
     Timed t(c, K_INIT_PIVOT);
-    k_init_pivot<<<1, N_INIT, 0, c->ls>>>(c->dc, c->t0buf);
+    k_init_pivot<<<1, N_INIT_WARPS * 32, 0, c->ls>>>(c->dc, c->t0buf);
   }
   if (int e = check_launch("k_init_pivot")) return e;
   {

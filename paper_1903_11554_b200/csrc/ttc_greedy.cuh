@@ -28,6 +28,8 @@ namespace cg = cooperative_groups;
 namespace ttc {
 
 #define N_INIT 64
+#define N_INIT_WARPS 32
+#define INIT_UQ 128   // coordinates per sample staged in shared memory by init_entry_warp
 #define TTC_MAX_SAMPLES 1024
 
 // ---------------------------------------------------------------------------------------
@@ -56,17 +58,80 @@ __device__ double init_entry(const DevCtx& c, int q) {
   return dde_div(p, SS);
 }
 
-// one block of N_INIT threads: t0 = first argmax |A| over the seeded samples -> t0buf[d],
-// A(t0) -> p0val.  Part of loading a grid (tt_cross_init / tt_cross_load_grid): the start
-// depends only on the grid and the seed, so every solve of the same problem reuses it.
-__global__ void __launch_bounds__(N_INIT) k_init_pivot(DevCtx c, int* t0buf) {
+// init_entry by one warp (t-form families): the lanes split the coordinates (exact integer
+// sums) and the d(d-1)/2 rho pairs (partial double-double products, rho on its branch-free
+// fast path), then a shuffle tree -- the product is rounded once, so the grouping gives the
+// entry of init_entry (R3); lane 0's value is returned on every lane.  (A thread per
+// sample ran its 190 IEEE-division pairs of D_20 one after another: ~110 us per solve.)
+__device__ double init_entry_warp(const DevCtx& c, int q) {
+  const int lane = threadIdx.x & 31;
+  const int d = c.d, n = c.n;
+  if (c.family >= 2) {
+    const double v = lane == 0 ? init_entry(c, q) : 0.0;
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+  ESum s = esum_zero();
+  for (int j = lane; j < d; j += 32) {
+    const int t = init_coord(c, q, j);
+    esum_add(s, c.chi[j * n + t], c.clo[j * n + t]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s.h += __shfl_xor_sync(0xffffffffu, s.h, o);
+    s.l += __shfl_xor_sync(0xffffffffu, s.l, o);
+  }
+  const double S = esum_round(s);
+  const double SS = __dmul_rn(S, S);
+  if (c.family == 0) return __drcp_rn(SS);
+  DDE p = dde_one();
+  // the sample's node values, gathered once per warp (one round of loads instead of a
+  // dependent pair of loads per rho pair)
+  __shared__ double s_uq[N_INIT_WARPS][INIT_UQ];
+  double* uq = s_uq[threadIdx.x >> 5];
+  const bool staged = d <= INIT_UQ;
+  if (staged)
+    for (int j = lane; j < d; j += 32) uq[j] = c.u[j * n + init_coord(c, q, j)];
+  __syncwarp();
+  for (int e = lane; e < d * d; e += 32) {
+    const int i = e / d, j = e - i * d;
+    if (j <= i) continue;
+    const double ui = staged ? uq[i] : c.u[i * n + init_coord(c, q, i)];
+    const double uj = staged ? uq[j] : c.u[j * n + init_coord(c, q, j)];
+    bool ok;
+    double rr = rho_fast(ui, uj, ok);
+    if (!ok) rr = rho_ool(ui, uj);
+    dde_mul_d(p, rr);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    DDE y;
+    y.hi = __shfl_xor_sync(0xffffffffu, p.hi, o);
+    y.lo = __shfl_xor_sync(0xffffffffu, p.lo, o);
+    y.e = __shfl_xor_sync(0xffffffffu, p.e, o);
+    y.pad = 0;
+    dde_mul(p, y);
+  }
+  const double v = lane == 0 ? dde_div(p, SS) : 0.0;
+  __syncwarp();   // (uq is rewritten by this warp's next sample)
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// one block of N_INIT_WARPS warps: t0 = first argmax |A| over the N_INIT seeded samples (a warp
+// per sample) -> t0buf[d], A(t0) -> p0val.  Part of loading a grid (tt_cross_init /
+// tt_cross_load_grid) and of every tt_cross_reset.
+__global__ void __launch_bounds__(N_INIT_WARPS * 32) k_init_pivot(DevCtx c, int* t0buf) {
   __shared__ double sv[N_INIT], sgn[N_INIT];
   __shared__ int best;
-  const int q = threadIdx.x;
-  sgn[q] = init_entry(c, q);
-  sv[q] = fabs(sgn[q]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < N_INIT; q += N_INIT_WARPS) {
+    const double v = init_entry_warp(c, q);
+    if (lane == 0) {
+      sgn[q] = v;
+      sv[q] = fabs(v);
+    }
+  }
   __syncthreads();
-  if (q == 0) {
+  if (threadIdx.x == 0) {
     int b = 0;
     for (int t = 1; t < N_INIT; ++t)
       if (sv[t] > sv[b]) b = t;
@@ -74,7 +139,7 @@ __global__ void __launch_bounds__(N_INIT) k_init_pivot(DevCtx c, int* t0buf) {
     *c.p0val = sgn[b];  // A(t0): u_0(x_0) of every superblock at the first sweep
   }
   __syncthreads();
-  for (int j = q; j < c.d; j += blockDim.x) t0buf[j] = init_coord(c, best, j);
+  for (int j = threadIdx.x; j < c.d; j += blockDim.x) t0buf[j] = init_coord(c, best, j);
 }
 
 // rank-1 records (t0, parents (0, 0)) for every interface + fresh superblock state
