@@ -353,9 +353,12 @@ int do_integrate_local(ttc_ctx* c) {
     if (int e = side_join(c, 0)) return e;
     {
       Timed t(c, K_SOLVE);
-      // split the right-hand sides over 4 CTAs when the interfaces leave SMs idle
-      const int split = (cap >= 32 && 4 * c->n_owned <= c->sms) ? 4 : 1;
-      k_solve<<<dim3(c->n_owned, split), 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc);
+      // split the right-hand sides over CTAs while the interfaces leave SMs idle (each CTA
+      // repeats the LU of M_k): up to 8 x 512 threads at cap 64 (D_20 0.20 -> 0.16 ms), 4 x 256
+      // at cap 32 (more CTAs or threads measured slower on the smaller matrices)
+      const int split = cap >= 64 ? std::max(1, std::min(8, c->sms / std::max(1, c->n_owned)))
+                                  : ((cap >= 32 && 4 * c->n_owned <= c->sms) ? 4 : 1);
+      k_solve<<<dim3(c->n_owned, split), cap >= 64 ? 512 : 256, 2 * cap * cap * sizeof(DD), c->ls>>>(dc);
     }
     if (int e = check_launch("k_solve")) return e;
   }

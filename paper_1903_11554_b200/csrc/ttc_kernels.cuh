@@ -457,13 +457,13 @@ __device__ __forceinline__ DD dd_recip(DD y) {
   return dd_add(dd_make(q1), dd_mul_d(e, q1));
 }
 
-__global__ void __launch_bounds__(256) k_solve(DevCtx c) {
+__global__ void __launch_bounds__(512) k_solve(DevCtx c) {
   const int i = blockIdx.x + c.kb;
   const int cap = c.cap, d = c.d;
   extern __shared__ DD smd[];
   DD* A = smd;                 // [cap][cap]
   DD* Bm = smd + cap * cap;    // [cap][cap]
-  __shared__ DD dinv[TTC_MAX_RANK_DEV];
+  __shared__ DD dinv[TTC_MAX_RANK_DEV], lmul[TTC_MAX_RANK_DEV];
   __shared__ int perm[TTC_MAX_RANK_DEV];
   const int r = rec_rank(c.rec_cur, c.RS, i);
   const int nc_all = (i + 1 < d - 1) ? rec_rank(c.rec_cur, c.RS, i + 1) : 1;
@@ -511,10 +511,13 @@ __global__ void __launch_bounds__(256) k_solve(DevCtx c) {
     const DD inv = dd_recip(A[pk * cap + k]);
     if (threadIdx.x == 0) dinv[k] = inv;
     const int nr = r - k - 1, width = nr + nc;
+    // the step's multipliers once per row (not once per updated element)
+    for (int q = threadIdx.x; q < nr; q += blockDim.x) lmul[q] = dd_mul(A[perm[k + 1 + q] * cap + k], inv);
+    __syncthreads();
     for (int t = threadIdx.x; t < nr * width; t += blockDim.x) {
       const int q = t / width, colx = t - q * width;
       const int row = perm[k + 1 + q];
-      const DD l = dd_mul(A[row * cap + k], inv);
+      const DD l = lmul[q];
       if (colx < nr) {
         const int col = k + 1 + colx;
         A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l, A[pk * cap + col]));
