@@ -601,6 +601,10 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
 //   (3) the final values (columns: acc_s / u_s(x_s)) straight to U / V.
 // coef[t][s] is kept as coefL[t][l][i] (s = L*i + l), so a lane's slots are contiguous.
 #define EXR_NS 16
+#ifndef TTC_EXT_PREFETCH
+#define TTC_EXT_PREFETCH 0   // phase 2 raw entries: the next group's Q gathers prefetched into L1 (D_20 14.52 -> 14.70 ms: off)
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 #ifndef TTC_EXT_ALL
 #define TTC_EXT_ALL 1   // phase 2, streaming shapes: every CTA extends a share of the rows, then of the columns
 #endif
@@ -832,10 +836,18 @@ __device__ TTC_EXT_INLINE void extend_side_reg(const DevCtx& c, int sweep, int j
       if (FAMILY == 1) po = Pown[x];
       else po = dde_one();
       const double uo = uown[z];
+      if (TTC_EXT_PREFETCH && FAMILY == 1)   // the first group's Q factors into L1
+#pragma unroll
+        for (int u = 0; u < 4; ++u) prefetch_l1(&Qg[fix[min(L * u + l, r - 1)].q + z]);
 #pragma unroll 1
       for (int g = 0; g < EXR_NS / 4 && 4 * L * g < r; ++g) {   // (warp-uniform)
         double v[4];
         unsigned slow = 0;
+        // the next group's Q gathers go out now (L1 prefetch: no registers), so its loads hit L1
+        // instead of waiting a loaded-L2 round trip after this group's arithmetic
+        if (TTC_EXT_PREFETCH && FAMILY == 1 && 4 * L * (g + 1) < r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) prefetch_l1(&Qg[fix[min(L * (4 * (g + 1) + u) + l, r - 1)].q + z]);
         ext_raw4<FAMILY>(v, 4 * g, L, l, r, fix, so, po, uo, Qg, z, slow);
         if (slow) {   // (rare: a division off its fast path -- the entry the plain way, out of line)
 #pragma unroll 1
@@ -903,8 +915,6 @@ __host__ __device__ __forceinline__ long long extend_smem_doubles(int cap) {
 #ifndef TTC_PREFETCH
 #define TTC_PREFETCH 0   // rook steps: prefetch the next row block's tables into L1 (A/B)
 #endif
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-
 struct Cand {
   double val;
   long long idx;
