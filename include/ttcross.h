@@ -255,7 +255,9 @@ int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, 
  * steps, us_out[12..13] = [raw entries, recurrence] of the extension's row tiles (written when
  * count >= 14); with count >= 14 + 16*256 also a per-sweep log: us_out[14 + 16*s + p] = slot p
  * (0..13 as above) for sweep s < 256 alone, except slot 7 = the sweep's rook rounds.  count >= 12.
- * Reset by tt_cross_set_timing(1). */
+ * Reset by tt_cross_set_timing(1).  Diagnostics: only a library compiled with
+ * -DTTC_PHASE_CLOCKS=1 keeps the clocks (tools/probe_phases.py builds one); the default build
+ * returns TTC_ERR_STATE. */
 int tt_cross_get_phase_times(ttc_ctx* ctx, double* us_out, int32_t count);
 
 /* tt_cross_set_timing -- 1: bracket every kernel launch with CUDA events on the context

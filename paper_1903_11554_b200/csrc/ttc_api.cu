@@ -1262,6 +1262,9 @@ int tt_cross_set_timing(ttc_ctx* c, int32_t enable) {
 int tt_cross_get_phase_times(ttc_ctx* c, double* us_out, int32_t count) {
   if (!c || !us_out) return fail(TTC_ERR_ARG, "null argument");
   if (count < 12) return fail(TTC_ERR_ARG, "need 12 slots");
+  if (!TTC_PHASE_CLOCKS)
+    return fail(TTC_ERR_STATE, "library built without the phase clocks (TTC_PHASE_CLOCKS=0): "
+                               "tools/probe_phases.py uses build/libttcross_clocks.so");
   std::vector<unsigned long long> v(TTC_PHASE_WORDS);
   CK(cudaMemcpyAsync(v.data(), c->phase_buf, sizeof(unsigned long long) * TTC_PHASE_WORDS, cudaMemcpyDeviceToHost,
                      c->stream));

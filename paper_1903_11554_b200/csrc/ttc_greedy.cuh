@@ -28,6 +28,13 @@ namespace cg = cooperative_groups;
 namespace ttc {
 
 #define N_INIT 64
+#ifndef TTC_PHASE_CLOCKS
+// per-phase device clocks of one superblock (tt_cross_get_phase_times): a diagnostics build
+// only (tools/probe_phases.py builds build/libttcross_clocks.so) -- the clock code's live
+// registers cost the sweep kernel spills even when the clocks are off (D_20 14.52 vs 14.21 ms,
+// C_200 4.81 vs 4.61, profiles/r02t_phase_clocks.log)
+#define TTC_PHASE_CLOCKS 0
+#endif
 #define N_INIT_WARPS 32
 #define INIT_UQ 128   // coordinates per sample staged in shared memory by init_entry_warp
 #define TTC_MAX_SAMPLES 1024
@@ -456,7 +463,7 @@ __device__ __noinline__ void extend_side(const DevCtx& c, int sweep, int job, in
   // rows per tile, tile stride and lanes per row of the recurrence (host: extend_tile_shape)
   const int tile_rows = c.ext_tile;
   double* dst = side == 0 ? U : V;
-  const bool timer = c.phase_ns && job == c.phase_job && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0;
+  const bool timer = TTC_PHASE_CLOCKS && c.phase_ns && job == c.phase_job && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0;
   unsigned long long tm = timer ? gtimer() : 0;
   auto clock_to = [&](int ph) {
     if (timer) {
@@ -762,7 +769,7 @@ __device__ TTC_EXT_INLINE void extend_side_reg(const DevCtx& c, int sweep, int j
     }
   }
   double* dst = side == 0 ? U : V;
-  const bool timer = c.phase_ns && job == c.phase_job && tid == 0 && cg::this_cluster().block_rank() == 0;
+  const bool timer = TTC_PHASE_CLOCKS && c.phase_ns && job == c.phase_job && tid == 0 && cg::this_cluster().block_rank() == 0;
   unsigned long long tm = timer ? gtimer() : 0;
   auto clock_to = [&](int ph) {
     if (timer) {
@@ -1620,7 +1627,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
   ESum* SBc = reinterpret_cast<ESum*>(Erow + rpcap);  // [rpcap]
   DDE* PBc = reinterpret_cast<DDE*>(SBc + rpcap);     // [rpcap]
 
-  const bool timer = c.phase_ns && job == c.phase_job && cr == 0 && tid == 0;
+  const bool timer = TTC_PHASE_CLOCKS && c.phase_ns && job == c.phase_job && cr == 0 && tid == 0;
   unsigned long long t_last = timer ? gtimer() : 0;
   auto phase = [&](int ph) {
     if (timer) {
@@ -1688,7 +1695,7 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
   // ---- phase 2: u / v of the existing pivots on the new rows and columns
   // (per-sweep log slots 14 / 15: this phase's own time in the first row CTA / the first column
   // CTA of the logged superblock, before the cluster barrier)
-  const bool ext_clock = c.phase_ns && job == c.phase_job && tid == 0 && (cr == 0 || cr == (G >= 2 ? G / 2 : 0));
+  const bool ext_clock = TTC_PHASE_CLOCKS && c.phase_ns && job == c.phase_job && tid == 0 && (cr == 0 || cr == (G >= 2 ? G / 2 : 0));
   const unsigned long long t_ext0 = ext_clock ? gtimer() : 0;
   {
     __shared__ int p_al[TTC_MAX_RANK_DEV], p_a[TTC_MAX_RANK_DEV];
@@ -2142,7 +2149,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
     if (threadIdx.x == 0) {
       int abort = 0;
       const long long t0 = clock64();
-      const unsigned long long w0 = c.phase_ns ? gtimer() : 0;
+      const unsigned long long w0 = (TTC_PHASE_CLOCKS && c.phase_ns) ? gtimer() : 0;
       if (k > 0)
         while (ld_acquire(&c.done[k - 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
         }
@@ -2151,7 +2158,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         }
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort[s & 1] = abort;
-      if (c.phase_ns && job == c.phase_job && cl.block_rank() == 0) {
+      if (TTC_PHASE_CLOCKS && c.phase_ns && job == c.phase_job && cl.block_rank() == 0) {
         ph_add(c.phase_ns, s, PH_START, gtimer() - w0);
       }
     }

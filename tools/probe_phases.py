@@ -9,6 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+if not os.environ.get("TTC_LIB_PATH"):   # the phase clocks live in a diagnostics build
+    import __graft_entry__  # noqa: E402
+    os.environ["TTC_LIB_PATH"] = __graft_entry__.build_diagnostics()
+
 import torch  # noqa: E402
 
 from paper_1903_11554_b200 import TTCross  # noqa: E402
