@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(ALL_WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the CUDA graph")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="N > 1: one launch + NCCL all-gather per sweep instead of the cross-GPU wavefront")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
     return ap.parse_args()
@@ -461,7 +463,7 @@ def main():
             return tt.integrate_read()
         core = tt
     else:
-        dtt = DistTTCross(wl.family, u_d, w_d, wl.rank_cap, wl.tol, **kw)
+        dtt = DistTTCross(wl.family, u_d, w_d, wl.rank_cap, wl.tol, peer=not args.no_peer, **kw)
 
         last = {}
 
@@ -580,6 +582,9 @@ def main():
             "evals_per_step": evals_total, "sweep_ms": ms_max / args.steps,
             "integral": {"value": val[0], "log10_abs": val[1], "sign": val[2]},
             "graph": use_graph, "gpu_launches": int(launches_step) * args.steps,
+            "exchange": ("none (one GPU)" if world == 1 else
+                         "cross-GPU wavefront: boundary records through CUDA IPC peer memory, one NCCL all-gather per solve"
+                         if dtt.peer else "NCCL all-gather of the new records after every sweep"),
             "launch_shape": core.launch_shape(),
             "roofline": roof, "fiber_roofline": froof, "kernel_ms_per_solve": kernel_ms, "clocks": clocks, "e2e": e2e,
             "cpu_baseline": cpu,

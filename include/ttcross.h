@@ -160,6 +160,51 @@ int tt_cross_exchange_buffer(ttc_ctx* ctx, void** dev_ptr, int64_t* bytes_total,
                              int64_t* bytes_per_rank);
 
 /*
+ * Cross-GPU wavefront (world > 1; Alg. 6 lines 6-8, lines 604-608: after a sweep a
+ * process sends its new pivots to its neighbouring processes only).  Instead of one launch and
+ * one all-gather per sweep (tt_cross_sweep_local / exchange / commit), every rank runs its
+ * superblocks' sweeps as ONE persistent launch, as tt_cross_sweep does on one GPU: a rank's
+ * first and last superblock publish their new pivot record, rank and done flag also into the
+ * neighbour rank's copies through CUDA IPC peer memory (NVLink), the flag with a system-scope
+ * release, and wait on the neighbour rank's flag with a system-scope acquire.  The pivots are
+ * those of tt_cross_sweep on one GPU, bit for bit.
+ *
+ * tt_cross_peer_handles -- writes TTC_PEER_HANDLE_BYTES bytes to `out` (host): the CUDA IPC
+ *   handles of this context's record buffer, rank ring and done flags, for the neighbour ranks
+ *   (exchange them with any host collective).  world > 1, else TTC_ERR_STATE.
+ * tt_cross_peer_open -- maps the left (rank-1) and right (rank+1) neighbours' handles (as written
+ *   by their tt_cross_peer_handles; host pointers, read during the call).  `left` must be NULL
+ *   exactly when rank == 0, `right` exactly when rank == world-1 (TTC_ERR_ARG).  Needs every
+ *   owned superblock's cluster resident at once (tt_cross_get_launch_shape bit 2), else
+ *   TTC_ERR_STATE.  Synchronises the context stream.  Mappings are closed by tt_cross_destroy.
+ * tt_cross_sweep_peer -- n_sweeps >= 1 sweeps of the owned superblocks (one persistent launch),
+ *   then this rank's records to its slot of the exchange buffer; the caller all-gathers the
+ *   exchange buffer (tt_cross_exchange_buffer) and calls tt_cross_commit, which advances the
+ *   sweep count by n_sweeps.  All ranks must call it with the same n_sweeps, and no rank may
+ *   launch it before every rank's previous reset / commit has completed on its device (the
+ *   neighbours write into this rank's buffers): put a device-side barrier (e.g. a one-element
+ *   NCCL all-reduce) after tt_cross_reset and after tt_cross_commit.  TTC_ERR_STATE after a
+ *   tt_cross_sweep_local since the last reset (its neighbour flags are not published).  A
+ *   neighbour wait longer than ~2 s abandons the launch (reported as by tt_cross_sweep).
+ *   Asynchronous on the context stream.
+ *
+ * Loopback test of the same code path on one GPU (world == 1, persistent launch):
+ * tt_cross_set_loopback -- boundary b in [1, d-2] splits the interfaces as if [0, b) and
+ *   [b, d-1) were on two ranks: superblocks b-1 and b exchange flag and rank through a mirror
+ *   buffer (system-scope release / acquire) and publish their records into the mirror's record
+ *   copy; b = 0 turns it off.  Resets the context to the rank-1 start (tt_cross_reset).
+ * tt_cross_get_loopback -- the mirror after the last sweep (synchronising): the record copy
+ *   (the layout of tt_cross_exchange_buffer's world == 1 records, d-1 records), the rank ring
+ *   [d-1][2] (rank of interface k after sweep s at [k][s & 1]) and the done flags [d-1].
+ */
+#define TTC_PEER_HANDLE_BYTES 192
+int tt_cross_peer_handles(ttc_ctx* ctx, void* out, int64_t capacity);
+int tt_cross_peer_open(ttc_ctx* ctx, const void* left, const void* right);
+int tt_cross_sweep_peer(ttc_ctx* ctx, int32_t n_sweeps);
+int tt_cross_set_loopback(ttc_ctx* ctx, int32_t boundary);
+int tt_cross_get_loopback(ttc_ctx* ctx, int32_t* rec_out, int32_t* ring_out, int32_t* done_out);
+
+/*
  * tt_solve_launch -- enqueue one whole solve on the context stream, asynchronously: reset to
  * the rank-1 start, n_sweeps sweeps (as tt_cross_sweep) and the quadrature (as
  * tt_integrate_launch).  use_graph != 0 captures this sequence once as a CUDA graph
@@ -241,7 +286,8 @@ int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64
 
 /* tt_cross_get_launch_shape -- the k_sweep launch chosen at init: CTAs per superblock cluster,
  * threads per CTA, flags in *cached (bit 0: the rook search keeps its rows/columns in shared
- * memory; bit 1: tt_cross_sweep runs the persistent wavefront launch), and the dynamic shared
+ * memory; bit 1: tt_cross_sweep runs the persistent wavefront launch; bit 2: every owned
+ * superblock's cluster is resident at once -- tt_cross_peer_open's condition), and the dynamic shared
  * memory per CTA (bytes).  Any pointer may be NULL. */
 int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, int32_t* cached,
                               int64_t* smem_bytes);

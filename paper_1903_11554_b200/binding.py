@@ -22,6 +22,7 @@ TTC_FAMILY_DX = 3
 TTC_FAMILY_EX = 4
 TTC_MEM_HOST = 0
 TTC_MEM_DEVICE = 1
+TTC_PEER_HANDLE_BYTES = 192   # include/ttcross.h
 
 # every symbol declared in include/ttcross.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -31,6 +32,8 @@ EXPORTS = [
     "tt_cross_get_state", "tt_cross_get_fiber", "tt_cross_get_stats", "tt_cross_get_kernel_time",
     "tt_cross_set_timing", "tt_cross_destroy", "tt_last_error", "tt_build_info", "tt_cross_get_launch_shape",
     "tt_cross_get_phase_times", "tt_selftest_division", "tt_cross_get_wsum",
+    "tt_cross_peer_handles", "tt_cross_peer_open", "tt_cross_sweep_peer", "tt_cross_set_loopback",
+    "tt_cross_get_loopback",
 ]
 N_KERNELS = 13
 
@@ -96,6 +99,11 @@ def load(path: str = LIB_PATH):
         "tt_last_error": (ctypes.c_char_p, []),
         "tt_build_info": (ctypes.c_char_p, []),
         "tt_selftest_division": (i32, [P, P, P, P, i64]),
+        "tt_cross_peer_handles": (i32, [P, P, i64]),
+        "tt_cross_peer_open": (i32, [P, P, P]),
+        "tt_cross_sweep_peer": (i32, [P, i32]),
+        "tt_cross_set_loopback": (i32, [P, i32]),
+        "tt_cross_get_loopback": (i32, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -228,6 +236,38 @@ class TTCross:
         self._synced()
         return v.value, l10.value, sg.value
 
+    # -- cross-GPU wavefront (include/ttcross.h: tt_cross_peer_handles ... tt_cross_get_loopback)
+    def peer_handles(self):
+        """This context's CUDA IPC handles (bytes, TTC_PEER_HANDLE_BYTES) for its neighbour ranks."""
+        buf = ctypes.create_string_buffer(TTC_PEER_HANDLE_BYTES)
+        _check(self.lib, self.lib.tt_cross_peer_handles(self._h, buf, TTC_PEER_HANDLE_BYTES), "tt_cross_peer_handles")
+        return buf.raw
+
+    def peer_open(self, left, right):
+        """Map the neighbour ranks' handles (bytes or None)."""
+        lb = ctypes.create_string_buffer(bytes(left), TTC_PEER_HANDLE_BYTES) if left is not None else None
+        rb = ctypes.create_string_buffer(bytes(right), TTC_PEER_HANDLE_BYTES) if right is not None else None
+        _check(self.lib, self.lib.tt_cross_peer_open(self._h, lb, rb), "tt_cross_peer_open")
+        self._synced()
+
+    def sweep_peer(self, n_sweeps):
+        _check(self.lib, self.lib.tt_cross_sweep_peer(self._h, int(n_sweeps)), "tt_cross_sweep_peer")
+
+    def set_loopback(self, boundary):
+        _check(self.lib, self.lib.tt_cross_set_loopback(self._h, int(boundary)), "tt_cross_set_loopback")
+
+    def loopback(self):
+        """(records [d-1][RS] int32, rank ring [d-1][2], done [d-1]) of the loopback mirror."""
+        rs = 1 + self.cap * self.d + 2 * self.cap
+        rec = np.zeros((self.d - 1, rs), dtype=np.int32)
+        ring = np.zeros((self.d - 1, 2), dtype=np.int32)
+        done = np.zeros(self.d - 1, dtype=np.int32)
+        _check(self.lib, self.lib.tt_cross_get_loopback(self._h, rec.ctypes.data_as(ctypes.c_void_p),
+                                                        ring.ctypes.data_as(ctypes.c_void_p),
+                                                        done.ctypes.data_as(ctypes.c_void_p)), "tt_cross_get_loopback")
+        self._synced()
+        return rec, ring, done
+
     # -- buffers for the multi-process exchange (zero-copy device views)
     def exchange_view(self):
         p, tot, per = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
@@ -311,6 +351,7 @@ class TTCross:
         _check(self.lib, self.lib.tt_cross_get_launch_shape(self._h, ctypes.byref(g), ctypes.byref(t), ctypes.byref(ca),
                                                             ctypes.byref(sm)), "tt_cross_get_launch_shape")
         return {"cluster": g.value, "threads": t.value, "cached": bool(ca.value & 1), "persistent": bool(ca.value & 2),
+                "all_resident": bool(ca.value & 4),
                 "smem_bytes": sm.value}
 
     def kernel_times(self):

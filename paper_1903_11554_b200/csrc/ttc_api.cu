@@ -86,6 +86,13 @@ struct ttc_ctx {
   const void* greedy_fn = nullptr;   // k_sweep variant (one sweep)
   const void* sweeps_fn = nullptr;   // k_sweeps variant (persistent, world == 1)
   bool persistent = false;           // k_sweeps usable (all clusters resident)
+  bool resident_all = false;         // every owned superblock's cluster resident at once (any world)
+  // cross-GPU wavefront (tt_cross_peer_open / tt_cross_sweep_peer)
+  void* peer_maps[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};   // opened IPC mappings
+  bool peer_consistent = true;       // rank_ring / done of every interface current (no tt_cross_sweep_local since reset)
+  int* lb_rec = nullptr;             // loopback mirror (tt_cross_set_loopback)
+  int* lb_ring = nullptr;
+  int* lb_done = nullptr;
   // buffers
   std::vector<void*> allocs;
   long long rec_ints = 0;
@@ -271,6 +278,7 @@ int do_sweep_local(ttc_ctx* c) {
     if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweep launch: ") + cudaGetErrorString(e));
     if (int e2 = check_launch("k_sweep")) return e2;
   }
+  c->peer_consistent = false;   // (the neighbour ranks' flags and ranks are not published here)
   if (c->cfg.world > 1 && c->n_owned > 0)   // own records -> own slot of the exchange buffer
     CK(cudaMemcpyAsync(c->xbuf + (long long)c->cfg.rank * c->chunk * c->dc.RS, c->dc.rec_next + (long long)c->kb * c->dc.RS,
                        sizeof(int32_t) * c->n_owned * c->dc.RS, cudaMemcpyDeviceToDevice, c->ls));
@@ -278,9 +286,9 @@ int do_sweep_local(ttc_ctx* c) {
   return TTC_OK;
 }
 
-// n sweeps [c->sweeps, c->sweeps + n) in one persistent launch (world == 1)
-int do_sweeps_persistent(ttc_ctx* c, int n) {
-  if (n <= 0) return TTC_OK;
+// n sweeps [c->sweeps, c->sweeps + n) of the owned superblocks in one persistent launch
+// (k_sweeps); c->sweeps is advanced by the caller
+int launch_sweeps(ttc_ctx* c, int n) {
   DevCtx& dc = c->dc;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(c->n_owned * dc.G);
@@ -300,8 +308,28 @@ int do_sweeps_persistent(ttc_ctx* c, int n) {
     e = cudaLaunchKernelEx(&lc, (void (*)(DevCtx, int, int))c->sweeps_fn, dc, c->sweeps, n);
   }
   if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweeps launch: ") + cudaGetErrorString(e));
-  if (int e2 = check_launch("k_sweeps")) return e2;
+  return check_launch("k_sweeps");
+}
+
+// n sweeps in one persistent launch (world == 1)
+int do_sweeps_persistent(ttc_ctx* c, int n) {
+  if (n <= 0) return TTC_OK;
+  if (int e = launch_sweeps(c, n)) return e;
   c->sweeps += n;
+  return TTC_OK;
+}
+
+// n sweeps of this rank's superblocks in one persistent launch, the boundary superblocks
+// exchanging their records with the neighbour ranks' kernels through peer memory (world > 1),
+// then this rank's records -> its slot of the exchange buffer; tt_cross_commit after the
+// caller's all-gather completes the n sweeps
+int do_sweeps_peer(ttc_ctx* c, int n) {
+  if (n > 0 && c->n_owned > 0)
+    if (int e = launch_sweeps(c, n)) return e;
+  if (c->n_owned > 0)
+    CK(cudaMemcpyAsync(c->xbuf + (long long)c->cfg.rank * c->chunk * c->dc.RS, c->dc.rec_cur + (long long)c->kb * c->dc.RS,
+                       sizeof(int32_t) * c->n_owned * c->dc.RS, cudaMemcpyDeviceToDevice, c->ls));
+  c->pending = n;
   return TTC_OK;
 }
 
@@ -315,8 +343,8 @@ int do_commit(ttc_ctx* c) {
                                                       c->dc.RS);
     if (int e = check_launch("k_unpack_records")) return e;
   }
+  c->sweeps += c->pending;   // (1 after tt_cross_sweep_local, n after tt_cross_sweep_peer)
   c->pending = 0;
-  c->sweeps++;
   return TTC_OK;
 }
 
@@ -493,6 +521,7 @@ int reset_device(ttc_ctx* c) {
 int reset_host(ttc_ctx* c) {
   c->sweeps = 0;
   c->pending = 0;
+  c->peer_consistent = true;
   c->launches = 0;
   if (int e = resolve_timing(c)) return e;
   for (double& m : c->ms) m = 0.0;
@@ -692,6 +721,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       (e = dalloc(c, &c->chainA, (size_t)(nj + 1) * cap * cap)) || (e = dalloc(c, &c->chainB, (size_t)(nj + 1) * cap * cap)) ||
       (e = dalloc(c, &c->chainAd, (size_t)(nj + 1) * 3)) || (e = dalloc(c, &c->chainBd, (size_t)(nj + 1) * 3)))
     return bail(e);
+  dc.rdone = dc.done;        // (a remote neighbour's flag and rank land in this rank's own copies)
+  dc.rring = dc.rank_ring;
   if (cudaMemset(dc.wcnt, 0, sizeof(int) * d * ((cap + FW_TA - 1) / FW_TA) * ((cap + FW_TB - 1) / FW_TB)) != cudaSuccess)
     return bail(fail(TTC_ERR_CUDA, "cudaMemset(wcnt) failed"));
   if (k.family == TTC_FAMILY_D) {
@@ -955,8 +986,9 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       // the wavefront needs every cluster resident at once
       // (queried for the persistent kernel itself: its register / shared-memory footprint
       // differs from the single-sweep kernel's)
-      c->persistent = k.world == 1 && resident_of(c->sweeps_fn, G, cached) >= nj && resident(G, cached) >= nj &&
-                      !std::getenv("TTC_NO_PERSISTENT");
+      c->resident_all = resident_of(c->sweeps_fn, G, cached) >= nj && resident(G, cached) >= nj &&
+                        !std::getenv("TTC_NO_PERSISTENT");
+      c->persistent = k.world == 1 && c->resident_all;
     }
   }
   if (dc.tma) {
@@ -1246,7 +1278,7 @@ int tt_cross_get_launch_shape(ttc_ctx* c, int32_t* cluster, int32_t* threads, in
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (cluster) *cluster = c->dc.G;
   if (threads) *threads = c->greedy_threads;
-  if (cached) *cached = (c->greedy_cached ? 1 : 0) | (c->persistent ? 2 : 0);
+  if (cached) *cached = (c->greedy_cached ? 1 : 0) | (c->persistent ? 2 : 0) | (c->resident_all ? 4 : 0);
   if (smem_bytes) *smem_bytes = (int64_t)c->greedy_smem;
   return TTC_OK;
 }
@@ -1292,9 +1324,115 @@ void tt_cross_destroy(ttc_ctx* c) {
     if (c->ev_fork[i]) cudaEventDestroy(c->ev_fork[i]);
     if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
   }
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (c->peer_maps[i][j]) cudaIpcCloseMemHandle(c->peer_maps[i][j]);
   for (void* p : c->allocs) cudaFree(p);
   if (c->out_host) cudaFreeHost(c->out_host);
   delete c;
+}
+
+// ---------------------------------------------------------------------------------------
+// cross-GPU wavefront (include/ttcross.h: tt_cross_peer_handles ... tt_cross_get_loopback)
+// ---------------------------------------------------------------------------------------
+static_assert(3 * sizeof(cudaIpcMemHandle_t) == TTC_PEER_HANDLE_BYTES, "TTC_PEER_HANDLE_BYTES");
+int tt_cross_peer_handles(ttc_ctx* c, void* out, int64_t capacity) {
+  if (!c || !out) return fail(TTC_ERR_ARG, "null argument");
+  if (capacity < TTC_PEER_HANDLE_BYTES) return fail(TTC_ERR_ARG, "capacity < TTC_PEER_HANDLE_BYTES");
+  if (c->cfg.world < 2) return fail(TTC_ERR_STATE, "tt_cross_peer_handles needs world > 1");
+  int* bases[3] = {c->dc.rec_cur, c->dc.rank_ring, c->dc.done};
+  for (int j = 0; j < 3; ++j) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, bases[j]));
+    std::memcpy(static_cast<unsigned char*>(out) + j * sizeof(cudaIpcMemHandle_t), &h, sizeof(h));
+  }
+  return TTC_OK;
+}
+
+int tt_cross_peer_open(ttc_ctx* c, const void* left, const void* right) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world < 2) return fail(TTC_ERR_STATE, "tt_cross_peer_open needs world > 1");
+  if (c->dc.loopback) return fail(TTC_ERR_STATE, "loopback mode is on");
+  if (!c->resident_all) return fail(TTC_ERR_STATE, "the owned superblocks' clusters are not all resident at once");
+  if ((left != nullptr) != (c->cfg.rank > 0) || (right != nullptr) != (c->cfg.rank < c->cfg.world - 1))
+    return fail(TTC_ERR_ARG, "a rank needs exactly its existing neighbours' handles (left: rank > 0, right: rank < world-1)");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  CK(cudaStreamSynchronize(c->stream));
+  const void* hs[2] = {left, right};
+  for (int i = 0; i < 2; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      if (c->peer_maps[i][j]) { cudaIpcCloseMemHandle(c->peer_maps[i][j]); c->peer_maps[i][j] = nullptr; }
+      if (!hs[i]) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const unsigned char*>(hs[i]) + j * sizeof(cudaIpcMemHandle_t), sizeof(h));
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_maps[i][j] = p;
+    }
+    c->dc.prec[i] = static_cast<int*>(c->peer_maps[i][0]);
+    c->dc.pring[i] = static_cast<int*>(c->peer_maps[i][1]);
+    c->dc.pdone[i] = static_cast<int*>(c->peer_maps[i][2]);
+  }
+  c->dc.rdone = c->dc.done;
+  c->dc.rring = c->dc.rank_ring;
+  c->dc.pb_lo = left ? c->kb : -1;    // this rank's first superblock: left neighbour on rank - 1
+  c->dc.pb_hi = right ? c->ke : -1;   // its last (k + 1 == ke): right neighbour on rank + 1
+  return TTC_OK;
+}
+
+int tt_cross_sweep_peer(ttc_ctx* c, int32_t n_sweeps) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world < 2) return fail(TTC_ERR_STATE, "tt_cross_sweep_peer needs world > 1 (world == 1: tt_cross_sweep)");
+  if (!c->dc.pdone[0] && !c->dc.pdone[1]) return fail(TTC_ERR_STATE, "tt_cross_peer_open first");
+  if (n_sweeps < 1) return fail(TTC_ERR_ARG, "n_sweeps < 1");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  if (!c->peer_consistent) return fail(TTC_ERR_STATE, "tt_cross_sweep_local ran since the last reset");
+  return do_sweeps_peer(c, n_sweeps);
+}
+
+int tt_cross_set_loopback(ttc_ctx* c, int32_t boundary) {
+  if (!c) return fail(TTC_ERR_ARG, "null context");
+  if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_cross_set_loopback needs world == 1");
+  const int d = c->dc.d;
+  if (boundary != 0 && (boundary < 1 || boundary > d - 2)) return fail(TTC_ERR_ARG, "boundary must be 0 or in [1, d-2]");
+  if (boundary != 0 && !c->persistent) return fail(TTC_ERR_STATE, "loopback needs the persistent sweep launch");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  if (boundary != 0 && !c->lb_rec) {
+    if (int e = dalloc(c, &c->lb_rec, (size_t)c->rec_ints)) return e;
+    if (int e = dalloc(c, &c->lb_ring, (size_t)2 * d)) return e;
+    if (int e = dalloc(c, &c->lb_done, (size_t)d)) return e;
+  }
+  DevCtx& dc = c->dc;
+  const bool on = boundary != 0;
+  for (int i = 0; i < 2; ++i) {
+    dc.prec[i] = on ? c->lb_rec : nullptr;
+    dc.pring[i] = on ? c->lb_ring : nullptr;
+    dc.pdone[i] = on ? c->lb_done : nullptr;
+  }
+  dc.rdone = on ? c->lb_done : dc.done;
+  dc.rring = on ? c->lb_ring : dc.rank_ring;
+  dc.pb_lo = on ? boundary : -1;   // superblock `boundary` sees its left neighbour as remote,
+  dc.pb_hi = on ? boundary : -1;   // superblock `boundary - 1` its right neighbour
+  dc.loopback = on ? 1 : 0;
+  if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }   // (captured kernel parameters)
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  c->graph_sweeps = -1;
+  return do_reset(c);
+}
+
+int tt_cross_get_loopback(ttc_ctx* c, int32_t* rec_out, int32_t* ring_out, int32_t* done_out) {
+  if (!c || !rec_out || !ring_out || !done_out) return fail(TTC_ERR_ARG, "null argument");
+  if (!c->dc.loopback) return fail(TTC_ERR_STATE, "loopback mode is off");
+  if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
+  const int d = c->dc.d;
+  CK(cudaMemcpyAsync(rec_out, c->lb_rec, sizeof(int32_t) * c->rec_ints, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(ring_out, c->lb_ring, sizeof(int32_t) * 2 * (d - 1), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(done_out, c->lb_done, sizeof(int32_t) * (d - 1), cudaMemcpyDeviceToHost, c->stream));
+  int32_t flags[2] = {0, 0};
+  CK(cudaMemcpyAsync(flags, c->dc.flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (flags[1]) return fail(TTC_ERR_CUDA, kWaveTimeout);
+  return TTC_OK;
 }
 
 }  // extern "C"

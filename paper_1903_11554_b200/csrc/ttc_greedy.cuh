@@ -167,7 +167,14 @@ __global__ void k_init_records(DevCtx c, const int* t0buf, int nrec, int n_owned
     c.rank_ring[2 * i] = 1;
     c.rank_ring[2 * i + 1] = 1;
     c.done[i] = 0;
+    if (c.loopback) {   // the loopback test's mirror of a neighbour rank's copies
+      c.rring[2 * i] = 1;
+      c.rring[2 * i + 1] = 1;
+      c.rdone[i] = 0;
+    }
   }
+  if (c.loopback && i < nrec)
+    for (int t = threadIdx.x; t < c.RS; t += blockDim.x) c.prec[0][(long long)i * c.RS + t] = c.rec_cur[(long long)i * c.RS + t];
   if (i < n_owned && threadIdx.x == 0) {
     c.sbstate[i * 4 + 0] = 0;
     c.sbstate[i * 4 + 1] = 0;
@@ -1587,6 +1594,34 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// system scope: a flag written by (or for) a kernel on another GPU through NVLink peer memory
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Cross-GPU wavefront (DevCtx prec/pring/pdone): superblock k's new record (slot r: tuple and
+// parents; the rank word), its rank after the sweep and its done flag, written into the copies
+// of the neighbour rank `side` -- plain stores over NVLink, then the flag with a system-scope
+// release, which orders them before it for the peer's system-scope acquire (Alg. 6
+// lines 6-8: the new pivots go to the neighbouring processes only).  Rn: this rank's record
+// of k, already complete (same thread).
+__device__ __noinline__ void peer_publish(const DevCtx& c, int side, int k, int sweep, int r, bool add, const int* Rn) {
+  int* R = c.prec[side] + (long long)k * c.RS;
+  if (add) {
+    const int d = c.d;
+    for (int q = 0; q < d; ++q) R[1 + (long long)r * d + q] = Rn[1 + (long long)r * d + q];
+    R[1 + (long long)c.cap * d + 2 * r] = Rn[1 + (long long)c.cap * d + 2 * r];
+    R[2 + (long long)c.cap * d + 2 * r] = Rn[2 + (long long)c.cap * d + 2 * r];
+    R[0] = r + 1;
+  }
+  c.pring[side][k * 2 + (sweep & 1)] = add ? r + 1 : r;
+  st_release_sys(&c.pdone[side][k], sweep + 1);
+}
 
 template <int FAMILY, bool CACHED>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, GreedySmem& S, double* dyn, int sweep, int job, int r,
@@ -1800,6 +1835,9 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
     if (release) {
       c.rank_ring[k * 2 + (sweep & 1)] = add ? r + 1 : r;
       st_release(&c.done[k], sweep + 1);  // the record writes above happen-before this release
+      // boundary superblocks of a rank: the same to the neighbour rank's copies
+      if (c.pdone[0] && k == c.pb_lo) peer_publish(cs, 0, k, sweep, r, add, Rn);   // (cs: the shared copy -- a
+      if (c.pdone[1] && k + 1 == c.pb_hi) peer_publish(cs, 1, k, sweep, r, add, Rn);   // reference to c would copy it to local memory)
     }
   };
   const bool stage_n = n <= STAGE_N;
@@ -2150,11 +2188,16 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
       int abort = 0;
       const long long t0 = clock64();
       const unsigned long long w0 = (TTC_PHASE_CLOCKS && c.phase_ns) ? gtimer() : 0;
+      // a neighbour on another rank (cross-GPU wavefront): its flag, written by the peer with a
+      // system-scope release, is acquired at system scope from rdone
+      const bool lrem = c.pdone[0] && k == c.pb_lo, rrem = c.pdone[1] && k + 1 == c.pb_hi;
       if (k > 0)
-        while (ld_acquire(&c.done[k - 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
+        while ((lrem ? ld_acquire_sys(&c.rdone[k - 1]) : ld_acquire(&c.done[k - 1])) < s &&
+               !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
         }
       if (!abort && k < d - 2)
-        while (ld_acquire(&c.done[k + 1]) < s && !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
+        while ((rrem ? ld_acquire_sys(&c.rdone[k + 1]) : ld_acquire(&c.done[k + 1])) < s &&
+               !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
         }
       if (abort) atomicOr(&c.flags[1], 1);
       s_abort[s & 1] = abort;
@@ -2175,8 +2218,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         break;
       }
     }
-    const int rl = k > 0 ? c.rank_ring[(k - 1) * 2 + ((s - 1) & 1)] : 1;
-    const int rr = k < d - 2 ? c.rank_ring[(k + 1) * 2 + ((s - 1) & 1)] : 1;
+    const bool lrem = c.pdone[0] && k == c.pb_lo, rrem = c.pdone[1] && k + 1 == c.pb_hi;
+    const int rl = k > 0 ? (lrem ? c.rring : c.rank_ring)[(k - 1) * 2 + ((s - 1) & 1)] : 1;
+    const int rr = k < d - 2 ? (rrem ? c.rring : c.rank_ring)[(k + 1) * 2 + ((s - 1) & 1)] : 1;
     // (sweep_body publishes rank_ring[k] and releases done[k] as soon as the pivot is known)
     r = sweep_body<FAMILY, CACHED>(c, s_ctx, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
                                    s > s0, true);

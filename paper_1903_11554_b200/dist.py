@@ -102,14 +102,30 @@ def allgather_slices(buf: torch.Tensor, per_rank: int, group=None):
     return buf
 
 
+def neighbour_handles(handles, rank: int, world: int):
+    """(left, right) entries of the all-gathered per-rank handle list for ``rank``: the
+    neighbour ranks' handles, None at the ends of the chain (tt_cross_peer_open's contract)."""
+    if len(handles) != world:
+        raise ValueError(f"{len(handles)} handles for world {world}")
+    return (handles[rank - 1] if rank > 0 else None), (handles[rank + 1] if rank < world - 1 else None)
+
+
 class DistTTCross:
     """A TT-cross problem whose interfaces are partitioned over the ranks of ``group``.
 
     All device work (the library's and NCCL's) is ordered on torch's current CUDA stream.
+
+    ``peer=True`` runs the sweeps (when every rank's superblock clusters fit its device at once;
+    ``self.peer`` says whether they do) as the cross-GPU wavefront (include/ttcross.h,
+    tt_cross_sweep_peer): each rank's superblocks in ONE persistent launch per call, the
+    boundary superblocks exchanging their new records with the neighbour ranks' kernels through
+    CUDA IPC peer memory (Alg. 6 lines 6-8: neighbours only), and one all-gather of
+    the records per call instead of one per sweep.  Needs a device per rank (IPC handles cannot
+    be opened by their own process) with peer access between neighbours.
     """
 
     def __init__(self, family, u, w, rank_cap, tol, n_samples=32, rook_iters=4, seed=0, group=None,
-                 fold_weights=False):
+                 fold_weights=False, peer=False):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -124,9 +140,42 @@ class DistTTCross:
         self.pbuf = torch.as_tensor(pv, device=dev)
         self.pper = pper // 8
         self.d = self.tt.d
+        self.peer = bool(peer) and self.world > 1
+        if self.peer:
+            # every rank's superblocks must be resident at once (the persistent launch)
+            ok = torch.tensor([1 if self.tt.launch_shape()["all_resident"] else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            self.peer = bool(ok.item())
+        if self.peer:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.tt.peer_handles(), group=self.group)
+            left, right = neighbour_handles(handles, self.rank, self.world)
+            self.tt.peer_open(left, right)
+            self._bar = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def _device_barrier(self):
+        """Every rank's work enqueued so far has completed on its device before anything this rank
+        enqueues next runs (a one-element all-reduce on the stream): the neighbours' kernels write
+        into this rank's record buffers, so no rank may start before every reset / commit is done."""
+        dist.all_reduce(self._bar, group=self.group)
+
+    def reset(self):
+        self.tt.reset()
+        if self.peer:
+            self._device_barrier()
 
     def sweep(self, n_sweeps=1):
-        """n_sweeps Alg. 6 sweeps: local superblock updates, all-gather of the records, commit."""
+        """n_sweeps Alg. 6 sweeps: local superblock updates, all-gather of the records, commit
+        (peer: one persistent launch of n_sweeps, the neighbour exchange in peer memory, then one
+        all-gather + commit)."""
+        if self.peer:
+            if n_sweeps < 1:
+                return
+            self.tt.sweep_peer(n_sweeps)
+            allgather_slices(self.xbuf, self.xper, self.group)
+            self.tt.commit()
+            self._device_barrier()
+            return
         for _ in range(n_sweeps):
             self.tt.sweep_local()
             allgather_slices(self.xbuf, self.xper, self.group)
@@ -142,7 +191,7 @@ class DistTTCross:
 
     def solve(self, n_sweeps):
         """reset + n_sweeps sweeps + quadrature; returns (value, log10|value|, sign)."""
-        self.tt.reset()
+        self.reset()
         self.sweep(n_sweeps)
         return self.integrate()
 

@@ -107,3 +107,16 @@ def test_two_process_sweeps_equal_single_process(d, world):
     for _ in range(sweeps):
         st = X.sweep(prob, st)
     assert [p.tolist() for p in st.piv] == got
+
+
+def test_neighbour_handles_chain():
+    """tt_cross_peer_open's contract: rank p gets rank p-1's handles on the left and rank p+1's
+    on the right, None at the ends of the chain (Alg. 6 lines 6-8: neighbours only)."""
+    from paper_1903_11554_b200.dist import neighbour_handles
+    hs = [bytes([p]) * 4 for p in range(4)]
+    assert neighbour_handles(hs, 0, 4) == (None, hs[1])
+    assert neighbour_handles(hs, 2, 4) == (hs[1], hs[3])
+    assert neighbour_handles(hs, 3, 4) == (hs[2], None)
+    assert neighbour_handles(hs[:1], 0, 1) == (None, None)
+    with pytest.raises(ValueError):
+        neighbour_handles(hs, 0, 3)
