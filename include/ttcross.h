@@ -174,9 +174,9 @@ int tt_cross_exchange_buffer(ttc_ctx* ctx, void** dev_ptr, int64_t* bytes_total,
  *   (exchange them with any host collective).  world > 1, else TTC_ERR_STATE.
  * tt_cross_peer_open -- maps the left (rank-1) and right (rank+1) neighbours' handles (as written
  *   by their tt_cross_peer_handles; host pointers, read during the call).  `left` must be NULL
- *   exactly when rank == 0, `right` exactly when rank == world-1 (TTC_ERR_ARG).  Needs every
- *   owned superblock's cluster resident at once (tt_cross_get_launch_shape bit 2), else
- *   TTC_ERR_STATE.  Synchronises the context stream.  Mappings are closed by tt_cross_destroy.
+ *   exactly when rank == 0, `right` exactly when rank == world-1 (TTC_ERR_ARG).  Needs a t-form
+ *   family (TTC_FAMILY_C / D) with every owned superblock's cluster resident at once
+ *   (tt_cross_get_launch_shape bit 2), else TTC_ERR_STATE.  Synchronises the context stream.  Mappings are closed by tt_cross_destroy.
  * tt_cross_sweep_peer -- n_sweeps >= 1 sweeps of the owned superblocks (one persistent launch),
  *   then this rank's records to its slot of the exchange buffer; the caller all-gathers the
  *   exchange buffer (tt_cross_exchange_buffer) and calls tt_cross_commit, which advances the
@@ -286,8 +286,9 @@ int tt_cross_get_kernel_time(ttc_ctx* ctx, int32_t kid, const char** name, int64
 
 /* tt_cross_get_launch_shape -- the k_sweep launch chosen at init: CTAs per superblock cluster,
  * threads per CTA, flags in *cached (bit 0: the rook search keeps its rows/columns in shared
- * memory; bit 1: tt_cross_sweep runs the persistent wavefront launch; bit 2: every owned
- * superblock's cluster is resident at once -- tt_cross_peer_open's condition), and the dynamic shared
+ * memory; bit 1: tt_cross_sweep runs the persistent wavefront launch; bit 2: the cross-GPU
+ * wavefront is available -- a t-form family with every owned superblock's cluster resident at
+ * once, tt_cross_peer_open's condition), and the dynamic shared
  * memory per CTA (bytes).  Any pointer may be NULL. */
 int tt_cross_get_launch_shape(ttc_ctx* ctx, int32_t* cluster, int32_t* threads, int32_t* cached,
                               int64_t* smem_bytes);

@@ -106,7 +106,11 @@ def load(path: str = LIB_PATH):
         "tt_cross_get_loopback": (i32, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and os.environ.get("TTC_LIB_PATH"):
+            continue   # (an older build variant for A/B runs; tests/test_abi.py checks the product library)
+        if fn is None:
+            raise OSError(f"{path}: symbol {name} missing (stale build?)")
         fn.restype = res
         fn.argtypes = args
     _lib = lib

@@ -85,6 +85,8 @@ struct ttc_ctx {
   int fw_ns = 0;               // k_fiber_wsum node ranges per tile override (TTC_FW_NS; 0 = host rule)
   const void* greedy_fn = nullptr;   // k_sweep variant (one sweep)
   const void* sweeps_fn = nullptr;   // k_sweeps variant (persistent, world == 1)
+  const void* sweeps_peer_fn = nullptr;   // its cross-GPU wavefront instantiation (t-form families), or null
+  bool peer_resident = false;        // sweeps_peer_fn's clusters all resident at once
   bool persistent = false;           // k_sweeps usable (all clusters resident)
   bool resident_all = false;         // every owned superblock's cluster resident at once (any world)
   // cross-GPU wavefront (tt_cross_peer_open / tt_cross_sweep_peer)
@@ -305,7 +307,8 @@ int launch_sweeps(ttc_ctx* c, int n) {
   cudaError_t e;
   {
     Timed t(c, K_SWEEP);
-    e = cudaLaunchKernelEx(&lc, (void (*)(DevCtx, int, int))c->sweeps_fn, dc, c->sweeps, n);
+    const bool peer = dc.pdone[0] || dc.pdone[1];   // (tt_cross_peer_open / tt_cross_set_loopback)
+    e = cudaLaunchKernelEx(&lc, (void (*)(DevCtx, int, int))(peer ? c->sweeps_peer_fn : c->sweeps_fn), dc, c->sweeps, n);
   }
   if (e != cudaSuccess) return fail(TTC_ERR_CUDA, std::string("k_sweeps launch: ") + cudaGetErrorString(e));
   return check_launch("k_sweeps");
@@ -758,6 +761,11 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
     allow((const void*)k_sweeps<1, false, 512>, -1);
     allow((const void*)k_sweeps<0, true, 512>, -1);
     allow((const void*)k_sweeps<1, true, 512>, -1);
+    for (const void* f : {(const void*)k_sweeps<0, false, 256, true>, (const void*)k_sweeps<1, false, 256, true>,
+                          (const void*)k_sweeps<0, true, 256, true>, (const void*)k_sweeps<1, true, 256, true>,
+                          (const void*)k_sweeps<0, false, 512, true>, (const void*)k_sweeps<1, false, 512, true>,
+                          (const void*)k_sweeps<0, true, 512, true>, (const void*)k_sweeps<1, true, 512, true>})
+      allow(f, -1);   // (the cross-GPU wavefront instantiations)
     for (const void* f : {(const void*)k_sweep<2, false, 256>, (const void*)k_sweep<2, false, 512>,
                           (const void*)k_sweep<3, false, 256>, (const void*)k_sweep<3, false, 512>,
                           (const void*)k_sweep<4, false, 256>, (const void*)k_sweep<4, false, 512>,
@@ -860,6 +868,18 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
         case TTC_FAMILY_CX: return big ? (const void*)k_sweeps<2, false, 512> : (const void*)k_sweeps<2, false, 256>;
         case TTC_FAMILY_DX: return big ? (const void*)k_sweeps<3, false, 512> : (const void*)k_sweeps<3, false, 256>;
         default: return big ? (const void*)k_sweeps<4, false, 512> : (const void*)k_sweeps<4, false, 256>;
+      }
+    };
+    auto sweeps_peer_for = [&](bool cached) -> const void* {
+      const bool big = T > 256;
+      switch (k.family) {
+        case TTC_FAMILY_C:
+          return big ? (cached ? (const void*)k_sweeps<0, true, 512, true> : (const void*)k_sweeps<0, false, 512, true>)
+                     : (cached ? (const void*)k_sweeps<0, true, 256, true> : (const void*)k_sweeps<0, false, 256, true>);
+        case TTC_FAMILY_D:
+          return big ? (cached ? (const void*)k_sweeps<1, true, 512, true> : (const void*)k_sweeps<1, false, 512, true>)
+                     : (cached ? (const void*)k_sweeps<1, true, 256, true> : (const void*)k_sweeps<1, false, 256, true>);
+        default: return nullptr;   // (x-form families: the per-sweep exchange only)
       }
     };
     // resident clusters for (G, cached)
@@ -989,6 +1009,8 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       c->resident_all = resident_of(c->sweeps_fn, G, cached) >= nj && resident(G, cached) >= nj &&
                         !std::getenv("TTC_NO_PERSISTENT");
       c->persistent = k.world == 1 && c->resident_all;
+      c->sweeps_peer_fn = sweeps_peer_for(cached);
+      c->peer_resident = c->sweeps_peer_fn && resident_of(c->sweeps_peer_fn, G, cached) >= nj && c->resident_all;
     }
   }
   if (dc.tma) {
@@ -1278,7 +1300,7 @@ int tt_cross_get_launch_shape(ttc_ctx* c, int32_t* cluster, int32_t* threads, in
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (cluster) *cluster = c->dc.G;
   if (threads) *threads = c->greedy_threads;
-  if (cached) *cached = (c->greedy_cached ? 1 : 0) | (c->persistent ? 2 : 0) | (c->resident_all ? 4 : 0);
+  if (cached) *cached = (c->greedy_cached ? 1 : 0) | (c->persistent ? 2 : 0) | (c->peer_resident ? 4 : 0);
   if (smem_bytes) *smem_bytes = (int64_t)c->greedy_smem;
   return TTC_OK;
 }
@@ -1353,7 +1375,9 @@ int tt_cross_peer_open(ttc_ctx* c, const void* left, const void* right) {
   if (!c) return fail(TTC_ERR_ARG, "null context");
   if (c->cfg.world < 2) return fail(TTC_ERR_STATE, "tt_cross_peer_open needs world > 1");
   if (c->dc.loopback) return fail(TTC_ERR_STATE, "loopback mode is on");
-  if (!c->resident_all) return fail(TTC_ERR_STATE, "the owned superblocks' clusters are not all resident at once");
+  if (!c->peer_resident)
+    return fail(TTC_ERR_STATE, "no cross-GPU wavefront for this context (x-form family, or the owned superblocks' clusters "
+                               "are not all resident at once)");
   if ((left != nullptr) != (c->cfg.rank > 0) || (right != nullptr) != (c->cfg.rank < c->cfg.world - 1))
     return fail(TTC_ERR_ARG, "a rank needs exactly its existing neighbours' handles (left: rank > 0, right: rank < world-1)");
   if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
@@ -1395,7 +1419,8 @@ int tt_cross_set_loopback(ttc_ctx* c, int32_t boundary) {
   if (c->cfg.world != 1) return fail(TTC_ERR_STATE, "tt_cross_set_loopback needs world == 1");
   const int d = c->dc.d;
   if (boundary != 0 && (boundary < 1 || boundary > d - 2)) return fail(TTC_ERR_ARG, "boundary must be 0 or in [1, d-2]");
-  if (boundary != 0 && !c->persistent) return fail(TTC_ERR_STATE, "loopback needs the persistent sweep launch");
+  if (boundary != 0 && !(c->persistent && c->peer_resident))
+    return fail(TTC_ERR_STATE, "loopback needs the persistent sweep launch of a t-form family");
   if (c->pending) return fail(TTC_ERR_STATE, "uncommitted local sweep");
   if (boundary != 0 && !c->lb_rec) {
     if (int e = dalloc(c, &c->lb_rec, (size_t)c->rec_ints)) return e;

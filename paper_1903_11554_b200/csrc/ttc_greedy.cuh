@@ -1623,7 +1623,7 @@ __device__ __noinline__ void peer_publish(const DevCtx& c, int side, int k, int 
   st_release_sys(&c.pdone[side][k], sweep + 1);
 }
 
-template <int FAMILY, bool CACHED>
+template <int FAMILY, bool CACHED, bool PEER = false>
 __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, GreedySmem& S, double* dyn, int sweep, int job, int r,
                                           int rl, int rr, int* Rn, int& xstep, RingPos& rpos, bool end_sync,
                                           int rows_done, int cols_done, bool xy_known, bool release) {
@@ -1836,8 +1836,8 @@ __device__ __forceinline__ int sweep_body(const DevCtx& c, const DevCtx& cs, Gre
       c.rank_ring[k * 2 + (sweep & 1)] = add ? r + 1 : r;
       st_release(&c.done[k], sweep + 1);  // the record writes above happen-before this release
       // boundary superblocks of a rank: the same to the neighbour rank's copies
-      if (c.pdone[0] && k == c.pb_lo) peer_publish(cs, 0, k, sweep, r, add, Rn);   // (cs: the shared copy -- a
-      if (c.pdone[1] && k + 1 == c.pb_hi) peer_publish(cs, 1, k, sweep, r, add, Rn);   // reference to c would copy it to local memory)
+      if (PEER && c.pdone[0] && k == c.pb_lo) peer_publish(cs, 0, k, sweep, r, add, Rn);   // (cs: the shared copy -- a
+      if (PEER && c.pdone[1] && k + 1 == c.pb_hi) peer_publish(cs, 1, k, sweep, r, add, Rn);   // reference to c would copy it to local memory)
     }
   };
   const bool stage_n = n <= STAGE_N;
@@ -2156,7 +2156,10 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweep(DevCtx c, int 
 // in global memory instead of a grid-wide barrier.  Records are appended in place (slots
 // below a published rank never change).  A wait longer than ~2 s sets flags[1] and abandons
 // the launch (reported as an error), so a scheduling failure cannot hang the device.
-template <int FAMILY, bool CACHED, int THREADS>
+// PEER: the cross-GPU wavefront variant (boundary superblocks exchange through peer memory,
+// DevCtx prec/pring/pdone); a separate instantiation, so the one-GPU kernel carries none of its
+// code (its branches cost the one-GPU kernel ~0.8% on D_20: 14.33 vs 14.22 ms, profiles/r02w_*)
+template <int FAMILY, bool CACHED, int THREADS, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int s0, int nsweeps) {
   __shared__ GreedySmem S;
   __shared__ int s_abort[2];   // by sweep parity: one cluster barrier per sweep start
@@ -2190,7 +2193,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
       const unsigned long long w0 = (TTC_PHASE_CLOCKS && c.phase_ns) ? gtimer() : 0;
       // a neighbour on another rank (cross-GPU wavefront): its flag, written by the peer with a
       // system-scope release, is acquired at system scope from rdone
-      const bool lrem = c.pdone[0] && k == c.pb_lo, rrem = c.pdone[1] && k + 1 == c.pb_hi;
+      const bool lrem = PEER && c.pdone[0] && k == c.pb_lo, rrem = PEER && c.pdone[1] && k + 1 == c.pb_hi;
       if (k > 0)
         while ((lrem ? ld_acquire_sys(&c.rdone[k - 1]) : ld_acquire(&c.done[k - 1])) < s &&
                !(abort = (clock64() - t0 > (1LL << 32)) || c.flags[1])) {
@@ -2218,11 +2221,11 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) k_sweeps(DevCtx c, int
         break;
       }
     }
-    const bool lrem = c.pdone[0] && k == c.pb_lo, rrem = c.pdone[1] && k + 1 == c.pb_hi;
+    const bool lrem = PEER && c.pdone[0] && k == c.pb_lo, rrem = PEER && c.pdone[1] && k + 1 == c.pb_hi;
     const int rl = k > 0 ? (lrem ? c.rring : c.rank_ring)[(k - 1) * 2 + ((s - 1) & 1)] : 1;
     const int rr = k < d - 2 ? (rrem ? c.rring : c.rank_ring)[(k + 1) * 2 + ((s - 1) & 1)] : 1;
     // (sweep_body publishes rank_ring[k] and releases done[k] as soon as the pivot is known)
-    r = sweep_body<FAMILY, CACHED>(c, s_ctx, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
+    r = sweep_body<FAMILY, CACHED, PEER>(c, s_ctx, S, dyn, s, job, r, rl, rr, Rk, xstep, rpos, s + 1 == s0 + nsweeps, rdone, cdone,
                                    s > s0, true);
     rdone = rl;   // (= the sbstate the sweep wrote)
     cdone = rr;

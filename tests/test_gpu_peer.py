@@ -87,8 +87,8 @@ def test_loopback_workloads_one_launch(lib, name, b):
     u, w = wl.grid()
     kw = dict(n_samples=wl.n_samples, rook_iters=wl.rook_iters, seed=wl.seed)
     ref = TTCross(wl.family, u, w, wl.rank_cap, wl.tol, **kw)
-    if not ref.launch_shape()["persistent"]:
-        pytest.skip("no persistent launch for this shape")
+    shape = ref.launch_shape()
+    assert shape["persistent"] and shape["all_resident"], "the BASELINE configs run the (cross-GPU) wavefront"
     rs, rv = _solve(ref, wl.alg6_sweeps, False)
     tt = TTCross(wl.family, u, w, wl.rank_cap, wl.tol, **kw)
     tt.set_loopback(b)
