@@ -514,16 +514,20 @@ __global__ void __launch_bounds__(512) k_solve(DevCtx c) {
     // the step's multipliers once per row (not once per updated element)
     for (int q = threadIdx.x; q < nr; q += blockDim.x) lmul[q] = dd_mul(A[perm[k + 1 + q] * cap + k], inv);
     __syncthreads();
-    for (int t = threadIdx.x; t < nr * width; t += blockDim.x) {
-      const int q = t / width, colx = t - q * width;
-      const int row = perm[k + 1 + q];
-      const DD l = lmul[q];
-      if (colx < nr) {
-        const int col = k + 1 + colx;
-        A[row * cap + col] = dd_sub(A[row * cap + col], dd_mul(l, A[pk * cap + col]));
-      } else {
-        const int col = colx - nr;
-        Bm[row * cap + col] = dd_sub(Bm[row * cap + col], dd_mul(l, Bm[pk * cap + col]));
+    // a thread keeps one column and steps over the rows (no integer division per element: the
+    // 512 threads as qs row lanes x width columns, the last partial row lane idle); the pivot
+    // row's entry of the column is loaded once
+    if (nr > 0) {
+      const int qs = blockDim.x / width, colx = threadIdx.x % width, q0 = threadIdx.x / width;
+      if (q0 < qs) {
+        const bool inA = colx < nr;
+        DD* base = inA ? A + k + 1 + colx : Bm + (colx - nr);
+        const DD pv = base[pk * cap];
+#pragma unroll 2
+        for (int q = q0; q < nr; q += qs) {
+          DD* e = base + perm[k + 1 + q] * cap;
+          *e = dd_sub(*e, dd_mul(lmul[q], pv));
+        }
       }
     }
     __syncthreads();
@@ -532,14 +536,19 @@ __global__ void __launch_bounds__(512) k_solve(DevCtx c) {
   for (int k = r - 1; k >= 0; --k) {
     const int pk = perm[k];
     const DD dk = dinv[k];
-    for (int t = threadIdx.x; t < (k + 1) * nc; t += blockDim.x) {
-      const int q = t / nc, col = t - q * nc;   // q == k: write X[k]; q < k: update row q
-      const DD xk = dd_mul(Bm[pk * cap + col], dk);
-      if (q == k) {
-        H[(long long)k * cap + c0 + col] = xk;
-      } else {
-        const int pq = perm[q];
-        Bm[pq * cap + col] = dd_sub(Bm[pq * cap + col], dd_mul(A[pq * cap + k], xk));
+    // a thread keeps one column, rows q0, q0 + qs, ... (q == k: write X[k]; q < k: update row q)
+    {
+      const int qs = blockDim.x / nc, col = threadIdx.x % nc, q0 = threadIdx.x / nc;
+      if (q0 < qs) {
+        const DD xk = dd_mul(Bm[pk * cap + col], dk);
+        for (int q = q0; q <= k; q += qs) {
+          if (q == k) {
+            H[(long long)k * cap + c0 + col] = xk;
+          } else {
+            const int pq = perm[q];
+            Bm[pq * cap + col] = dd_sub(Bm[pq * cap + col], dd_mul(A[pq * cap + k], xk));
+          }
+        }
       }
     }
     __syncthreads();
