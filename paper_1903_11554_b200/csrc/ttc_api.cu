@@ -1023,7 +1023,6 @@ int tt_cross_init(ttc_ctx** out, const ttc_config* cfg, const double* nodes_u, c
       return bail(fail(TTC_ERR_CUDA, "cuTensorMapEncodeTiled: driver entry point not found"));
     auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     CUtensorMap maps[2];
-    const int T = c->greedy_threads;
     const cuuint32_t bw = 32;   // a warp's rows (TmaRing: one ring per warp)
     const cuuint64_t dims[2] = {(cuuint64_t)dc.sbn, (cuuint64_t)nj * cap};
     const cuuint64_t strides[1] = {(cuuint64_t)dc.sbn * sizeof(double)};

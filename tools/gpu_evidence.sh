@@ -1,6 +1,7 @@
 # round evidence: full GPU tests, default bench (D_20) + C_200 + D_5, launch list and one
-# ncu --set full capture of k_sweeps (D_20) and of the fiber kernel: tools/gpu_evidence.sh <tag>
+# ncu --set full capture of k_sweeps (D_20) and of the fiber kernel, smoke(): tools/gpu_evidence.sh <tag>
 mkdir -p gpurun_out; tag=$1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${tag}_smoke.log
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
 timeout 600 python bench.py > gpurun_out/${tag}_bench_d20.jsonl 2> gpurun_out/${tag}_bench_d20.err
 timeout 600 python bench.py --workload C200 --no-cpu-baseline > gpurun_out/${tag}_bench_c200.jsonl 2>&1

@@ -62,6 +62,10 @@ def main():
     if "--headers" in sys.argv:
         print("# columns:", hdr)
     data = rows[2:]
+    for i, r in enumerate(data):   # (a report may print the kernel's page more than once)
+        if r and r[0] == "Kernel Name":
+            data = data[:i]
+            break
     base = int(data[0][ia], 16)
     table = line_table(so, kernel)
     by_line = collections.defaultdict(lambda: [0, 0, 0])
